@@ -1,0 +1,234 @@
+/*
+ * spc.h — C ABI of libspc: the per-decode-step retrieval + sparse-attention
+ * hot path of SpeContext (arXiv 2512.00722), hand-written for sm_100a (B200).
+ *
+ * Citation keys: P:n = PAPER.md line n (the paper's LaTeX source);
+ * "O<n>" = the arithmetic contract in DESIGN.md §3 (the written, bit-level
+ * definition that both this library and the independent CPU oracle follow).
+ *
+ * Conventions (apply to every call below)
+ * ---------------------------------------
+ *  - extern "C", stateless, reentrant.  Every compute call only ENQUEUES work on
+ *    `stream` (a cudaStream_t passed as void*; NULL = legacy default stream).
+ *    No call synchronises the host, allocates memory or keeps state between
+ *    calls.  The caller owns the rolling state (previous selection, slot map).
+ *  - All tensors are caller-owned, dense, row-major with the innermost
+ *    dimension last, and must stay valid until the enqueued work completes.
+ *    Pointers are DEVICE pointers unless stated; a KV source for
+ *    spc_gather_kv / spc_sparse_decode_attn may also be mapped pinned host
+ *    memory (cudaHostAlloc(..., cudaHostAllocMapped) or cudaHostRegister with
+ *    the device alias), read zero-copy over PCIe.
+ *  - bf16 tensors are passed as raw 16-bit words (IEEE bfloat16 bit pattern).
+ *  - Errors: host-checkable argument errors are reported as a spc_status
+ *    BEFORE anything is enqueued (nothing aborts, nothing throws across the
+ *    ABI).  Data-dependent contract violations (unsorted index lists, index >=
+ *    seq_len, slot map inconsistent with the previous set) are undefined
+ *    behaviour unless stated.  SPC_E_CUDA means a CUDA launch error; its text
+ *    is available from spc_last_cuda_error().
+ *  - Index lists are int32, ascending, padded with -1 after `count` entries.
+ */
+#ifndef SPC_H_
+#define SPC_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef void* spc_stream_t; /* a cudaStream_t */
+
+typedef enum { SPC_BF16 = 0, SPC_F32 = 1 } spc_dtype;
+
+typedef enum {
+  SPC_OK = 0,
+  SPC_E_NULL = 1,        /* a required pointer is NULL                              */
+  SPC_E_SHAPE = 2,       /* Hq % G != 0, D not in {64,128}, k < 1, sizes <= 0 ...  */
+  SPC_E_BUDGET = 3,      /* k larger than the supported maximum (SPC_MAX_K)          */
+  SPC_E_RANGE = 4,       /* a host-checkable index/range argument is out of range    */
+  SPC_E_STATE = 5,       /* reserved: slot map inconsistent with previous set        */
+  SPC_E_WORKSPACE = 6,   /* ws NULL or ws_bytes smaller than the *_workspace() value */
+  SPC_E_UNSUPPORTED = 7, /* dtype / alpha / head-dim combination not compiled in     */
+  SPC_E_CUDA = 8         /* CUDA launch error, see spc_last_cuda_error()             */
+} spc_status;
+
+enum { SPC_MAX_K = 4096 };      /* largest supported budget k                       */
+enum { SPC_MAX_SEQ = 1 << 23 }; /* O4's fixed-point sum is exact for S < 2^23       */
+
+const char* spc_status_string(int status);
+const char* spc_last_cuda_error(void);
+int spc_version(void);
+/* Number of kernels this library has launched since it was loaded (all
+ * threads).  Used by bench.py to report how many of its own kernels ran. */
+uint64_t spc_launch_count(void);
+
+/* ------------------------------------------------------------------------
+ * spc_score — retrieval-head scoring, O1..O6.
+ *
+ * Paper: Eq.1 attn_weight = softmax(Q K^T / sqrt(d)) of the
+ * retrieval head over every cached retrieval key ("matrix
+ * multiplication of Query ... with Keys_candidate to get the importance
+ * scores"; "maintains a full Key (K) cache and calculates attention
+ * weights"); GQA mapping P:328: "element-wise maximum ... within the same
+ * group of heads ... to generate the group-level attention weights"
+ * (MQA P:331 = one group; MHA = alpha 1).
+ *
+ * Query head h belongs to KV group g = h / alpha, alpha = Hq / G (DESIGN.md
+ * reading R4).  For request b only tokens t < seq_len[b] exist.
+ *
+ * Phases (bit flags, so a context-sharded caller can all-reduce between them):
+ *   SPC_SCORE_LOGITS: logits[b][h][t] = fl(dot_seq(q[b][h], kr[b][g][t]) * scale)
+ *                     (O1: fp32 fma chain over d ascending, then one RN mul);
+ *                     head_max[b][h] = max_t logits (O2).          (overwrites)
+ *   SPC_SCORE_NORM:   head_sumfix[b][h] = sum_t trunc(spc_exp(s - m) * 2^40)
+ *                     as exact int64 (O3, O4); m = head_max (input). (overwrites)
+ *   SPC_SCORE_GROUP:  group_score[b][g][t] = max_{j<alpha} fl(spc_exp(s - m) * r)
+ *                     with r = 1 / fl((float)F * 2^-40) (O4..O6).  Entries
+ *                     t >= seq_len[b] are written as 0.
+ *
+ * q           [B][Hq][D]     bf16      retrieval-head query of this step
+ * kr          [B][G][Smax][D] bf16     retrieval-head key cache
+ * seq_len     [B]            int32, DEVICE; 1 <= seq_len[b] <= Smax
+ * logits      [B][Hq][Smax]  f32       out (LOGITS) / in (NORM, GROUP)
+ * head_max    [B][Hq]        f32       out (LOGITS) / in (NORM, GROUP)
+ * head_sumfix [B][Hq]        int64     out (NORM)   / in (GROUP)
+ * group_score [B][G][Smax]   f32       out (GROUP); may be NULL otherwise
+ * ws          >= spc_score_workspace(B, Hq, Smax) bytes of device scratch
+ * Supported: dtype SPC_BF16; D in {64, 128}; alpha in {1, 2, 4, 8};
+ * Smax < SPC_MAX_SEQ.
+ * ---------------------------------------------------------------------- */
+enum { SPC_SCORE_LOGITS = 1, SPC_SCORE_NORM = 2, SPC_SCORE_GROUP = 4, SPC_SCORE_ALL = 7 };
+size_t spc_score_workspace(int B, int Hq, int Smax);
+int spc_score(int dtype, const void* q, const void* kr, const int32_t* seq_len, int B, int Hq, int G,
+              int D, int Smax, float scale, int phases, float* logits, float* head_max,
+              int64_t* head_sumfix, float* group_score, void* ws, size_t ws_bytes,
+              spc_stream_t stream);
+
+/* ------------------------------------------------------------------------
+ * spc_topk — per-(b,g) top-k selection, O7.
+ *
+ * Paper: "select the Top-K candidates"; head-level (per KV group)
+ * retrieval; budget k = 2048.  The selection is the
+ * first n = min(k, len) positions under the total order
+ *     (value descending, global id ascending)         (reading R8)
+ * emitted ASCENDING by position, -1 padded; len = min(seq_len[b], n_cols).
+ * The global id of position p is p*id_stride + id_offset (single device:
+ * stride 1, offset 0; context shard r of P: stride P, offset r).  Because
+ * that map is increasing, ties among one shard's positions break by position.
+ * force_last != 0 treats position len-1 as +inf (R10: the newest token is
+ * always selected); its out_val is +inf.
+ *
+ * val        [B][G][n_cols] f32 >= 0 (a group_score)
+ * seq_len    [B] int32 DEVICE
+ * out_idx    [B][G][k] int32 out: selected positions, ascending, -1 padded
+ * out_val    [B][G][k] f32 out or NULL: value at each selected position
+ * out_count  [B][G] int32 out: min(k, len)
+ * out_thresh [B][G] uint64 out or NULL: composite key of the LAST selected
+ *            element in the total order, (bits(value) << 32) | ~uint32(id);
+ *            0 when nothing is selected.
+ * ws         >= spc_topk_workspace(B, G, n_cols, k) bytes
+ * Supported: 1 <= k <= SPC_MAX_K, n_cols < SPC_MAX_SEQ.
+ * ---------------------------------------------------------------------- */
+size_t spc_topk_workspace(int B, int G, int n_cols, int k);
+int spc_topk(const float* val, const int32_t* seq_len, int B, int G, int n_cols, int k, int force_last,
+             int id_stride, int id_offset, int32_t* out_idx, float* out_val, int32_t* out_count,
+             uint64_t* out_thresh, void* ws, size_t ws_bytes, spc_stream_t stream);
+
+/* spc_topk_merge — global threshold from P shards' local top-k lists (O13).
+ * cand_val/cand_pos [P][R][k], cand_count [P][R] (R = B*G rows) as produced by
+ * spc_topk on shard p with id_stride P, id_offset p; global id = pos*P + p.
+ * out_thresh [R]: composite key of the k-th element of the union in the O7
+ * order (0 if the union has fewer than k elements: everything is kept).
+ * ws >= spc_topk_merge_workspace(P, R, k). */
+size_t spc_topk_merge_workspace(int P, int R, int k);
+int spc_topk_merge(const float* cand_val, const int32_t* cand_pos, const int32_t* cand_count, int P,
+                   int R, int k, uint64_t* out_thresh, void* ws, size_t ws_bytes,
+                   spc_stream_t stream);
+
+/* spc_topk_filter — keep, in place and in order, the entries of an ascending
+ * list whose composite key (bits(val) << 32 | ~uint32(pos*id_stride+id_offset))
+ * is >= thresh[r]; pads with -1 and rewrites count.  idx/val [R][k],
+ * count [R], thresh [R]. */
+int spc_topk_filter(int32_t* idx, const float* val, int32_t* count, const uint64_t* thresh, int R,
+                    int k, int id_stride, int id_offset, spc_stream_t stream);
+
+/* ------------------------------------------------------------------------
+ * spc_elastic_diff — elastic loading set difference, O8.
+ *
+ * Paper §5.4: evict S_last - S_now, load S_now - S_last
+ * ("S_pre" read as S_last, reading R12), fixed budget, in-place update of
+ * the GPU-resident KV through Tensor.copy_().
+ *
+ * prev_idx/cur_idx [B][G][k] ascending lists with counts prev_count/cur_count
+ * [B][G] (prev_count may be 0: first step).
+ *   load_tok  [B][G][k] out: cur \ prev, ascending, -1 padded; n_load [B][G].
+ *   evict_tok [B][G][k] out or NULL: prev \ cur, ascending; n_evict or NULL.
+ * Slot bookkeeping (SLOTS mode; slot_tok != NULL), reading R13:
+ *   slot_tok [B][G][k] in/out: token resident in each slot, -1 = empty.
+ *   Freed slots = slots whose token is -1 or not in cur, ascending by slot;
+ *   new token i (ascending) goes to freed slot i: load_slot[i] = freed[i],
+ *   slot_tok[freed[i]] = load_tok[i].  Kept slots never move.  The caller
+ *   guarantees the non-empty slot tokens equal prev (then #new <= #freed).
+ *   load_slot [B][G][k] out (required iff slot_tok != NULL).
+ * ---------------------------------------------------------------------- */
+int spc_elastic_diff(const int32_t* prev_idx, const int32_t* prev_count, const int32_t* cur_idx,
+                     const int32_t* cur_count, int B, int G, int k, int32_t* slot_tok,
+                     int32_t* load_tok, int32_t* load_slot, int32_t* n_load, int32_t* evict_tok,
+                     int32_t* n_evict, spc_stream_t stream);
+
+/* ------------------------------------------------------------------------
+ * spc_gather_kv — elastic load of newly selected KV rows into budget slots, O9.
+ *
+ * Paper: P:374 in-place copy_ of the rows S_now - S_last; P:350 prefetch on
+ * separate CUDA streams; source may be CPU DRAM.
+ * For every layer l in [layer_begin, layer_end), every (b,g), i < n_load[b][g]:
+ *   k_buf[l][b][g][load_slot[i]][:] = k_src[l][b][g][load_tok[i]][:]   (same for v)
+ * k_src/v_src: DEVICE arrays of L pointers, one per layer, each to
+ *   [B][G][Smax][D] (device memory or mapped pinned host memory).
+ * k_buf/v_buf: DEVICE arrays of L pointers, each to [B][G][k][D] (device).
+ * ---------------------------------------------------------------------- */
+int spc_gather_kv(int dtype, const void* const* k_src, const void* const* v_src, int L, int B, int G,
+                  int D, int Smax, int k, int layer_begin, int layer_end, const int32_t* load_tok,
+                  const int32_t* load_slot, const int32_t* n_load, void* const* k_buf,
+                  void* const* v_buf, spc_stream_t stream);
+
+/* ------------------------------------------------------------------------
+ * spc_sparse_decode_attn — GQA decode attention over the selected rows, O10.
+ *
+ * Paper: Eq.1 softmax(QK^T/sqrt(d)) V restricted to the selected tokens,
+ * mapped to the LLM's KV heads (P:324 torch.gather, P:328 GQA group sets);
+ * renormalised over the subset (reading R15).
+ * For every layer l in [layer_begin, layer_end), request b, query head h
+ * (group g = h / alpha):
+ *   J = the selected rows of (b, g);  z_j = scale * <q[l][b][h], K_j>
+ *   out[l][b][h][:] = sum_j softmax(z)_j V_j ;  lse[l][b][h] = log sum_j e^{z_j}
+ * kv_mode SPC_KV_INDEXED: k_layers/v_layers[l] -> [B][G][rows][D] full cache,
+ *   J = idx[b][g][0 .. count[b][g]) (positions < rows).
+ * kv_mode SPC_KV_SLOTS:   k_layers/v_layers[l] -> [B][G][rows][D] budget
+ *   buffers (rows = k), J = slots 0 .. count[b][g]) ; idx ignored (may be NULL).
+ * k_layers/v_layers: DEVICE arrays of L pointers (device or mapped host).
+ * q [L][B][Hq][D] (dtype), out [L][B][Hq][D] f32, lse [L][B][Hq] f32 or NULL.
+ * A (b,g) with count 0 yields out = 0, lse = -inf.
+ * ws >= spc_attn_workspace(L, B, Hq, D, k) bytes.
+ * Supported: dtype SPC_BF16 or SPC_F32; D in {64, 128}; alpha in {1,2,4,8}.
+ * ---------------------------------------------------------------------- */
+enum { SPC_KV_INDEXED = 0, SPC_KV_SLOTS = 1 };
+size_t spc_attn_workspace(int L, int B, int Hq, int D, int k);
+int spc_sparse_decode_attn(int dtype, const void* q, const void* const* k_layers,
+                           const void* const* v_layers, int kv_mode, const int32_t* idx,
+                           const int32_t* count, int L, int layer_begin, int layer_end, int B, int Hq,
+                           int G, int D, int rows, int k, float scale, float* out, float* lse,
+                           void* ws, size_t ws_bytes, spc_stream_t stream);
+
+/* spc_attn_merge — log-sum-exp merge of P partial attentions, O12.
+ * o_parts [P][n][D] f32, lse_parts [P][n] f32 (-inf = empty part);
+ * out [n][D] = sum_p e^{lse_p - M} o_p / sum_p e^{lse_p - M}, M = max_p lse_p;
+ * lse_out [n] (or NULL) = M + log sum_p e^{lse_p - M}. */
+int spc_attn_merge(const float* o_parts, const float* lse_parts, int P, int n, int D, float* out,
+                   float* lse_out, spc_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPC_H_ */

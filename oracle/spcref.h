@@ -1,0 +1,79 @@
+/*
+ * spcref.h — CPU ORACLE for the SpeContext retrieval + sparse-attention hot
+ * path.  TEST INFRASTRUCTURE ONLY: only tests/, __graft_entry__.smoke() and
+ * bench.py's cpu_baseline / --impl reference legs may load it.  The product
+ * path (libspc, paper_2512_00722_b200) never links, imports or calls it.
+ *
+ * It shares no code, header, constant table or helper with the CUDA path:
+ * every definition here is written from PAPER.md and the arithmetic contract
+ * in DESIGN.md §3 (O1..O13).  Plain, slow, single-threaded C.
+ *
+ * bf16 values are passed as uint16_t bit patterns.
+ */
+#ifndef SPCREF_H_
+#define SPCREF_H_
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* O3: the contract's exponential for x <= 0. */
+float spcref_exp(float x);
+
+/* Max |spcref_exp(x) - exp(x)| in ulps of the float result, over every float
+ * x whose bit pattern lies in [lo_bits, hi_bits] (negative floats: sign bit
+ * set; pass lo_bits <= hi_bits as unsigned ranges).  Also counts results that
+ * are not finite or are subnormal.  Used by the pin tests (exhaustive sweep). */
+double spcref_exp_max_ulp(uint32_t lo_bits, uint32_t hi_bits, uint64_t* n_subnormal);
+
+/* O1 + O2 (phase LOGITS).  logits [B][Hq][Smax], head_max [B][Hq]. */
+void spcref_logits(const uint16_t* q, const uint16_t* kr, const int32_t* seq_len, int B, int Hq,
+                   int G, int D, int Smax, float scale, float* logits, float* head_max);
+/* O3 + O4 (phase NORM).  head_sumfix [B][Hq]. */
+void spcref_norm(const float* logits, const float* head_max, const int32_t* seq_len, int B, int Hq,
+                 int Smax, int64_t* head_sumfix);
+/* O3..O6 (phase GROUP).  group_score [B][G][Smax]; t >= seq_len[b] -> 0. */
+void spcref_group(const float* logits, const float* head_max, const int64_t* head_sumfix,
+                  const int32_t* seq_len, int B, int Hq, int G, int Smax, float* group_score);
+
+/* The fp64 mathematical definition (Eq.1 + P:328) used to check that the
+ * determinised contract is faithful: gs[b][g][t] = max_h exp(s_h(t) - LSE_h)
+ * with s in fp64 and scale applied in fp64. */
+void spcref_group_score_f64(const uint16_t* q, const uint16_t* kr, const int32_t* seq_len, int B,
+                            int Hq, int G, int D, int Smax, double scale, double* group_score);
+
+/* O7: top-k of one row by (value desc, id asc), ids = pos*id_stride +
+ * id_offset (or cand_id[pos] when cand_id != NULL); force_pos >= 0 makes that
+ * position +inf.  Writes min(k, n) selected POSITIONS ascending into out_pos,
+ * their values into out_val (may be NULL); returns the count.  *out_thresh
+ * (may be NULL) = composite key of the last selected element, 0 if none. */
+int spcref_topk_row(const float* val, const int32_t* cand_id, int n, int k, int force_pos,
+                    int id_stride, int id_offset, int32_t* out_pos, float* out_val,
+                    uint64_t* out_thresh);
+
+/* Composite key of O7's total order: larger = earlier. */
+uint64_t spcref_composite(float value, int32_t id);
+
+/* O8: elastic diff of one (b,g) row.  slot_tok may be NULL (INDEXED mode);
+ * load_slot required iff slot_tok != NULL.  Returns 0, or -1 if the slot map
+ * is inconsistent with prev (state error) or a new token has no free slot. */
+int spcref_elastic_diff_row(const int32_t* prev, int n_prev, const int32_t* cur, int n_cur, int k,
+                            int32_t* slot_tok, int32_t* load_tok, int32_t* load_slot, int* n_load,
+                            int32_t* evict_tok, int* n_evict);
+
+/* O10: attention of ONE query head over the rows listed in rows[0..n) of a
+ * [n_rows_total][D] key/value block, everything in fp64.  is_bf16 selects the
+ * element type of q/k/v (uint16 bf16 bits or float).  out [D]; returns lse
+ * (natural log), -inf and out = 0 for n == 0. */
+double spcref_attn_head(const void* q, const void* k, const void* v, int is_bf16, const int32_t* rows,
+                        int n, int D, double scale, double* out);
+
+/* O12: merge P partials (o [P][D], lse [P]) -> out [D]; returns lse. */
+double spcref_attn_merge_row(const double* o_parts, const double* lse_parts, int P, int D,
+                             double* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif
