@@ -125,8 +125,9 @@ int spc_score(int dtype, const void* q, const void* kr, const int32_t* seq_len, 
  * out_val    [B][G][k] f32 out or NULL: value at each selected position
  * out_count  [B][G] int32 out: min(k, len)
  * out_thresh [B][G] uint64 out or NULL: composite key of the LAST selected
- *            element in the total order, (bits(value) << 32) | ~uint32(id);
- *            0 when nothing is selected.
+ *            element in the total order, (bits(value) << 32) | ~uint32(id),
+ *            when len > k (a real cut); 0 when every valid element is kept.
+ *            The selection is exactly {positions whose composite >= thresh}.
  * ws         >= spc_topk_workspace(B, G, n_cols, k) bytes
  * Supported: 1 <= k <= SPC_MAX_K, n_cols < SPC_MAX_SEQ.
  * ---------------------------------------------------------------------- */

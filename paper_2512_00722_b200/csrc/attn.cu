@@ -1,0 +1,464 @@
+// attn.cu — spc_sparse_decode_attn (O10) and spc_attn_merge (O12).
+//
+// Paper: the LLM's attention Eq.1 restricted to the tokens the
+// retrieval head selected, mapped per KV head (P:324 torch.gather; GQA group
+// sets P:328), renormalised over the subset (reading R15).
+//
+// Split-K flash-decode.  Work item = (layer, request b, KV group g, chunk of
+// 128 selected rows).  The selected K and V rows (256 B each for d = 128 bf16)
+// are gathered straight from the full cache by per-row cp.async.bulk copies
+// (INDEXED) or read from the budget slots (SLOTS) into padded shared rows; no
+// compacted copy is materialised in HBM.  All alpha query heads of the group
+// share each K/V row (GQA: one read of the row serves alpha heads).
+//
+// bf16 path: the contraction [alpha x D]·[D x rows] and [alpha x rows]·[rows x D]
+// runs on mma.sync m16n8k16 (heads padded to 16 rows of the A operand; the
+// score accumulator fragments are re-used as the A operand of P·V, P split
+// into bf16 hi + lo so P keeps ~16 mantissa bits).  The kernel is HBM-bound;
+// the tensor cores only remove the FMA/shuffle instruction load.
+// fp32 path: CUDA-core dot products (used for the 1e-5 tolerance tests).
+//
+// Each CTA writes (m, l, o) partials; the last CTA of a (layer, b, g) merges
+// them with the log-sum-exp rule (O12).
+#include "common.cuh"
+
+namespace spc {
+namespace {
+
+constexpr int AT_ROWS = 128;   // selected rows per CTA
+constexpr int AT_THREADS = 128;
+constexpr float LOG2E = 1.4426950408889634f;
+constexpr float LN2 = 0.6931471805599453f;
+
+struct AttnWs {
+  float* part_o;   // [L][B][Hq][nsplit][D]  (unnormalised o relative to m)
+  float* part_ml;  // [L][B][Hq][nsplit][2]  (m in log2 units, l)
+  unsigned* cnt;   // [L][B][G]
+  size_t bytes;
+};
+AttnWs attn_ws_layout(void* ws, int L, int B, int Hq, int D, int k) {
+  const size_t ns = (k + AT_ROWS - 1) / AT_ROWS;
+  uint8_t* p = (uint8_t*)ws;
+  AttnWs w;
+  size_t off = 0;
+  w.part_o = (float*)(p + off);
+  off = align_up(off + sizeof(float) * (size_t)L * B * Hq * ns * D, 256);
+  w.part_ml = (float*)(p + off);
+  off = align_up(off + sizeof(float) * 2 * (size_t)L * B * Hq * ns, 256);
+  w.cnt = (unsigned*)(p + off);
+  off = align_up(off + sizeof(unsigned) * (size_t)L * B * Hq, 256);
+  w.bytes = off;
+  return w;
+}
+
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2,
+                                        uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2,
+                                          uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(addr));
+}
+// D = A(16x16 bf16, row) * B(16x8 bf16, col) + D, fp32 accumulate; a1 = a3 = 0.
+__device__ __forceinline__ void mma_bf16(float (&c)[4], uint32_t a0, uint32_t a2, uint32_t b0,
+                                         uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, "
+      "{%8, %9}, {%0, %1, %2, %3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a0), "r"(0u), "r"(a2), "r"(0u), "r"(b0), "r"(b1));
+}
+
+// Merge the nsplit partials of one (layer, b, g) with the LSE rule (O12); run by
+// the last CTA of the group.  m is in log2 units.
+template <int D, int ALPHA>
+__device__ void merge_partials(const float* part_o, const float* part_ml, int nsplit,
+                               size_t head_base /* (lr*B + b)*Hq + g*ALPHA */, float* out,
+                               float* lse, size_t out_head_base) {
+  for (int i = threadIdx.x; i < ALPHA * D; i += blockDim.x) {
+    const int j = i / D, d = i % D;
+    const size_t h = head_base + j;
+    const float* ml = part_ml + h * nsplit * 2;
+    float M = -INFINITY;
+    for (int s = 0; s < nsplit; ++s) M = fmaxf(M, __ldcg(ml + 2 * s));
+    float den = 0.f, num = 0.f;
+    if (M != -INFINITY) {
+      for (int s = 0; s < nsplit; ++s) {
+        const float m = __ldcg(ml + 2 * s);
+        if (m == -INFINITY) continue;
+        const float w = exp2f(m - M);
+        den += w * __ldcg(ml + 2 * s + 1);
+        num += w * __ldcg(part_o + (h * nsplit + s) * D + d);
+      }
+    }
+    out[(out_head_base + j) * D + d] = den > 0.f ? num / den : 0.f;
+    if (lse && d == 0) lse[out_head_base + j] = den > 0.f ? (M + log2f(den)) * LN2 : -INFINITY;
+  }
+}
+
+// ---------------------------------------------------------------- bf16 / mma path
+template <int D, int ALPHA>
+__global__ void __launch_bounds__(AT_THREADS) attn_bf16_kernel(
+    const uint16_t* __restrict__ q, const void* const* __restrict__ k_layers,
+    const void* const* __restrict__ v_layers, int kv_mode, const int32_t* __restrict__ idx,
+    const int32_t* __restrict__ count, int layer_begin, int B, int G, int rows, int kbud,
+    float scale, int nsplit, float* __restrict__ part_o, float* __restrict__ part_ml,
+    unsigned* __restrict__ cnt, float* __restrict__ out, float* __restrict__ lse) {
+  constexpr int RS = D + 8;  // padded row stride in bf16 elements (conflict-free ldmatrix)
+  constexpr int Hq_ = ALPHA;
+  extern __shared__ __align__(128) uint8_t at_smem[];
+  uint16_t* Ks = (uint16_t*)at_smem;                   // [AT_ROWS][RS]
+  uint16_t* Vs = (uint16_t*)at_smem + AT_ROWS * RS;    // [AT_ROWS][RS]
+  float(*red_o)[ALPHA][D] = (float(*)[ALPHA][D])at_smem;  // aliases Ks once QK is done
+  __shared__ __align__(8) uint64_t bar[2];
+  __shared__ float red_m[4][8], red_l[4][8];
+  __shared__ int flag;
+  static_assert(sizeof(float) * 4 * ALPHA * D <= sizeof(uint16_t) * AT_ROWS * RS, "red_o alias");
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int gid = lane >> 2, tig = lane & 3;
+  const int split = blockIdx.x, bg = blockIdx.y, lr = blockIdx.z;
+  const int l = layer_begin + lr;
+  const int b = bg / G, g = bg % G;
+  const int Hq = G * ALPHA;
+  const int n_sel = min(count[bg], kbud);
+  const int r0 = split * AT_ROWS;
+  const int nrows = max(0, min(AT_ROWS, n_sel - r0));
+  const size_t head_base = ((size_t)lr * B + b) * Hq + g * ALPHA;
+
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (nrows > 0) {
+    const uint16_t* Kl = (const uint16_t*)k_layers[l] + (size_t)bg * rows * D;
+    const uint16_t* Vl = (const uint16_t*)v_layers[l] + (size_t)bg * rows * D;
+    if (tid < nrows) {
+      const int tok = kv_mode == SPC_KV_INDEXED ? idx[(size_t)bg * kbud + r0 + tid] : r0 + tid;
+      bulk_g2s(Ks + tid * RS, Kl + (size_t)tok * D, D * 2, &bar[0]);
+      bulk_g2s(Vs + tid * RS, Vl + (size_t)tok * D, D * 2, &bar[1]);
+    } else {
+      uint4 z = make_uint4(0, 0, 0, 0);
+#pragma unroll
+      for (int i = 0; i < D / 8; ++i) {
+        *(uint4*)(Ks + tid * RS + i * 8) = z;
+        *(uint4*)(Vs + tid * RS + i * 8) = z;
+      }
+    }
+    if (tid == 0) {
+      mbar_arrive_expect_tx(&bar[0], nrows * D * 2);
+      mbar_arrive_expect_tx(&bar[1], nrows * D * 2);
+    }
+  }
+  // query fragments (A operand): row = head gid (< ALPHA real), k = d
+  constexpr int KS = D / 16;
+  uint32_t qa0[KS], qa2[KS];
+  {
+    const uint16_t* qh = q + (((size_t)l * B + b) * Hq + g * ALPHA + (gid < ALPHA ? gid : 0)) * D;
+#pragma unroll
+    for (int s = 0; s < KS; ++s) {
+      const uint32_t x0 = *(const uint32_t*)(qh + s * 16 + 2 * tig);
+      const uint32_t x2 = *(const uint32_t*)(qh + s * 16 + 8 + 2 * tig);
+      qa0[s] = gid < ALPHA ? x0 : 0u;
+      qa2[s] = gid < ALPHA ? x2 : 0u;
+    }
+  }
+  float mloc = -INFINITY, lloc = 0.f;
+  float p[4][2];  // this lane's scores: 4 n-tiles x 2 rows, head gid
+  if (nrows > 0) {
+    __syncthreads();  // zero-filled padding rows visible
+    mbar_wait(&bar[0], 0);
+    const uint32_t kb = smem_u32(Ks);
+    const float sl2 = scale * LOG2E;
+#pragma unroll
+    for (int rg = 0; rg < 2; ++rg) {
+      float c0[4] = {0, 0, 0, 0}, c1[4] = {0, 0, 0, 0};
+      const int rbase = warp * 32 + rg * 16;
+      const int mi = lane >> 3, ri = lane & 7;
+      const uint32_t a_row = rbase + ri + ((mi & 2) ? 8 : 0);
+      const uint32_t a_col = (mi & 1) ? 8 : 0;
+#pragma unroll
+      for (int s = 0; s < KS; ++s) {
+        uint32_t b0, b1, b2, b3;
+        ldsm_x4(kb + (a_row * RS + s * 16 + a_col) * 2, b0, b1, b2, b3);
+        mma_bf16(c0, qa0[s], qa2[s], b0, b1);
+        mma_bf16(c1, qa0[s], qa2[s], b2, b3);
+      }
+      // c0: rows rbase + 2tig + {0,1}; c1: rows rbase + 8 + 2tig + {0,1}
+      const int rr[4] = {rbase + 2 * tig, rbase + 2 * tig + 1, rbase + 8 + 2 * tig,
+                         rbase + 9 + 2 * tig};
+      const float v[4] = {c0[0], c0[1], c1[0], c1[1]};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float s2 = rr[e] < nrows ? v[e] * sl2 : -INFINITY;
+        p[rg * 2 + (e >> 1)][e & 1] = s2;
+        mloc = fmaxf(mloc, s2);
+      }
+    }
+  }
+  // CTA max per head (log2 units)
+  mloc = fmaxf(mloc, __shfl_xor_sync(0xffffffffu, mloc, 1));
+  mloc = fmaxf(mloc, __shfl_xor_sync(0xffffffffu, mloc, 2));
+  if (tig == 0) red_m[warp][gid] = mloc;
+  __syncthreads();
+  const float M = fmaxf(fmaxf(red_m[0][gid], red_m[1][gid]), fmaxf(red_m[2][gid], red_m[3][gid]));
+
+  float o[D / 8][2];
+#pragma unroll
+  for (int i = 0; i < D / 8; ++i) o[i][0] = o[i][1] = 0.f;
+  if (nrows > 0) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const float x = (M == -INFINITY) ? 0.f : exp2f(p[i][e] - M);
+        p[i][e] = x;
+        lloc += x;
+      }
+    mbar_wait(&bar[1], 0);
+    const uint32_t vb = smem_u32(Vs);
+#pragma unroll
+    for (int rg = 0; rg < 2; ++rg) {
+      // A = P (heads x 16 rows): a0 = rows 2tig.., a2 = rows 8+2tig..
+      const uint32_t ah0 = pack_bf16(p[rg * 2][0], p[rg * 2][1]);
+      const uint32_t ah2 = pack_bf16(p[rg * 2 + 1][0], p[rg * 2 + 1][1]);
+      const float2 h0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&ah0));
+      const float2 h2 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&ah2));
+      const uint32_t al0 = pack_bf16(p[rg * 2][0] - h0.x, p[rg * 2][1] - h0.y);
+      const uint32_t al2 = pack_bf16(p[rg * 2 + 1][0] - h2.x, p[rg * 2 + 1][1] - h2.y);
+      const int rbase = warp * 32 + rg * 16;
+      const int mi = lane >> 3, ri = lane & 7;
+      const uint32_t b_row = rbase + ri + ((mi & 1) ? 8 : 0);
+      const uint32_t b_col = (mi & 2) ? 8 : 0;
+#pragma unroll
+      for (int dn = 0; dn < D / 16; ++dn) {
+        uint32_t b0, b1, b2, b3;
+        ldsm_x4_t(vb + (b_row * RS + dn * 16 + b_col) * 2, b0, b1, b2, b3);
+        float c[4] = {o[2 * dn][0], o[2 * dn][1], 0.f, 0.f};
+        mma_bf16(c, ah0, ah2, b0, b1);
+        mma_bf16(c, al0, al2, b0, b1);
+        o[2 * dn][0] = c[0];
+        o[2 * dn][1] = c[1];
+        float c2[4] = {o[2 * dn + 1][0], o[2 * dn + 1][1], 0.f, 0.f};
+        mma_bf16(c2, ah0, ah2, b2, b3);
+        mma_bf16(c2, al0, al2, b2, b3);
+        o[2 * dn + 1][0] = c2[0];
+        o[2 * dn + 1][1] = c2[1];
+      }
+    }
+  }
+  // CTA sums: l per head, o per (head, d)
+  lloc += __shfl_xor_sync(0xffffffffu, lloc, 1);
+  lloc += __shfl_xor_sync(0xffffffffu, lloc, 2);
+  if (tig == 0) red_l[warp][gid] = lloc;
+  if (gid < ALPHA) {
+#pragma unroll
+    for (int i = 0; i < D / 8; ++i) {
+      red_o[warp][gid][8 * i + 2 * tig] = o[i][0];
+      red_o[warp][gid][8 * i + 2 * tig + 1] = o[i][1];
+    }
+  }
+  __syncthreads();
+  for (int i = tid; i < ALPHA * D; i += AT_THREADS) {
+    const int j = i / D, d = i % D;
+    const float s = red_o[0][j][d] + red_o[1][j][d] + red_o[2][j][d] + red_o[3][j][d];
+    part_o[((head_base + j) * nsplit + split) * D + d] = s;
+  }
+  if (tid < ALPHA) {
+    const int j = tid;
+    const float mm = fmaxf(fmaxf(red_m[0][j], red_m[1][j]), fmaxf(red_m[2][j], red_m[3][j]));
+    const float ll = red_l[0][j] + red_l[1][j] + red_l[2][j] + red_l[3][j];
+    part_ml[((head_base + j) * nsplit + split) * 2] = nrows > 0 ? mm : -INFINITY;
+    part_ml[((head_base + j) * nsplit + split) * 2 + 1] = nrows > 0 ? ll : 0.f;
+  }
+  const size_t grp = (size_t)lr * B * G + bg;
+  if (last_block_ticket(&cnt[grp], nsplit, &flag))
+    merge_partials<D, ALPHA>(part_o, part_ml, nsplit, head_base, out, lse,
+                             ((size_t)l * B + b) * Hq + g * ALPHA);
+  (void)Hq_;
+}
+
+// ---------------------------------------------------------------- fp32 / CUDA-core path
+template <int D, int ALPHA>
+__global__ void __launch_bounds__(AT_THREADS) attn_f32_kernel(
+    const float* __restrict__ q, const void* const* __restrict__ k_layers,
+    const void* const* __restrict__ v_layers, int kv_mode, const int32_t* __restrict__ idx,
+    const int32_t* __restrict__ count, int layer_begin, int B, int G, int rows, int kbud,
+    float scale, int nsplit, float* __restrict__ part_o, float* __restrict__ part_ml,
+    unsigned* __restrict__ cnt, float* __restrict__ out, float* __restrict__ lse) {
+  __shared__ float qs[ALPHA][D];
+  __shared__ float ps[ALPHA][AT_ROWS];
+  __shared__ int toks[AT_ROWS];
+  __shared__ float red[AT_THREADS / 32][ALPHA];
+  __shared__ float mh[ALPHA], lh[ALPHA];
+  __shared__ int flag;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int split = blockIdx.x, bg = blockIdx.y, lr = blockIdx.z;
+  const int l = layer_begin + lr;
+  const int b = bg / G, g = bg % G;
+  const int Hq = G * ALPHA;
+  const int n_sel = min(count[bg], kbud);
+  const int r0 = split * AT_ROWS;
+  const int nrows = max(0, min(AT_ROWS, n_sel - r0));
+  const size_t head_base = ((size_t)lr * B + b) * Hq + g * ALPHA;
+  const float* Kl = (const float*)k_layers[l] + (size_t)bg * rows * D;
+  const float* Vl = (const float*)v_layers[l] + (size_t)bg * rows * D;
+  for (int i = tid; i < ALPHA * D; i += AT_THREADS)
+    qs[i / D][i % D] = q[(((size_t)l * B + b) * Hq + g * ALPHA) * D + i];
+  if (tid < nrows)
+    toks[tid] = kv_mode == SPC_KV_INDEXED ? idx[(size_t)bg * kbud + r0 + tid] : r0 + tid;
+  __syncthreads();
+  float s[ALPHA];
+#pragma unroll
+  for (int j = 0; j < ALPHA; ++j) s[j] = -INFINITY;
+  if (tid < nrows) {
+    const float* kr = Kl + (size_t)toks[tid] * D;
+#pragma unroll
+    for (int j = 0; j < ALPHA; ++j) s[j] = 0.f;
+    for (int d = 0; d < D; ++d) {
+      const float kv = kr[d];
+#pragma unroll
+      for (int j = 0; j < ALPHA; ++j) s[j] = fmaf(qs[j][d], kv, s[j]);
+    }
+#pragma unroll
+    for (int j = 0; j < ALPHA; ++j) s[j] *= scale;
+  }
+#pragma unroll
+  for (int j = 0; j < ALPHA; ++j) {
+    float m = warp_max(s[j]);
+    if (lane == 0) red[warp][j] = m;
+  }
+  __syncthreads();
+  if (tid < ALPHA) {
+    float m = -INFINITY;
+    for (int w = 0; w < AT_THREADS / 32; ++w) m = fmaxf(m, red[w][tid]);
+    mh[tid] = m;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < ALPHA; ++j) {
+    const float pj = (tid < nrows) ? expf(s[j] - mh[j]) : 0.f;
+    ps[j][tid] = pj;
+    float sum = warp_sum(pj);
+    if (lane == 0) red[warp][j] = sum;
+  }
+  __syncthreads();
+  if (tid < ALPHA) {
+    float t = 0.f;
+    for (int w = 0; w < AT_THREADS / 32; ++w) t += red[w][tid];
+    lh[tid] = t;
+  }
+  for (int i = tid; i < ALPHA * D; i += AT_THREADS) {
+    const int j = i / D, d = i % D;
+    float acc = 0.f;
+    for (int r = 0; r < nrows; ++r) acc = fmaf(ps[j][r], Vl[(size_t)toks[r] * D + d], acc);
+    part_o[((head_base + j) * nsplit + split) * D + d] = acc;
+  }
+  __syncthreads();
+  if (tid < ALPHA) {
+    part_ml[((head_base + tid) * nsplit + split) * 2] = nrows > 0 ? mh[tid] * LOG2E : -INFINITY;
+    part_ml[((head_base + tid) * nsplit + split) * 2 + 1] = nrows > 0 ? lh[tid] : 0.f;
+  }
+  const size_t grp = (size_t)lr * B * G + bg;
+  if (last_block_ticket(&cnt[grp], nsplit, &flag))
+    merge_partials<D, ALPHA>(part_o, part_ml, nsplit, head_base, out, lse,
+                             ((size_t)l * B + b) * Hq + g * ALPHA);
+}
+
+__global__ void merge_kernel(const float* __restrict__ o_parts, const float* __restrict__ lse_parts,
+                             int P, int n, int D, float* __restrict__ out,
+                             float* __restrict__ lse_out) {
+  const int row = blockIdx.x;
+  float M = -INFINITY;
+  for (int p = 0; p < P; ++p) M = fmaxf(M, lse_parts[(size_t)p * n + row]);
+  float den = 0.f;
+  for (int p = 0; p < P; ++p) {
+    const float x = lse_parts[(size_t)p * n + row];
+    if (x != -INFINITY) den += expf(x - M);
+  }
+  for (int d = threadIdx.x; d < D; d += blockDim.x) {
+    float num = 0.f;
+    if (M != -INFINITY)
+      for (int p = 0; p < P; ++p) {
+        const float x = lse_parts[(size_t)p * n + row];
+        if (x != -INFINITY) num += expf(x - M) * o_parts[((size_t)p * n + row) * D + d];
+      }
+    out[(size_t)row * D + d] = den > 0.f ? num / den : 0.f;
+  }
+  if (threadIdx.x == 0 && lse_out) lse_out[row] = den > 0.f ? M + logf(den) : -INFINITY;
+}
+
+}  // namespace
+}  // namespace spc
+
+using namespace spc;
+
+extern "C" size_t spc_attn_workspace(int L, int B, int Hq, int D, int k) {
+  if (L <= 0 || B <= 0 || Hq <= 0 || D <= 0 || k <= 0) return 0;
+  return attn_ws_layout(nullptr, L, B, Hq, D, k).bytes;
+}
+
+extern "C" int spc_sparse_decode_attn(int dtype, const void* q, const void* const* k_layers,
+                                      const void* const* v_layers, int kv_mode, const int32_t* idx,
+                                      const int32_t* count, int L, int layer_begin, int layer_end,
+                                      int B, int Hq, int G, int D, int rows, int k, float scale,
+                                      float* out, float* lse, void* ws, size_t ws_bytes,
+                                      spc_stream_t stream) {
+  if (!q || !k_layers || !v_layers || !count || !out) return SPC_E_NULL;
+  if (kv_mode == SPC_KV_INDEXED && !idx) return SPC_E_NULL;
+  if (kv_mode != SPC_KV_INDEXED && kv_mode != SPC_KV_SLOTS) return SPC_E_RANGE;
+  if (L <= 0 || B <= 0 || Hq <= 0 || G <= 0 || Hq % G || rows <= 0) return SPC_E_SHAPE;
+  if (k < 1 || k > SPC_MAX_K) return SPC_E_BUDGET;
+  if (kv_mode == SPC_KV_SLOTS && rows < k) return SPC_E_SHAPE;
+  if (layer_begin < 0 || layer_end > L || layer_begin > layer_end) return SPC_E_RANGE;
+  if (layer_begin == layer_end) return SPC_OK;
+  if (!ws || ws_bytes < spc_attn_workspace(L, B, Hq, D, k)) return SPC_E_WORKSPACE;
+  const int alpha = Hq / G;
+  if (!(D == 64 || D == 128) || !(alpha == 1 || alpha == 2 || alpha == 4 || alpha == 8))
+    return SPC_E_UNSUPPORTED;
+  if (dtype != SPC_BF16 && dtype != SPC_F32) return SPC_E_UNSUPPORTED;
+  AttnWs w = attn_ws_layout(ws, L, B, Hq, D, k);
+  const int nsplit = (k + AT_ROWS - 1) / AT_ROWS;
+  dim3 grid(nsplit, B * G, layer_end - layer_begin);
+  cudaStream_t st = as_stream(stream);
+#define AT(DD, AA)                                                                              \
+  if (D == DD && alpha == AA) {                                                                 \
+    if (dtype == SPC_BF16) {                                                                    \
+      const int smem = (int)(2 * sizeof(uint16_t) * AT_ROWS * (DD + 8));                        \
+      static bool attr = false;                                                                 \
+      if (!attr) {                                                                              \
+        cudaFuncSetAttribute(attn_bf16_kernel<DD, AA>,                                          \
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, smem);                \
+        attr = true;                                                                            \
+      }                                                                                         \
+      attn_bf16_kernel<DD, AA><<<grid, AT_THREADS, smem, st>>>(                                 \
+          (const uint16_t*)q, k_layers, v_layers, kv_mode, idx, count, layer_begin, B, G, rows, \
+          k, scale, nsplit, w.part_o, w.part_ml, w.cnt, out, lse);                              \
+    } else                                                                                      \
+      attn_f32_kernel<DD, AA><<<grid, AT_THREADS, 0, st>>>(                                     \
+          (const float*)q, k_layers, v_layers, kv_mode, idx, count, layer_begin, B, G, rows, k, \
+          scale, nsplit, w.part_o, w.part_ml, w.cnt, out, lse);                                 \
+    return launched();                                                                          \
+  }
+  AT(64, 1) AT(64, 2) AT(64, 4) AT(64, 8) AT(128, 1) AT(128, 2) AT(128, 4) AT(128, 8)
+#undef AT
+  return SPC_E_UNSUPPORTED;
+}
+
+extern "C" int spc_attn_merge(const float* o_parts, const float* lse_parts, int P, int n, int D,
+                              float* out, float* lse_out, spc_stream_t stream) {
+  if (!o_parts || !lse_parts || !out) return SPC_E_NULL;
+  if (P < 1 || n < 1 || D < 1) return SPC_E_SHAPE;
+  merge_kernel<<<n, 128, 0, as_stream(stream)>>>(o_parts, lse_parts, P, n, D, out, lse_out);
+  return launched();
+}

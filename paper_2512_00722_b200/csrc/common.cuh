@@ -1,0 +1,219 @@
+// common.cuh — device/host helpers shared by the libspc kernels (sm_100a).
+// Nothing here is shared with the CPU oracle (oracle/); the contract functions
+// below are written from DESIGN.md §3, independently of oracle/spcref.c.
+#pragma once
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <atomic>
+
+#include "../../include/spc.h"
+
+namespace spc {
+
+// ----------------------------------------------------------------- host side
+extern std::atomic<uint64_t> g_launches;
+void set_cuda_error(cudaError_t e);
+inline int launched(cudaError_t pre = cudaSuccess) {
+  cudaError_t e = pre != cudaSuccess ? pre : cudaGetLastError();
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  if (e != cudaSuccess) {
+    set_cuda_error(e);
+    return SPC_E_CUDA;
+  }
+  return SPC_OK;
+}
+#define SPC_TRY(x)               \
+  do {                           \
+    int _rc = (x);               \
+    if (_rc != SPC_OK) return _rc; \
+  } while (0)
+
+inline cudaStream_t as_stream(spc_stream_t s) { return reinterpret_cast<cudaStream_t>(s); }
+inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+int num_sms();
+// Encode a tiled TMA descriptor (driver entry point fetched through cudart).
+int make_tmap_3d_bf16(CUtensorMap* map, const void* base, uint64_t d0, uint64_t d1, uint64_t d2,
+                      uint32_t box0, uint32_t box1, CUtensorMapSwizzle swz);
+
+// --------------------------------------------------------------- device side
+__device__ __forceinline__ float bf16lo(uint32_t w) { return __uint_as_float(w << 16); }
+__device__ __forceinline__ float bf16hi(uint32_t w) { return __uint_as_float(w & 0xFFFF0000u); }
+
+// O3, written from DESIGN.md §3: exp for x <= 0 with IEEE RN ops only.
+__device__ __forceinline__ float spc_exp_dev(float x) {
+  if (x < -87.0f) return 0.0f;
+  const float n = rintf(__fmul_rn(x, __uint_as_float(0x3FB8AA3Bu)));
+  float r = __fmaf_rn(-n, __uint_as_float(0x3F317200u), x);
+  r = __fmaf_rn(-n, __uint_as_float(0x35BFBE8Eu), r);
+  float p = __uint_as_float(0x39500D01u);                 // 1/7!
+  p = __fmaf_rn(p, r, __uint_as_float(0x3AB60B61u));      // 1/6!
+  p = __fmaf_rn(p, r, __uint_as_float(0x3C088889u));      // 1/5!
+  p = __fmaf_rn(p, r, __uint_as_float(0x3D2AAAABu));      // 1/4!
+  p = __fmaf_rn(p, r, __uint_as_float(0x3E2AAAABu));      // 1/3!
+  p = __fmaf_rn(p, r, __uint_as_float(0x3F000000u));      // 1/2!
+  p = __fmaf_rn(p, r, __uint_as_float(0x3F800000u));      // 1/1!
+  p = __fmaf_rn(p, r, __uint_as_float(0x3F800000u));      // 1/0!
+  const float two_n = __uint_as_float((uint32_t)((int)n + 127) << 23);
+  return __fmul_rn(p, two_n);
+}
+
+// trunc(e * 2^40) as int64 for 0 <= e <= 1 (e * 2^40 is exact in fp32).
+__device__ __forceinline__ long long fixpoint40(float e) {
+  return __float2ll_rz(__fmul_rn(e, 1099511627776.0f));
+}
+
+// Composite key of the O7 order: (bits(v) << 32) | ~uint32(id); larger = earlier.
+__device__ __forceinline__ unsigned long long composite(uint32_t vbits, int id) {
+  return ((unsigned long long)vbits << 32) | (unsigned long long)(uint32_t)(~(uint32_t)id);
+}
+
+// -------------------------------------------- packed fp32 FMA (sm_100 FFMA2)
+// d = a*b + c per lane, IEEE RN, no FTZ: per-element identical to fmaf().
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+  float2 d;
+  asm("{\n\t.reg .b64 ra, rb, rc, rd;\n\t"
+      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\tmov.b64 rc, {%6, %7};\n\t"
+      "fma.rn.f32x2 rd, ra, rb, rc;\n\t"
+      "mov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+  return d;
+}
+
+// ------------------------------------------------ mbarrier / bulk async copy
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+// 1-D bulk copy global -> shared, completion counted in bytes on `bar`.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+// 3-D tiled TMA load (box) -> shared.
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, "
+      "{%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(map) : "memory");
+}
+
+// explicit shared-memory loads by 32-bit shared address (never generic LD)
+__device__ __forceinline__ uint4 lds128(uint32_t a) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "r"(a));
+  return v;
+}
+__device__ __forceinline__ float4 lds128f(uint32_t a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(a));
+  return v;
+}
+__device__ __forceinline__ float2 lds64f(uint32_t a) {
+  float2 v;
+  asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(a));
+  return v;
+}
+
+// -------------------------------------------------------- warp reductions
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ long long warp_sum_ll(long long v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Block-wide exclusive scan of one int per thread.
+// (requires blockDim.x a multiple of 32, <= 1024; contains __syncthreads)
+__device__ __forceinline__ int block_excl_scan(int v, int* wsum, int* total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  __syncthreads();  // wsum may still be read by a previous call
+  int incl = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  if (lane == 31) wsum[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    const int nw = blockDim.x / 32;
+    int x = lane < nw ? wsum[lane] : 0;
+    int xi = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int t = __shfl_up_sync(0xffffffffu, xi, o);
+      if (lane >= o) xi += t;
+    }
+    if (lane < nw) wsum[lane] = xi - x;
+    if (lane == 31) *total = xi;
+  }
+  __syncthreads();
+  return wsum[warp] + incl - v;
+}
+
+// "Last block done" ticket: returns true in exactly one CTA of a group after
+// all `total` CTAs of that group have published their results; that CTA also
+// resets the counter to 0 so the workspace stays reusable.
+__device__ __forceinline__ bool last_block_ticket(unsigned int* counter, unsigned int total,
+                                                  int* smem_flag) {
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned int t = atomicAdd(counter, 1u);
+    *smem_flag = (t == total - 1);
+    if (t == total - 1) *counter = 0u;
+  }
+  __syncthreads();
+  bool last = *smem_flag != 0;
+  if (last) __threadfence();
+  return last;
+}
+
+}  // namespace spc

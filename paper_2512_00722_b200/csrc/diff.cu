@@ -1,0 +1,200 @@
+// diff.cu — spc_elastic_diff (O8) and spc_gather_kv (O9).
+//
+// Paper §5.4: with S_last the previous selection and S_now the
+// current one, load S_now − S_last and overwrite S_last − S_now in place with
+// Tensor.copy_(); the fixed budget makes both sets equally large.  Prefetch on
+// separate CUDA streams; the KV source may live in CPU DRAM.
+//
+// spc_elastic_diff: one CTA per (b,g) row.  Sorted-set membership by binary
+// search in shared memory, order-preserving compaction with a ballot/shuffle
+// block scan, slot reuse in ascending slot order (reading R13).
+// spc_gather_kv: vectorised 16-byte row copies, one warp per (layer, row);
+// sources may be mapped pinned host memory (zero-copy PCIe reads).
+#include "common.cuh"
+
+namespace spc {
+namespace {
+
+constexpr int DF_THREADS = 1024;
+constexpr int DF_PER = SPC_MAX_K / DF_THREADS;
+
+__device__ __forceinline__ bool contains(const int32_t* a, int n, int x) {
+  int lo = 0, hi = n;  // a ascending
+  while (lo < hi) {
+    int mid = (lo + hi) >> 1;
+    int v = a[mid];
+    if (v == x) return true;
+    if (v < x)
+      lo = mid + 1;
+    else
+      hi = mid;
+  }
+  return false;
+}
+
+__global__ void __launch_bounds__(DF_THREADS) diff_kernel(
+    const int32_t* __restrict__ prev_idx, const int32_t* __restrict__ prev_count,
+    const int32_t* __restrict__ cur_idx, const int32_t* __restrict__ cur_count, int k,
+    int32_t* __restrict__ slot_tok, int32_t* __restrict__ load_tok, int32_t* __restrict__ load_slot,
+    int32_t* __restrict__ n_load, int32_t* __restrict__ evict_tok, int32_t* __restrict__ n_evict) {
+  extern __shared__ int32_t dsm[];
+  int32_t* sprev = dsm;       // [k]
+  int32_t* scur = dsm + k;    // [k]
+  int32_t* snew = dsm + 2 * k;  // [k]
+  __shared__ int wsum[DF_THREADS / 32];
+  __shared__ int total;
+  const int row = blockIdx.x, tid = threadIdx.x;
+  const int np = min(max(prev_count[row], 0), k), nc = min(max(cur_count[row], 0), k);
+  const int32_t* pv = prev_idx + (size_t)row * k;
+  const int32_t* cv = cur_idx + (size_t)row * k;
+  for (int i = tid; i < np; i += DF_THREADS) sprev[i] = pv[i];
+  for (int i = tid; i < nc; i += DF_THREADS) scur[i] = cv[i];
+  __syncthreads();
+  const int per = (k + DF_THREADS - 1) / DF_THREADS;
+  const int e0 = tid * per;
+
+  // new = cur \ prev (ascending)
+  int flag[DF_PER];
+  int cnt = 0;
+#pragma unroll
+  for (int i = 0; i < DF_PER; ++i) {
+    const int e = e0 + i;
+    flag[i] = (i < per && e < nc) ? !contains(sprev, np, scur[e]) : 0;
+    cnt += flag[i];
+  }
+  int pos = block_excl_scan(cnt, wsum, &total);
+#pragma unroll
+  for (int i = 0; i < DF_PER; ++i)
+    if (flag[i]) snew[pos++] = scur[e0 + i];
+  __syncthreads();
+  const int nl = total;
+  int32_t* lt = load_tok + (size_t)row * k;
+  for (int i = tid; i < k; i += DF_THREADS) lt[i] = i < nl ? snew[i] : -1;
+  if (tid == 0) n_load[row] = nl;
+
+  // evicted = prev \ cur (ascending)
+  if (evict_tok || n_evict) {
+    cnt = 0;
+#pragma unroll
+    for (int i = 0; i < DF_PER; ++i) {
+      const int e = e0 + i;
+      flag[i] = (i < per && e < np) ? !contains(scur, nc, sprev[e]) : 0;
+      cnt += flag[i];
+    }
+    pos = block_excl_scan(cnt, wsum, &total);
+    if (evict_tok) {
+      int32_t* et = evict_tok + (size_t)row * k;
+#pragma unroll
+      for (int i = 0; i < DF_PER; ++i)
+        if (flag[i]) et[pos++] = sprev[e0 + i];
+      for (int i = total + tid; i < k; i += DF_THREADS) et[i] = -1;
+    }
+    if (n_evict && tid == 0) n_evict[row] = total;
+  }
+
+  // slot reuse: freed slots (empty or token not in cur) in ascending slot order
+  if (slot_tok) {
+    int32_t* st = slot_tok + (size_t)row * k;
+    int tok[DF_PER];
+    cnt = 0;
+#pragma unroll
+    for (int i = 0; i < DF_PER; ++i) {
+      const int s = e0 + i;
+      tok[i] = (i < per && s < k) ? st[s] : -2;
+      flag[i] = tok[i] != -2 && (tok[i] < 0 || !contains(scur, nc, tok[i]));
+      cnt += flag[i];
+    }
+    pos = block_excl_scan(cnt, wsum, &total);
+    int32_t* ls = load_slot + (size_t)row * k;
+#pragma unroll
+    for (int i = 0; i < DF_PER; ++i) {
+      if (!flag[i]) continue;
+      const int s = e0 + i;
+      if (pos < nl) {
+        st[s] = snew[pos];
+        ls[pos] = s;
+      } else {
+        st[s] = -1;
+      }
+      ++pos;
+    }
+    for (int i = nl + tid; i < k; i += DF_THREADS) ls[i] = -1;
+  }
+}
+
+// ------------------------------------------------------------------ gather (O9)
+template <typename VecT>
+__global__ void __launch_bounds__(256) gather_kernel(
+    const void* const* __restrict__ k_src, const void* const* __restrict__ v_src, int B, int G,
+    int Smax, int kbud, int row_vecs, int layer_begin, const int32_t* __restrict__ load_tok,
+    const int32_t* __restrict__ load_slot, const int32_t* __restrict__ n_load,
+    void* const* __restrict__ k_buf, void* const* __restrict__ v_buf) {
+  // grid: x = chunks of the budget, y = B*G row, z = layer
+  const int bg = blockIdx.y;
+  const int l = layer_begin + blockIdx.z;
+  const int n = n_load[bg];
+  const int lanes_per_row = row_vecs;  // 16-byte vectors per row (8 or 16)
+  const int rows_per_block = blockDim.x / lanes_per_row;
+  const int sub = threadIdx.x / lanes_per_row, lane = threadIdx.x % lanes_per_row;
+  const VecT* ks = (const VecT*)k_src[l];
+  const VecT* vs = (const VecT*)v_src[l];
+  VecT* kd = (VecT*)k_buf[l];
+  VecT* vd = (VecT*)v_buf[l];
+  const size_t src_base = (size_t)bg * Smax * row_vecs, dst_base = (size_t)bg * kbud * row_vecs;
+  for (int i = blockIdx.x * rows_per_block + sub; i < n; i += gridDim.x * rows_per_block) {
+    const int t = load_tok[(size_t)bg * kbud + i];
+    const int s = load_slot[(size_t)bg * kbud + i];
+    const VecT a = ks[src_base + (size_t)t * row_vecs + lane];
+    const VecT b = vs[src_base + (size_t)t * row_vecs + lane];
+    kd[dst_base + (size_t)s * row_vecs + lane] = a;
+    vd[dst_base + (size_t)s * row_vecs + lane] = b;
+  }
+}
+
+}  // namespace
+}  // namespace spc
+
+using namespace spc;
+
+extern "C" int spc_elastic_diff(const int32_t* prev_idx, const int32_t* prev_count,
+                                const int32_t* cur_idx, const int32_t* cur_count, int B, int G,
+                                int k, int32_t* slot_tok, int32_t* load_tok, int32_t* load_slot,
+                                int32_t* n_load, int32_t* evict_tok, int32_t* n_evict,
+                                spc_stream_t stream) {
+  if (!prev_idx || !prev_count || !cur_idx || !cur_count || !load_tok || !n_load) return SPC_E_NULL;
+  if (slot_tok && !load_slot) return SPC_E_NULL;
+  if (B <= 0 || G <= 0) return SPC_E_SHAPE;
+  if (k < 1 || k > SPC_MAX_K) return SPC_E_BUDGET;
+  const size_t smem = sizeof(int32_t) * 3 * (size_t)k;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(diff_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)(sizeof(int32_t) * 3 * SPC_MAX_K));
+    attr = true;
+  }
+  diff_kernel<<<B * G, DF_THREADS, smem, as_stream(stream)>>>(prev_idx, prev_count, cur_idx,
+                                                              cur_count, k, slot_tok, load_tok,
+                                                              load_slot, n_load, evict_tok, n_evict);
+  return launched();
+}
+
+extern "C" int spc_gather_kv(int dtype, const void* const* k_src, const void* const* v_src, int L,
+                             int B, int G, int D, int Smax, int k, int layer_begin, int layer_end,
+                             const int32_t* load_tok, const int32_t* load_slot,
+                             const int32_t* n_load, void* const* k_buf, void* const* v_buf,
+                             spc_stream_t stream) {
+  if (!k_src || !v_src || !load_tok || !load_slot || !n_load || !k_buf || !v_buf) return SPC_E_NULL;
+  if (L <= 0 || B <= 0 || G <= 0 || Smax <= 0) return SPC_E_SHAPE;
+  if (k < 1 || k > SPC_MAX_K) return SPC_E_BUDGET;
+  if (layer_begin < 0 || layer_end > L || layer_begin > layer_end) return SPC_E_RANGE;
+  if (layer_begin == layer_end) return SPC_OK;
+  const int esz = dtype == SPC_BF16 ? 2 : (dtype == SPC_F32 ? 4 : 0);
+  if (!esz) return SPC_E_UNSUPPORTED;
+  if ((D * esz) % 16 || D * esz / 16 > 32 || 32 % (D * esz / 16)) return SPC_E_UNSUPPORTED;
+  const int row_vecs = D * esz / 16;
+  dim3 grid((k + 63) / 64, B * G, layer_end - layer_begin);
+  gather_kernel<uint4><<<grid, 256, 0, as_stream(stream)>>>(k_src, v_src, B, G, Smax, k, row_vecs,
+                                                            layer_begin, load_tok, load_slot, n_load,
+                                                            k_buf, v_buf);
+  return launched();
+}

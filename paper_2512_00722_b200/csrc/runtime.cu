@@ -1,0 +1,85 @@
+// runtime.cu — status strings, launch counter, device queries, TMA descriptor
+// encoding.  Part of libspc.so (see include/spc.h).
+#include <cudaTypedefs.h>
+
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+
+#include "common.cuh"
+
+namespace spc {
+std::atomic<uint64_t> g_launches{0};
+static thread_local char g_err[256] = "";
+
+void set_cuda_error(cudaError_t e) {
+  snprintf(g_err, sizeof(g_err), "%s: %s", cudaGetErrorName(e), cudaGetErrorString(e));
+}
+
+int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &p, 12000, cudaEnableDefault,
+                                         &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+int make_tmap_3d_bf16(CUtensorMap* map, const void* base, uint64_t d0, uint64_t d1, uint64_t d2,
+                      uint32_t box0, uint32_t box1, CUtensorMapSwizzle swz) {
+  auto enc = get_encode();
+  if (!enc) {
+    snprintf(g_err, sizeof(g_err), "cuTensorMapEncodeTiled unavailable");
+    return SPC_E_CUDA;
+  }
+  cuuint64_t dims[3] = {d0, d1, d2};
+  cuuint64_t strides[2] = {d0 * 2, d0 * d1 * 2};
+  cuuint32_t box[3] = {box0, box1, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    snprintf(g_err, sizeof(g_err), "cuTensorMapEncodeTiled failed (%d)", (int)r);
+    return SPC_E_CUDA;
+  }
+  return SPC_OK;
+}
+}  // namespace spc
+
+extern "C" {
+
+const char* spc_status_string(int s) {
+  switch (s) {
+    case SPC_OK: return "SPC_OK";
+    case SPC_E_NULL: return "SPC_E_NULL: required pointer is NULL";
+    case SPC_E_SHAPE: return "SPC_E_SHAPE: invalid shape";
+    case SPC_E_BUDGET: return "SPC_E_BUDGET: budget k out of range";
+    case SPC_E_RANGE: return "SPC_E_RANGE: argument out of range";
+    case SPC_E_STATE: return "SPC_E_STATE: inconsistent state";
+    case SPC_E_WORKSPACE: return "SPC_E_WORKSPACE: workspace too small";
+    case SPC_E_UNSUPPORTED: return "SPC_E_UNSUPPORTED: configuration not compiled in";
+    case SPC_E_CUDA: return "SPC_E_CUDA: CUDA error";
+    default: return "unknown spc_status";
+  }
+}
+const char* spc_last_cuda_error(void) { return spc::g_err; }
+int spc_version(void) { return 100; }
+uint64_t spc_launch_count(void) { return spc::g_launches.load(); }
+}

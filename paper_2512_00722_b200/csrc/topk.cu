@@ -1,0 +1,521 @@
+// topk.cu — spc_topk / spc_topk_merge / spc_topk_filter: O7 and O13.
+//
+// Paper: "select the Top-K candidates" per KV group (head-level
+// retrieval), budget k = 2048.  Order (R8):
+// value descending, global id ascending, realised by the 64-bit composite key
+// (bits(v) << 32) | ~uint32(id) — values are >= 0 so float bits order like
+// unsigned integers (R20).  The k-th largest composite T is found by radix
+// select; the selection is then exactly {x : composite(x) >= T}.
+//
+// Kernels (rows R = B*G):
+//   hist_kernel     (multi-CTA / row)  2048-bin histogram of the top 11 bits
+//   find_kernel     (1 warp / row)     threshold bin b*, residual rank r
+//   collect_kernel  (multi-CTA / row)  composites of the elements in bin b*
+//   select_kernel   (1 CTA / row)      radix-refine the candidates to T in
+//                                      shared memory, then one ordered pass
+//                                      that emits positions >= T ascending.
+// Degenerate inputs (more than CAND_CAP elements in the threshold bin, e.g.
+// massive exact ties) fall back to refinement passes over the row itself.
+#include "common.cuh"
+
+namespace spc {
+namespace {
+
+constexpr int TK_THREADS = 256;
+constexpr int TK_PER = 16;
+constexpr int TK_TILE = TK_THREADS * TK_PER;
+constexpr int NBIN0 = 2048;          // top digit: 11 bits of the composite
+constexpr int CAND_CAP = 8192;       // candidates kept per row (global and shared)
+constexpr int SEL_THREADS = 1024;
+constexpr int RANK_MAX = 1024;       // rank by counting below this many candidates
+
+struct RowInfo {
+  int need;   // min(k, len)
+  int len;    // valid elements of the row
+  int r;      // rank still needed inside the prefix (1-based)
+  int cm;     // number of elements matching the prefix
+  int bits;   // prefix length in bits
+  int all;    // 1: every element selected (need == len)
+  unsigned long long prefix;  // composite high bits (left-aligned)
+};
+
+struct TopkWs {
+  unsigned* hist;
+  RowInfo* info;
+  unsigned* ccount;
+  unsigned long long* cand;
+  size_t bytes;
+};
+
+TopkWs topk_ws_layout(void* ws, int R) {
+  uint8_t* p = (uint8_t*)ws;
+  TopkWs w;
+  size_t off = 0;
+  w.hist = (unsigned*)(p + off);
+  off = align_up(off + sizeof(unsigned) * (size_t)R * NBIN0, 256);
+  w.info = (RowInfo*)(p + off);
+  off = align_up(off + sizeof(RowInfo) * (size_t)R, 256);
+  w.ccount = (unsigned*)(p + off);
+  off = align_up(off + sizeof(unsigned) * (size_t)R, 256);
+  w.cand = (unsigned long long*)(p + off);
+  off = align_up(off + sizeof(unsigned long long) * (size_t)R * CAND_CAP, 256);
+  w.bytes = off;
+  return w;
+}
+
+// composite of position p of a dense row
+__device__ __forceinline__ unsigned long long row_key(const float* row, int p, int len, int force,
+                                                      int stride, int offset) {
+  uint32_t vb = (force && p == len - 1) ? 0x7F800000u : __float_as_uint(__ldg(row + p));
+  return composite(vb, p * stride + offset);
+}
+
+__device__ __forceinline__ int row_len(const int32_t* seq_len, int row, int G, int n_cols) {
+  int s = seq_len[row / G];
+  return s < n_cols ? (s < 0 ? 0 : s) : n_cols;
+}
+
+__global__ void __launch_bounds__(TK_THREADS) hist_kernel(const float* __restrict__ val,
+                                                          const int32_t* __restrict__ seq_len, int G,
+                                                          int n_cols, int force,
+                                                          unsigned* __restrict__ hist) {
+  __shared__ unsigned h[NBIN0];
+  const int row = blockIdx.y;
+  const int len = row_len(seq_len, row, G, n_cols);
+  const int t0 = blockIdx.x * TK_TILE;
+  if (t0 >= len) return;
+  for (int i = threadIdx.x; i < NBIN0; i += TK_THREADS) h[i] = 0;
+  __syncthreads();
+  const float* v = val + (size_t)row * n_cols;
+#pragma unroll 4
+  for (int i = 0; i < TK_PER; ++i) {
+    const int p = t0 + i * TK_THREADS + threadIdx.x;
+    if (p < len) {
+      uint32_t vb = (force && p == len - 1) ? 0x7F800000u : __float_as_uint(__ldg(v + p));
+      atomicAdd(&h[vb >> 21], 1u);
+    }
+  }
+  __syncthreads();
+  unsigned* gh = hist + (size_t)row * NBIN0;
+  for (int i = threadIdx.x; i < NBIN0; i += TK_THREADS)
+    if (h[i]) atomicAdd(&gh[i], h[i]);
+}
+
+// Warp-cooperative search from the top bin down: returns (bin, above) with
+// above = sum of counts of bins > bin, above < r <= above + h[bin].
+template <int NB>
+__device__ __forceinline__ void find_bin_warp(const unsigned* h, int r, int* bin_out,
+                                              int* above_out) {
+  constexpr int PER = NB / 32;
+  const int lane = threadIdx.x & 31;
+  const int hi = NB - 1 - lane * PER;  // this lane owns bins hi .. hi-PER+1
+  unsigned s = 0;
+#pragma unroll 4
+  for (int i = 0; i < PER; ++i) s += h[hi - i];
+  unsigned incl = s;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    unsigned t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  const unsigned ballot = __ballot_sync(0xffffffffu, incl >= (unsigned)r);
+  const int L = __ffs(ballot) - 1;  // first lane whose cumulative count reaches r
+  unsigned before = __shfl_sync(0xffffffffu, incl - s, L);
+  if (lane == L) {
+    unsigned run = before;
+    int b = hi;
+    for (int i = 0; i < PER; ++i) {
+      b = hi - i;
+      if (run + h[b] >= (unsigned)r) break;
+      run += h[b];
+    }
+    *bin_out = b;
+    *above_out = (int)run;
+  }
+  __syncwarp();
+}
+
+__global__ void find_kernel(const unsigned* __restrict__ hist, const int32_t* __restrict__ seq_len,
+                            int G, int n_cols, int k, RowInfo* __restrict__ info,
+                            unsigned* __restrict__ ccount) {
+  const int row = blockIdx.x;
+  __shared__ int s_bin, s_above;
+  const int len = row_len(seq_len, row, G, n_cols);
+  const int need = k < len ? k : len;
+  RowInfo ri;
+  ri.need = need;
+  ri.len = len;
+  ri.all = (need == len);
+  ri.r = 0;
+  ri.cm = 0;
+  ri.bits = 0;
+  ri.prefix = 0;
+  if (!ri.all) {
+    const unsigned* h = hist + (size_t)row * NBIN0;
+    find_bin_warp<NBIN0>(h, need, &s_bin, &s_above);
+    __syncwarp();
+    ri.r = need - s_above;
+    ri.cm = (int)h[s_bin];
+    ri.bits = 11;
+    ri.prefix = (unsigned long long)s_bin << 53;
+  }
+  if (threadIdx.x == 0) {
+    info[row] = ri;
+    ccount[row] = 0;
+  }
+}
+
+__global__ void __launch_bounds__(TK_THREADS) collect_kernel(
+    const float* __restrict__ val, const int32_t* __restrict__ seq_len, int G, int n_cols,
+    int force, int stride, int offset, const RowInfo* __restrict__ info,
+    unsigned* __restrict__ ccount, unsigned long long* __restrict__ cand) {
+  const int row = blockIdx.y;
+  const RowInfo ri = info[row];
+  if (ri.all || ri.cm > CAND_CAP) return;
+  const int len = ri.len;
+  const int t0 = blockIdx.x * TK_TILE;
+  if (t0 >= len) return;
+  const unsigned want = (unsigned)(ri.prefix >> 53);
+  const float* v = val + (size_t)row * n_cols;
+  unsigned long long* c = cand + (size_t)row * CAND_CAP;
+  const int lane = threadIdx.x & 31;
+  for (int i = 0; i < TK_PER; ++i) {
+    const int p = t0 + i * TK_THREADS + threadIdx.x;
+    bool hit = false;
+    unsigned long long key = 0;
+    if (p < len) {
+      key = row_key(v, p, len, force, stride, offset);
+      hit = (unsigned)(key >> 53) == want;
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, hit);
+    if (!m) continue;
+    unsigned base = 0;
+    const int leader = __ffs(m) - 1;
+    if (lane == leader) base = atomicAdd(&ccount[row], (unsigned)__popc(m));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    if (hit) {
+      const unsigned slot = base + __popc(m & ((1u << lane) - 1));
+      if (slot < CAND_CAP) c[slot] = key;
+    }
+  }
+}
+
+// --------------------------------------------------------------- selection core
+// Shared-memory state of one selecting CTA.
+struct SelSmem {
+  unsigned long long cand[2][CAND_CAP];
+  unsigned hist[256];
+  int n[2];
+  int bin, above;
+  unsigned long long T;
+  int wsum[SEL_THREADS / 32];
+};
+
+// r-th largest among the cm composites in s.cand[cur][0..cm), all sharing the
+// top `bits` bits.  Radix passes of 8 bits until cm <= RANK_MAX, then rank by
+// counting.  Returns T in s.T (valid after the final __syncthreads).
+__device__ void refine_in_smem(SelSmem& s, int cur, int cm, int r, int bits) {
+  const int tid = threadIdx.x;
+  while (cm > RANK_MAX && bits < 64) {
+    const int db = (64 - bits) < 8 ? (64 - bits) : 8;
+    const int shift = 64 - bits - db;
+    const unsigned mask = (1u << db) - 1;
+    for (int i = tid; i < 256; i += SEL_THREADS) s.hist[i] = 0;
+    if (tid == 0) s.n[cur ^ 1] = 0;
+    __syncthreads();
+    for (int i = tid; i < cm; i += SEL_THREADS)
+      atomicAdd(&s.hist[(unsigned)(s.cand[cur][i] >> shift) & mask], 1u);
+    __syncthreads();
+    if (tid < 32) find_bin_warp<256>(s.hist, r, &s.bin, &s.above);
+    __syncthreads();
+    const unsigned b = (unsigned)s.bin;
+    for (int i = tid; i < cm; i += SEL_THREADS) {
+      const unsigned long long x = s.cand[cur][i];
+      if (((unsigned)(x >> shift) & mask) == b) s.cand[cur ^ 1][atomicAdd(&s.n[cur ^ 1], 1)] = x;
+    }
+    r -= s.above;
+    bits += db;
+    __syncthreads();
+    cm = s.n[cur ^ 1];
+    cur ^= 1;
+  }
+  // rank by counting: exactly one candidate has r-1 larger ones (composites unique)
+  for (int i = tid; i < cm; i += SEL_THREADS) {
+    const unsigned long long x = s.cand[cur][i];
+    int larger = 0;
+    for (int j = 0; j < cm; ++j) larger += s.cand[cur][j] > x;
+    if (larger == r - 1) s.T = x;
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ bool prefix_match(unsigned long long x, unsigned long long prefix, int bits) {
+  return bits == 0 || (x >> (64 - bits)) == (prefix >> (64 - bits));
+}
+
+// Row-scan refinement for degenerate rows (threshold bin > CAND_CAP): narrow
+// the prefix with 8-bit passes over the row until at most CAND_CAP elements
+// match, then collect them into shared memory.  Returns (cm, r, bits) updated.
+template <class KeyFn>
+__device__ void narrow_by_row_scan(SelSmem& s, const KeyFn& key, int len, unsigned long long& prefix,
+                                   int& bits, int& r, int& cm) {
+  const int tid = threadIdx.x;
+  while (cm > CAND_CAP && bits < 64) {
+    const int db = (64 - bits) < 8 ? (64 - bits) : 8;
+    const int shift = 64 - bits - db;
+    const unsigned mask = (1u << db) - 1;
+    for (int i = tid; i < 256; i += SEL_THREADS) s.hist[i] = 0;
+    __syncthreads();
+    for (int p = tid; p < len; p += SEL_THREADS) {
+      const unsigned long long x = key(p);
+      if (prefix_match(x, prefix, bits)) atomicAdd(&s.hist[(unsigned)(x >> shift) & mask], 1u);
+    }
+    __syncthreads();
+    if (tid < 32) find_bin_warp<256>(s.hist, r, &s.bin, &s.above);
+    __syncthreads();
+    r -= s.above;
+    cm = (int)s.hist[s.bin];
+    prefix |= (unsigned long long)s.bin << shift;
+    bits += db;
+    __syncthreads();
+  }
+  if (tid == 0) s.n[0] = 0;
+  __syncthreads();
+  for (int p = tid; p < len; p += SEL_THREADS) {
+    const unsigned long long x = key(p);
+    if (prefix_match(x, prefix, bits)) s.cand[0][atomicAdd(&s.n[0], 1)] = x;
+  }
+  __syncthreads();
+}
+
+struct DenseKey {
+  const float* row;
+  int len, force, stride, offset;
+  __device__ unsigned long long operator()(int p) const {
+    return row_key(row, p, len, force, stride, offset);
+  }
+};
+
+__global__ void __launch_bounds__(SEL_THREADS, 1) select_kernel(
+    const float* __restrict__ val, int n_cols, int k, int force, int stride, int offset,
+    const RowInfo* __restrict__ info, const unsigned* __restrict__ ccount,
+    const unsigned long long* __restrict__ cand, int32_t* __restrict__ out_idx,
+    float* __restrict__ out_val, int32_t* __restrict__ out_count,
+    unsigned long long* __restrict__ out_thresh) {
+  extern __shared__ __align__(16) uint8_t sel_raw[];
+  SelSmem& s = *reinterpret_cast<SelSmem*>(sel_raw);
+  __shared__ int s_total;
+  const int row = blockIdx.x, tid = threadIdx.x;
+  const RowInfo ri = info[row];
+  const int len = ri.len;
+  const float* v = val + (size_t)row * n_cols;
+  DenseKey key{v, len, force, stride, offset};
+  unsigned long long T = 0;
+  if (!ri.all) {
+    int cm = ri.cm, r = ri.r, bits = ri.bits;
+    unsigned long long prefix = ri.prefix;
+    if (cm <= CAND_CAP) {
+      const unsigned long long* c = cand + (size_t)row * CAND_CAP;
+      for (int i = tid; i < cm; i += SEL_THREADS) s.cand[0][i] = c[i];
+      __syncthreads();
+    } else {
+      narrow_by_row_scan(s, key, len, prefix, bits, r, cm);
+      cm = s.n[0];
+    }
+    refine_in_smem(s, 0, cm, r, bits);
+    T = s.T;
+  }
+  // ordered pass: positions with composite >= T, ascending (contiguous segment per thread)
+  const int per = (len + SEL_THREADS - 1) / SEL_THREADS;
+  const int p0 = tid * per, p1 = min(len, p0 + per);
+  int cnt = 0;
+  for (int p = p0; p < p1; ++p) cnt += key(p) >= T;
+  int pos = block_excl_scan(cnt, s.wsum, &s_total);
+  int32_t* oi = out_idx + (size_t)row * k;
+  for (int p = p0; p < p1; ++p) {
+    const unsigned long long x = key(p);
+    if (x >= T) {
+      oi[pos] = p;
+      if (out_val) out_val[(size_t)row * k + pos] = __uint_as_float((uint32_t)(x >> 32));
+      ++pos;
+    }
+  }
+  const int total = s_total;
+  for (int i = total + tid; i < k; i += SEL_THREADS) {
+    oi[i] = -1;
+    if (out_val) out_val[(size_t)row * k + i] = 0.0f;
+  }
+  if (tid == 0) {
+    out_count[row] = total;
+    if (out_thresh) out_thresh[row] = ri.all ? 0ull : T;
+  }
+}
+
+// ------------------------------------------------------------------ merge (O13)
+struct UnionKey {
+  const float* val;
+  const int32_t* pos;
+  const int* off;  // prefix offsets per shard (shared memory), P+1 entries
+  int P, R, k, row;
+  __device__ unsigned long long operator()(int i) const {
+    int p = 0;
+    while (i >= off[p + 1]) ++p;
+    const size_t e = ((size_t)p * R + row) * k + (i - off[p]);
+    return composite(__float_as_uint(val[e]), pos[e] * P + p);
+  }
+};
+
+__global__ void __launch_bounds__(SEL_THREADS, 1) merge_kernel(
+    const float* __restrict__ cval, const int32_t* __restrict__ cpos,
+    const int32_t* __restrict__ ccnt, int P, int R, int k,
+    unsigned long long* __restrict__ out_thresh) {
+  extern __shared__ __align__(16) uint8_t sel_raw[];
+  SelSmem& s = *reinterpret_cast<SelSmem*>(sel_raw);
+  __shared__ int off[65];
+  const int row = blockIdx.x, tid = threadIdx.x;
+  if (tid == 0) {
+    off[0] = 0;
+    for (int p = 0; p < P; ++p) off[p + 1] = off[p] + min(ccnt[(size_t)p * R + row], k);
+  }
+  __syncthreads();
+  const int n = off[P];
+  if (n <= k) {
+    if (tid == 0) out_thresh[row] = 0ull;
+    return;
+  }
+  UnionKey key{cval, cpos, off, P, R, k, row};
+  unsigned long long prefix = 0;
+  int bits = 0, r = k, cm = n;
+  narrow_by_row_scan(s, key, n, prefix, bits, r, cm);
+  refine_in_smem(s, 0, s.n[0], r, bits);
+  if (tid == 0) out_thresh[row] = s.T;
+}
+
+// ------------------------------------------------------------------ filter (O13)
+__global__ void __launch_bounds__(SEL_THREADS) filter_kernel(
+    int32_t* __restrict__ idx, const float* __restrict__ val, int32_t* __restrict__ count,
+    const unsigned long long* __restrict__ thresh, int k, int stride, int offset) {
+  __shared__ int wsum[SEL_THREADS / 32];
+  __shared__ int total;
+  const int row = blockIdx.x, tid = threadIdx.x;
+  const int n = count[row];
+  const unsigned long long T = thresh[row];
+  constexpr int MAXPER = SPC_MAX_K / SEL_THREADS;
+  int keep[MAXPER];
+  int nk = 0;
+  const int per = (k + SEL_THREADS - 1) / SEL_THREADS;
+  const int p0 = tid * per;
+#pragma unroll
+  for (int i = 0; i < MAXPER; ++i) {
+    const int p = p0 + i;
+    keep[i] = -1;
+    if (i < per && p < n) {
+      const int id = idx[(size_t)row * k + p];
+      const unsigned long long x =
+          composite(__float_as_uint(val[(size_t)row * k + p]), id * stride + offset);
+      if (x >= T) {
+        keep[i] = id;
+        ++nk;
+      }
+    }
+  }
+  int pos = block_excl_scan(nk, wsum, &total);
+  __syncthreads();  // every read of idx happened before any write below
+#pragma unroll
+  for (int i = 0; i < MAXPER; ++i)
+    if (keep[i] >= 0) idx[(size_t)row * k + pos++] = keep[i];
+  __syncthreads();
+  for (int i = total + tid; i < k; i += SEL_THREADS) idx[(size_t)row * k + i] = -1;
+  if (tid == 0) count[row] = total;
+}
+
+int set_big_smem(const void* fn, size_t bytes) {
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e != cudaSuccess) {
+    set_cuda_error(e);
+    return SPC_E_CUDA;
+  }
+  return SPC_OK;
+}
+
+}  // namespace
+}  // namespace spc
+
+using namespace spc;
+
+extern "C" size_t spc_topk_workspace(int B, int G, int n_cols, int k) {
+  (void)n_cols;
+  (void)k;
+  if (B <= 0 || G <= 0) return 0;
+  return topk_ws_layout(nullptr, B * G).bytes;
+}
+
+extern "C" int spc_topk(const float* val, const int32_t* seq_len, int B, int G, int n_cols, int k,
+                        int force_last, int id_stride, int id_offset, int32_t* out_idx,
+                        float* out_val, int32_t* out_count, uint64_t* out_thresh, void* ws,
+                        size_t ws_bytes, spc_stream_t stream) {
+  if (!val || !seq_len || !out_idx || !out_count) return SPC_E_NULL;
+  if (B <= 0 || G <= 0 || n_cols <= 0) return SPC_E_SHAPE;
+  if (k < 1 || k > SPC_MAX_K) return SPC_E_BUDGET;
+  if (n_cols >= SPC_MAX_SEQ || id_stride < 1 || id_offset < 0) return SPC_E_RANGE;
+  if ((long long)n_cols * id_stride + id_offset >= 0x7FFFFFFFLL) return SPC_E_RANGE;
+  if (!ws || ws_bytes < spc_topk_workspace(B, G, n_cols, k)) return SPC_E_WORKSPACE;
+  cudaStream_t st = as_stream(stream);
+  const int R = B * G;
+  TopkWs w = topk_ws_layout(ws, R);
+  cudaError_t e = cudaMemsetAsync(w.hist, 0, sizeof(unsigned) * (size_t)R * NBIN0, st);
+  if (e != cudaSuccess) return launched(e);
+  dim3 grid((n_cols + TK_TILE - 1) / TK_TILE, R);
+  hist_kernel<<<grid, TK_THREADS, 0, st>>>(val, seq_len, G, n_cols, force_last, w.hist);
+  SPC_TRY(launched());
+  find_kernel<<<R, 32, 0, st>>>(w.hist, seq_len, G, n_cols, k, w.info, w.ccount);
+  SPC_TRY(launched());
+  collect_kernel<<<grid, TK_THREADS, 0, st>>>(val, seq_len, G, n_cols, force_last, id_stride,
+                                              id_offset, w.info, w.ccount, w.cand);
+  SPC_TRY(launched());
+  static bool attr = false;
+  if (!attr) {
+    SPC_TRY(set_big_smem((const void*)select_kernel, sizeof(SelSmem)));
+    attr = true;
+  }
+  select_kernel<<<R, SEL_THREADS, sizeof(SelSmem), st>>>(
+      val, n_cols, k, force_last, id_stride, id_offset, w.info, w.ccount, w.cand, out_idx, out_val,
+      out_count, (unsigned long long*)out_thresh);
+  return launched();
+}
+
+extern "C" size_t spc_topk_merge_workspace(int P, int R, int k) {
+  (void)P;
+  (void)R;
+  (void)k;
+  return 256;
+}
+
+extern "C" int spc_topk_merge(const float* cand_val, const int32_t* cand_pos,
+                              const int32_t* cand_count, int P, int R, int k, uint64_t* out_thresh,
+                              void* ws, size_t ws_bytes, spc_stream_t stream) {
+  (void)ws;
+  (void)ws_bytes;
+  if (!cand_val || !cand_pos || !cand_count || !out_thresh) return SPC_E_NULL;
+  if (P < 1 || P > 64 || R < 1) return SPC_E_SHAPE;
+  if (k < 1 || k > SPC_MAX_K) return SPC_E_BUDGET;
+  static bool attr = false;
+  if (!attr) {
+    SPC_TRY(set_big_smem((const void*)merge_kernel, sizeof(SelSmem)));
+    attr = true;
+  }
+  merge_kernel<<<R, SEL_THREADS, sizeof(SelSmem), as_stream(stream)>>>(
+      cand_val, cand_pos, cand_count, P, R, k, (unsigned long long*)out_thresh);
+  return launched();
+}
+
+extern "C" int spc_topk_filter(int32_t* idx, const float* val, int32_t* count,
+                               const uint64_t* thresh, int R, int k, int id_stride, int id_offset,
+                               spc_stream_t stream) {
+  if (!idx || !val || !count || !thresh) return SPC_E_NULL;
+  if (R < 1) return SPC_E_SHAPE;
+  if (k < 1 || k > SPC_MAX_K) return SPC_E_BUDGET;
+  filter_kernel<<<R, SEL_THREADS, 0, as_stream(stream)>>>(
+      idx, val, count, (const unsigned long long*)thresh, k, id_stride, id_offset);
+  return launched();
+}

@@ -1,0 +1,146 @@
+"""One SpeContext decode step on one GPU, built only from libspc calls.
+
+Step: spc_score (LOGITS, NORM, GROUP) -> spc_topk (force the
+newest token, R10) -> spc_elastic_diff against the previous step's selection
+ -> [SLOTS mode: spc_gather_kv of the new rows into budget slots] ->
+spc_sparse_decode_attn over all L layers (one launch).
+
+The step state (previous selection, slot map) ping-pongs between two buffers,
+so two CUDA graphs (even / odd step) replay the whole step with one launch
+each.  Inputs are written into fixed device buffers (``q_ret``, ``q_llm``)
+before a replay; ``step_host`` is the end-to-end public call that takes pinned
+host inputs and returns host outputs.
+"""
+from __future__ import annotations
+
+import math
+
+import torch
+
+from . import spc
+
+
+class DecodeStep:
+    def __init__(self, kr: torch.Tensor, k_layers, v_layers, seq_len: torch.Tensor, L: int,
+                 Hq: int, k: int, mode: str = "indexed", force_last: bool = True, scale=None,
+                 kv_rows=None, k_src_layers=None, v_src_layers=None):
+        """kr: retrieval keys [B][G][Smax][D] bf16.  k_layers/v_layers: L tensors [B][G][rows][D]
+        (INDEXED: the full caches; SLOTS: the budget buffers [B][G][k][D], with
+        k_src_layers/v_src_layers the full caches, device or mapped host)."""
+        self.dev = kr.device
+        self.B, self.G, self.Smax, self.D = kr.shape
+        self.L, self.Hq, self.k = L, Hq, k
+        self.alpha = Hq // self.G
+        self.mode = mode
+        self.force_last = force_last
+        self.scale = float(torch.tensor(1.0 / math.sqrt(self.D), dtype=torch.float32)) \
+            if scale is None else float(scale)
+        self.kr, self.seq_len = kr, seq_len
+        self.k_layers, self.v_layers = list(k_layers), list(v_layers)
+        self.kv_dtype = self.k_layers[0].dtype
+        self.rows = kv_rows if kv_rows is not None else self.k_layers[0].shape[2]
+        self.k_tab = spc.ptr_table(self.k_layers, self.dev)
+        self.v_tab = spc.ptr_table(self.v_layers, self.dev)
+        if mode == "slots":
+            assert k_src_layers is not None
+            self.k_src, self.v_src = list(k_src_layers), list(v_src_layers)
+            # pinned host tensors are device-addressable under UVA (zero-copy PCIe reads)
+            self.k_src_tab = spc.ptr_table(self.k_src, self.dev)
+            self.v_src_tab = spc.ptr_table(self.v_src, self.dev)
+            self.src_rows = self.k_src[0].shape[2]
+        B, G, Hq, D, dev = self.B, self.G, Hq, self.D, self.dev
+        f32, i32 = torch.float32, torch.int32
+        self.q_ret = torch.zeros((B, Hq, D), dtype=torch.bfloat16, device=dev)
+        self.q_llm = torch.zeros((L, B, Hq, D), dtype=self.kv_dtype, device=dev)
+        self.logits = torch.zeros((B, Hq, self.Smax), dtype=f32, device=dev)
+        self.head_max = torch.zeros((B, Hq), dtype=f32, device=dev)
+        self.head_sumfix = torch.zeros((B, Hq), dtype=torch.int64, device=dev)
+        self.gs = torch.zeros((B, G, self.Smax), dtype=f32, device=dev)
+        self.idx = [torch.full((B, G, k), -1, dtype=i32, device=dev) for _ in range(2)]
+        self.cnt = [torch.zeros((B, G), dtype=i32, device=dev) for _ in range(2)]
+        self.load_tok = torch.full((B, G, k), -1, dtype=i32, device=dev)
+        self.n_load = torch.zeros((B, G), dtype=i32, device=dev)
+        self.slot_tok = torch.full((B, G, k), -1, dtype=i32, device=dev) if mode == "slots" else None
+        self.load_slot = torch.full((B, G, k), -1, dtype=i32, device=dev) if mode == "slots" else None
+        self.out = torch.zeros((L, B, Hq, D), dtype=f32, device=dev)
+        self.lse = torch.zeros((L, B, Hq), dtype=f32, device=dev)
+        self.ws_score = spc.alloc_workspace(spc.score_workspace(B, Hq, self.Smax), dev)
+        self.ws_topk = spc.alloc_workspace(spc.topk_workspace(B, G, self.Smax, k), dev)
+        self.ws_attn = spc.alloc_workspace(spc.attn_workspace(L, B, Hq, D, k), dev)
+        self.parity = 0
+        self.graphs = [None, None]
+
+    # ------------------------------------------------------------------ eager
+    def enqueue(self, parity: int, stream=None):
+        """Enqueue one step writing the selection into idx[parity] (prev = idx[1-parity])."""
+        cur, prev = parity, 1 - parity
+        spc.score(self.q_ret, self.kr, self.seq_len, self.G, self.scale, self.logits,
+                  self.head_max, self.head_sumfix, self.gs, self.ws_score, stream=stream)
+        spc.topk(self.gs, self.seq_len, self.k, self.idx[cur], self.cnt[cur], self.ws_topk,
+                 force_last=self.force_last, stream=stream)
+        spc.elastic_diff(self.idx[prev], self.cnt[prev], self.idx[cur], self.cnt[cur],
+                         self.load_tok, self.n_load, slot_tok=self.slot_tok,
+                         load_slot=self.load_slot, stream=stream)
+        if self.mode == "slots":
+            spc.gather_kv(self.k_src_tab, self.v_src_tab, self.L, self.B, self.G, self.D,
+                          self.src_rows, self.k, self.load_tok, self.load_slot, self.n_load,
+                          self.k_tab, self.v_tab,
+                          dtype=spc.BF16 if self.kv_dtype == torch.bfloat16 else spc.F32,
+                          stream=stream)
+            spc.sparse_decode_attn(self.q_llm, self.k_tab, self.v_tab, spc.KV_SLOTS, None,
+                                   self.cnt[cur], self.k, self.k, self.scale, self.out, self.lse,
+                                   self.ws_attn, self.G, stream=stream)
+        else:
+            spc.sparse_decode_attn(self.q_llm, self.k_tab, self.v_tab, spc.KV_INDEXED,
+                                   self.idx[cur], self.cnt[cur], self.rows, self.k, self.scale,
+                                   self.out, self.lse, self.ws_attn, self.G, stream=stream)
+
+    def step(self, q_ret=None, q_llm=None, use_graph: bool = False):
+        """Run one decode step on device tensors (copied into the step's input buffers)."""
+        if q_ret is not None:
+            self.q_ret.copy_(q_ret, non_blocking=True)
+        if q_llm is not None:
+            self.q_llm.copy_(q_llm, non_blocking=True)
+        p = self.parity
+        if use_graph:
+            if self.graphs[p] is None:
+                self.capture()
+            self.graphs[p].replay()
+        else:
+            self.enqueue(p)
+        self.parity ^= 1
+        return self.idx[p], self.cnt[p]
+
+    def capture(self):
+        """Capture the even and odd step as two CUDA graphs (after an eager warm-up)."""
+        s = torch.cuda.Stream(device=self.dev)
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            for p in (0, 1):
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=s):
+                    self.enqueue(p)
+                self.graphs[p] = g
+        torch.cuda.current_stream().wait_stream(s)
+
+    def reset_state(self):
+        for c in self.cnt:
+            c.zero_()
+        for i in self.idx:
+            i.fill_(-1)
+        if self.slot_tok is not None:
+            self.slot_tok.fill_(-1)
+        self.parity = 0
+
+    # ------------------------------------------------------------------ end to end
+    def step_host(self, q_ret_host: torch.Tensor, q_llm_host: torch.Tensor,
+                  out_host: torch.Tensor, use_graph: bool = True):
+        """Public end-to-end call: pinned host inputs -> step -> host attention output.
+        Returns (bytes host->device, bytes device->host)."""
+        self.q_ret.copy_(q_ret_host, non_blocking=True)
+        self.q_llm.copy_(q_llm_host, non_blocking=True)
+        self.step(use_graph=use_graph)
+        out_host.copy_(self.out, non_blocking=True)
+        return (q_ret_host.numel() * q_ret_host.element_size() +
+                q_llm_host.numel() * q_llm_host.element_size(),
+                out_host.numel() * out_host.element_size())

@@ -1,0 +1,210 @@
+"""ctypes binding of libspc.so (include/spc.h) — argument marshalling only.
+
+Every function has the name of the C entry point without the ``spc_`` prefix
+and takes torch tensors (device memory) plus plain ints/floats; it passes
+their data pointers and the current CUDA stream to the library and raises
+``SpcError`` on a non-OK status.  No arithmetic of the method happens here.
+There is no CPU fallback: if libspc.so is missing or CUDA is unavailable,
+``lib()`` raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libspc.so")
+
+BF16, F32 = 0, 1
+SCORE_LOGITS, SCORE_NORM, SCORE_GROUP, SCORE_ALL = 1, 2, 4, 7
+KV_INDEXED, KV_SLOTS = 0, 1
+MAX_K = 4096
+
+EXPORTS = [
+    "spc_status_string", "spc_last_cuda_error", "spc_version", "spc_launch_count",
+    "spc_score_workspace", "spc_score", "spc_topk_workspace", "spc_topk",
+    "spc_topk_merge_workspace", "spc_topk_merge", "spc_topk_filter", "spc_elastic_diff",
+    "spc_gather_kv", "spc_attn_workspace", "spc_sparse_decode_attn", "spc_attn_merge",
+]
+
+
+class SpcError(RuntimeError):
+    pass
+
+
+_lib = None
+
+
+def load_library(path: str = LIB_PATH):
+    """Load libspc.so and declare signatures (works without a GPU)."""
+    if not os.path.exists(path):
+        raise SpcError(f"{path} not found: build it with `python -m paper_2512_00722_b200.build` "
+                       "(there is no CPU fallback)")
+    L = ctypes.CDLL(path)
+    P, i32, f32, sz, u64 = (ctypes.c_void_p, ctypes.c_int, ctypes.c_float, ctypes.c_size_t,
+                            ctypes.c_uint64)
+    L.spc_status_string.argtypes = [i32]
+    L.spc_status_string.restype = ctypes.c_char_p
+    L.spc_last_cuda_error.restype = ctypes.c_char_p
+    L.spc_version.restype = i32
+    L.spc_launch_count.restype = u64
+    L.spc_score_workspace.argtypes = [i32, i32, i32]
+    L.spc_score_workspace.restype = sz
+    L.spc_score.argtypes = [i32, P, P, P, i32, i32, i32, i32, i32, f32, i32, P, P, P, P, P, sz, P]
+    L.spc_topk_workspace.argtypes = [i32, i32, i32, i32]
+    L.spc_topk_workspace.restype = sz
+    L.spc_topk.argtypes = [P, P, i32, i32, i32, i32, i32, i32, i32, P, P, P, P, P, sz, P]
+    L.spc_topk_merge_workspace.argtypes = [i32, i32, i32]
+    L.spc_topk_merge_workspace.restype = sz
+    L.spc_topk_merge.argtypes = [P, P, P, i32, i32, i32, P, P, sz, P]
+    L.spc_topk_filter.argtypes = [P, P, P, P, i32, i32, i32, i32, P]
+    L.spc_elastic_diff.argtypes = [P, P, P, P, i32, i32, i32, P, P, P, P, P, P, P]
+    L.spc_gather_kv.argtypes = [i32, P, P, i32, i32, i32, i32, i32, i32, i32, i32, P, P, P, P, P,
+                                P]
+    L.spc_attn_workspace.argtypes = [i32, i32, i32, i32, i32]
+    L.spc_attn_workspace.restype = sz
+    L.spc_sparse_decode_attn.argtypes = [i32, P, P, P, i32, P, P, i32, i32, i32, i32, i32, i32,
+                                         i32, i32, i32, f32, P, P, P, sz, P]
+    L.spc_attn_merge.argtypes = [P, P, i32, i32, i32, P, P, P]
+    for name in EXPORTS:  # every symbol must resolve (raises AttributeError otherwise)
+        getattr(L, name)
+    return L
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        _lib = load_library()
+    return _lib
+
+
+def _check(rc: int, what: str):
+    if rc != 0:
+        msg = lib().spc_status_string(rc).decode()
+        if rc == 8:
+            msg += " — " + lib().spc_last_cuda_error().decode()
+        raise SpcError(f"{what}: {msg}")
+
+
+def _p(t):
+    if t is None:
+        return None
+    if isinstance(t, int):
+        return ctypes.c_void_p(t)
+    assert t.is_contiguous(), "libspc tensors must be contiguous"
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _s(stream):
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream))
+
+
+def _dtype_code(t: torch.Tensor) -> int:
+    if t.dtype == torch.bfloat16:
+        return BF16
+    if t.dtype == torch.float32:
+        return F32
+    raise SpcError(f"unsupported dtype {t.dtype}")
+
+
+def launch_count() -> int:
+    return int(lib().spc_launch_count())
+
+
+def version() -> int:
+    return int(lib().spc_version())
+
+
+def ptr_table(tensors, device) -> torch.Tensor:
+    """Device array of data pointers (the per-layer pointer tables of the ABI)."""
+    return torch.tensor([int(t.data_ptr()) for t in tensors], dtype=torch.int64, device=device)
+
+
+# ------------------------------------------------------------------ workspaces
+def score_workspace(B: int, Hq: int, Smax: int) -> int:
+    return int(lib().spc_score_workspace(B, Hq, Smax))
+
+
+def topk_workspace(B: int, G: int, n_cols: int, k: int) -> int:
+    return int(lib().spc_topk_workspace(B, G, n_cols, k))
+
+
+def topk_merge_workspace(P: int, R: int, k: int) -> int:
+    return int(lib().spc_topk_merge_workspace(P, R, k))
+
+
+def attn_workspace(L: int, B: int, Hq: int, D: int, k: int) -> int:
+    return int(lib().spc_attn_workspace(L, B, Hq, D, k))
+
+
+def alloc_workspace(nbytes: int, device) -> torch.Tensor:
+    """Workspaces must start zero-filled (the library leaves them zero-filled)."""
+    return torch.zeros(max(int(nbytes), 1), dtype=torch.uint8, device=device)
+
+
+# ------------------------------------------------------------------ calls
+def score(q, kr, seq_len, G: int, scale: float, logits, head_max, head_sumfix, group_score, ws,
+          phases: int = SCORE_ALL, stream=None):
+    B, Hq, D = q.shape
+    Smax = kr.shape[2]
+    _check(lib().spc_score(_dtype_code(q), _p(q), _p(kr), _p(seq_len), B, Hq, G, D, Smax,
+                           float(scale), phases, _p(logits), _p(head_max), _p(head_sumfix),
+                           _p(group_score), _p(ws), ws.numel(), _s(stream)), "spc_score")
+
+
+def topk(val, seq_len, k: int, out_idx, out_count, ws, out_val=None, out_thresh=None,
+         force_last: bool = False, id_stride: int = 1, id_offset: int = 0, stream=None):
+    B, G, n_cols = val.shape
+    _check(lib().spc_topk(_p(val), _p(seq_len), B, G, n_cols, k, int(force_last), id_stride,
+                          id_offset, _p(out_idx), _p(out_val), _p(out_count), _p(out_thresh),
+                          _p(ws), ws.numel(), _s(stream)), "spc_topk")
+
+
+def topk_merge(cand_val, cand_pos, cand_count, k: int, out_thresh, ws=None, stream=None):
+    P, R = cand_count.shape
+    _check(lib().spc_topk_merge(_p(cand_val), _p(cand_pos), _p(cand_count), P, R, k,
+                                _p(out_thresh), _p(ws), 0 if ws is None else ws.numel(),
+                                _s(stream)), "spc_topk_merge")
+
+
+def topk_filter(idx, val, count, thresh, k: int, id_stride: int, id_offset: int, stream=None):
+    R = count.numel()
+    _check(lib().spc_topk_filter(_p(idx), _p(val), _p(count), _p(thresh), R, k, id_stride,
+                                 id_offset, _s(stream)), "spc_topk_filter")
+
+
+def elastic_diff(prev_idx, prev_count, cur_idx, cur_count, load_tok, n_load, slot_tok=None,
+                 load_slot=None, evict_tok=None, n_evict=None, stream=None):
+    B, G, k = cur_idx.shape
+    _check(lib().spc_elastic_diff(_p(prev_idx), _p(prev_count), _p(cur_idx), _p(cur_count), B, G,
+                                  k, _p(slot_tok), _p(load_tok), _p(load_slot), _p(n_load),
+                                  _p(evict_tok), _p(n_evict), _s(stream)), "spc_elastic_diff")
+
+
+def gather_kv(k_src_tab, v_src_tab, L: int, B: int, G: int, D: int, Smax: int, k: int,
+              load_tok, load_slot, n_load, k_buf_tab, v_buf_tab, layer_begin: int = 0,
+              layer_end=None, dtype: int = BF16, stream=None):
+    layer_end = L if layer_end is None else layer_end
+    _check(lib().spc_gather_kv(dtype, _p(k_src_tab), _p(v_src_tab), L, B, G, D, Smax, k,
+                               layer_begin, layer_end, _p(load_tok), _p(load_slot), _p(n_load),
+                               _p(k_buf_tab), _p(v_buf_tab), _s(stream)), "spc_gather_kv")
+
+
+def sparse_decode_attn(q, k_tab, v_tab, kv_mode: int, idx, count, rows: int, k: int, scale: float,
+                       out, lse, ws, G: int, layer_begin: int = 0, layer_end=None, stream=None):
+    L, B, Hq, D = q.shape
+    layer_end = L if layer_end is None else layer_end
+    _check(lib().spc_sparse_decode_attn(_dtype_code(q), _p(q), _p(k_tab), _p(v_tab), kv_mode,
+                                        _p(idx), _p(count), L, layer_begin, layer_end, B, Hq, G, D,
+                                        rows, k, float(scale), _p(out), _p(lse), _p(ws),
+                                        ws.numel(), _s(stream)), "spc_sparse_decode_attn")
+
+
+def attn_merge(o_parts, lse_parts, out, lse_out=None, stream=None):
+    P, n, D = o_parts.shape
+    _check(lib().spc_attn_merge(_p(o_parts), _p(lse_parts), P, n, D, _p(out), _p(lse_out),
+                                _s(stream)), "spc_attn_merge")

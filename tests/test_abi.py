@@ -1,0 +1,66 @@
+"""CPU-side checks of the boundary: libspc.so builds, loads without a GPU and exports every
+entry point include/spc.h declares; host-side argument validation returns the documented
+status codes before anything is enqueued."""
+import ctypes
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_symbols():
+    hdr = open(os.path.join(ROOT, "include", "spc.h")).read()
+    hdr = re.sub(r"/\*.*?\*/", "", hdr, flags=re.S)
+    return sorted(set(re.findall(r"\b(spc_[a-z0-9_]+)\s*\(", hdr)))
+
+
+@pytest.fixture(scope="module")
+def libspc():
+    from paper_2512_00722_b200 import build, spc
+    build.build()
+    return spc.load_library()
+
+
+def test_header_declares_the_north_star_calls():
+    syms = declared_symbols()
+    for s in ("spc_score", "spc_topk", "spc_elastic_diff", "spc_gather_kv",
+              "spc_sparse_decode_attn"):
+        assert s in syms
+
+
+def test_library_exports_every_declared_symbol(libspc):
+    for s in declared_symbols():
+        assert hasattr(libspc, s), s
+    from paper_2512_00722_b200 import spc
+    assert sorted(spc.EXPORTS) == declared_symbols()
+
+
+def test_status_strings_and_version(libspc):
+    assert libspc.spc_version() == 100
+    assert libspc.spc_status_string(0) == b"SPC_OK"
+    assert b"WORKSPACE" in libspc.spc_status_string(6)
+
+
+def test_host_validation_without_gpu(libspc):
+    """Argument errors are detected on the host, before any CUDA call."""
+    P = ctypes.c_void_p(16)
+    st = ctypes.c_void_p(0)
+    # NULL query
+    assert libspc.spc_score(0, None, P, P, 1, 4, 1, 64, 4096, 0.125, 7, P, P, P, P, P, 1 << 20, st) == 1
+    # Hq % G != 0
+    assert libspc.spc_score(0, P, P, P, 1, 5, 2, 64, 4096, 0.125, 7, P, P, P, P, P, 1 << 20, st) == 2
+    # unsupported head dim
+    assert libspc.spc_score(0, P, P, P, 1, 4, 1, 96, 4096, 0.125, 7, P, P, P, P, P, 1 << 20, st) == 7
+    # workspace too small
+    assert libspc.spc_score(0, P, P, P, 1, 4, 1, 64, 4096, 0.125, 7, P, P, P, P, P, 8, st) == 6
+    # budget out of range
+    assert libspc.spc_topk(P, P, 1, 1, 100, 0, 0, 1, 0, P, None, P, None, P, 1 << 30, st) == 3
+    assert libspc.spc_topk(P, P, 1, 1, 100, 5000, 0, 1, 0, P, None, P, None, P, 1 << 30, st) == 3
+    assert libspc.spc_elastic_diff(P, P, P, P, 1, 1, 0, None, P, None, P, None, None, st) == 3
+    # layer range
+    assert libspc.spc_gather_kv(0, P, P, 4, 1, 1, 128, 100, 16, 3, 2, P, P, P, P, P, st) == 4
+    assert libspc.spc_sparse_decode_attn(0, P, P, P, 0, P, P, 2, 0, 3, 1, 4, 1, 128, 100, 16,
+                                         0.1, P, None, P, 1 << 30, st) == 4
+    assert libspc.spc_score_workspace(1, 32, 32768) > 0

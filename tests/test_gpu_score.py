@@ -1,0 +1,80 @@
+"""GPU parity of spc_score (O1..O6) against the CPU oracle: BIT-EXACT logits, head maxima,
+int64 normalisers and group scores, on seeded synthetic inputs of the paper's shapes
+(config A; every head dim x alpha the library supports; ragged seq_len; a tail that is
+not a multiple of the 256-row tile; config B at full size)."""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from paper_2512_00722_b200 import spc, synth
+
+pytestmark = pytest.mark.gpu
+
+
+def run_score(q, kr, seq, G, scale):
+    dev = kr.device
+    B, Hq, D = q.shape
+    Smax = kr.shape[2]
+    lg = torch.zeros((B, Hq, Smax), dtype=torch.float32, device=dev)
+    hm = torch.zeros((B, Hq), dtype=torch.float32, device=dev)
+    F = torch.zeros((B, Hq), dtype=torch.int64, device=dev)
+    gs = torch.zeros((B, G, Smax), dtype=torch.float32, device=dev)
+    ws = spc.alloc_workspace(spc.score_workspace(B, Hq, Smax), dev)
+    spc.score(q, kr, seq, G, scale, lg, hm, F, gs, ws)
+    torch.cuda.synchronize()
+    return lg.cpu().numpy(), hm.cpu().numpy(), F.cpu().numpy(), gs.cpu().numpy()
+
+
+def check(oracle, q, kr, seq_list, G, scale):
+    dev = torch.device("cuda")
+    seq = torch.tensor(seq_list, dtype=torch.int32, device=dev)
+    lg, hm, F, gs = run_score(q.to(dev), kr.to(dev), seq, G, scale)
+    olg, ohm, oF, ogs = oracle.score(synth.bf16_bits(q), synth.bf16_bits(kr), seq_list, G, scale)
+    for b, S in enumerate(seq_list):
+        assert np.array_equal(lg[b, :, :S].view(np.uint32), olg[b, :, :S].view(np.uint32)), b
+    assert np.array_equal(hm.view(np.uint32), ohm.view(np.uint32))
+    assert np.array_equal(F, oF)
+    assert np.array_equal(gs.view(np.uint32), ogs.view(np.uint32))
+    return gs
+
+
+def f32(x):
+    return float(np.float32(x))
+
+
+def test_score_config_a(oracle):
+    c = synth.CONFIGS["A"]
+    kr = synth.retrieval_keys(1, c["G"], c["S"], c["D"], seed=synth.BASE_SEED)
+    q = synth.retrieval_queries(2, 1, c["Hq"], c["G"], c["D"], seed=synth.BASE_SEED)
+    for s in range(2):
+        check(oracle, q[s], kr, [c["S"]], c["G"], f32(1 / math.sqrt(c["D"])))
+
+
+@pytest.mark.parametrize("D", [64, 128])
+@pytest.mark.parametrize("alpha,G", [(1, 3), (2, 2), (4, 2), (8, 1)])
+def test_score_shapes_ragged(oracle, D, alpha, G):
+    B, Smax = 3, 1000  # 1000 = 3 full 256-row tiles + a ragged tail
+    Hq = alpha * G
+    kr = synth.retrieval_keys(B, G, Smax, D, seed=D + alpha)
+    q = synth.retrieval_queries(1, B, Hq, G, D, seed=D + alpha)[0]
+    check(oracle, q, kr, [1000, 1, 517], G, f32(1 / math.sqrt(D)))
+
+
+def test_score_extreme_logits_and_ties(oracle):
+    """Large query scale (logits ~1e3, most weights underflow to 0 in O3) and duplicated keys."""
+    B, G, Hq, D, S = 1, 2, 8, 128, 700
+    kr = synth.duplicate_rows(synth.retrieval_keys(B, G, S, D, seed=5), 200, seed=5)
+    q = (synth.retrieval_queries(1, B, Hq, G, D, seed=5)[0].float() * 40).to(torch.bfloat16)
+    check(oracle, q, kr, [S], G, 0.3)
+
+
+def test_score_config_b_full_size(oracle):
+    """Config B (8B shape, 32K context) at full size, bit-exact against the oracle."""
+    c = synth.CONFIGS["B"]
+    kr = synth.retrieval_keys(1, c["G"], c["S"], c["D"], seed=synth.BASE_SEED + 1,
+                              device="cuda")
+    q = synth.retrieval_queries(1, 1, c["Hq"], c["G"], c["D"], seed=synth.BASE_SEED + 1,
+                                device="cuda")[0]
+    check(oracle, q.cpu(), kr.cpu(), [c["S"]], c["G"], f32(1 / math.sqrt(c["D"])))
