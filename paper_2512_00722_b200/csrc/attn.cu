@@ -31,13 +31,14 @@ constexpr float LOG2E = 1.4426950408889634f;
 constexpr float LN2 = 0.6931471805599453f;
 
 struct AttnWs {
-  float* part_o;   // [L][B][Hq][nsplit][D]  (unnormalised o relative to m)
-  float* part_ml;  // [L][B][Hq][nsplit][2]  (m in log2 units, l)
+  float* part_o;   // [L][B][Hq][segstride][D]  (unnormalised o relative to m)
+  float* part_ml;  // [L][B][Hq][segstride][2]  (m in log2 units, l)
   unsigned* cnt;   // [L][B][G]
+  int segstride;   // max segments (partials) per group
   size_t bytes;
 };
 AttnWs attn_ws_layout(void* ws, int L, int B, int Hq, int D, int k) {
-  const size_t ns = (k + AT_ROWS - 1) / AT_ROWS;
+  const size_t ns = (k + 63) / 64 + 2;  // >= both the split count and the persistent segments
   uint8_t* p = (uint8_t*)ws;
   AttnWs w;
   size_t off = 0;
@@ -47,6 +48,7 @@ AttnWs attn_ws_layout(void* ws, int L, int B, int Hq, int D, int k) {
   off = align_up(off + sizeof(float) * 2 * (size_t)L * B * Hq * ns, 256);
   w.cnt = (unsigned*)(p + off);
   off = align_up(off + sizeof(unsigned) * (size_t)L * B * Hq, 256);
+  w.segstride = (int)ns;
   w.bytes = off;
   return w;
 }
@@ -81,12 +83,12 @@ __device__ __forceinline__ void mma_bf16(float (&c)[4], uint32_t a0, uint32_t a2
 // the last CTA of the group.  m is in log2 units.
 template <int D, int ALPHA>
 __device__ void merge_partials(const float* part_o, const float* part_ml, int nsplit,
-                               size_t head_base /* (lr*B + b)*Hq + g*ALPHA */, float* out,
-                               float* lse, size_t out_head_base) {
-  for (int i = threadIdx.x; i < ALPHA * D; i += blockDim.x) {
+                               int segstride, size_t head_base /* (lr*B + b)*Hq + g*ALPHA */, float* out,
+                               float* lse, size_t out_head_base, int nthreads) {
+  for (int i = threadIdx.x; i < ALPHA * D; i += nthreads) {
     const int j = i / D, d = i % D;
     const size_t h = head_base + j;
-    const float* ml = part_ml + h * nsplit * 2;
+    const float* ml = part_ml + h * segstride * 2;
     float M = -INFINITY;
     for (int s = 0; s < nsplit; ++s) M = fmaxf(M, __ldcg(ml + 2 * s));
     float den = 0.f, num = 0.f;
@@ -96,7 +98,7 @@ __device__ void merge_partials(const float* part_o, const float* part_ml, int ns
         if (m == -INFINITY) continue;
         const float w = exp2f(m - M);
         den += w * __ldcg(ml + 2 * s + 1);
-        num += w * __ldcg(part_o + (h * nsplit + s) * D + d);
+        num += w * __ldcg(part_o + (h * segstride + s) * D + d);
       }
     }
     out[(out_head_base + j) * D + d] = den > 0.f ? num / den : 0.f;
@@ -104,189 +106,7 @@ __device__ void merge_partials(const float* part_o, const float* part_ml, int ns
   }
 }
 
-// ---------------------------------------------------------------- bf16 / mma path
-template <int D, int ALPHA>
-__global__ void __launch_bounds__(AT_THREADS) attn_bf16_kernel(
-    const uint16_t* __restrict__ q, const void* const* __restrict__ k_layers,
-    const void* const* __restrict__ v_layers, int kv_mode, const int32_t* __restrict__ idx,
-    const int32_t* __restrict__ count, int layer_begin, int B, int G, int rows, int kbud,
-    float scale, int nsplit, float* __restrict__ part_o, float* __restrict__ part_ml,
-    unsigned* __restrict__ cnt, float* __restrict__ out, float* __restrict__ lse) {
-  constexpr int RS = D + 8;  // padded row stride in bf16 elements (conflict-free ldmatrix)
-  constexpr int Hq_ = ALPHA;
-  extern __shared__ __align__(128) uint8_t at_smem[];
-  uint16_t* Ks = (uint16_t*)at_smem;                   // [AT_ROWS][RS]
-  uint16_t* Vs = (uint16_t*)at_smem + AT_ROWS * RS;    // [AT_ROWS][RS]
-  float(*red_o)[ALPHA][D] = (float(*)[ALPHA][D])at_smem;  // aliases Ks once QK is done
-  __shared__ __align__(8) uint64_t bar[2];
-  __shared__ float red_m[4][8], red_l[4][8];
-  __shared__ int flag;
-  static_assert(sizeof(float) * 4 * ALPHA * D <= sizeof(uint16_t) * AT_ROWS * RS, "red_o alias");
-
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int gid = lane >> 2, tig = lane & 3;
-  const int split = blockIdx.x, bg = blockIdx.y, lr = blockIdx.z;
-  const int l = layer_begin + lr;
-  const int b = bg / G, g = bg % G;
-  const int Hq = G * ALPHA;
-  const int n_sel = min(count[bg], kbud);
-  const int r0 = split * AT_ROWS;
-  const int nrows = max(0, min(AT_ROWS, n_sel - r0));
-  const size_t head_base = ((size_t)lr * B + b) * Hq + g * ALPHA;
-
-  if (tid == 0) {
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
-    fence_mbar_init();
-  }
-  __syncthreads();
-  if (nrows > 0) {
-    const uint16_t* Kl = (const uint16_t*)k_layers[l] + (size_t)bg * rows * D;
-    const uint16_t* Vl = (const uint16_t*)v_layers[l] + (size_t)bg * rows * D;
-    if (tid < nrows) {
-      const int tok = kv_mode == SPC_KV_INDEXED ? idx[(size_t)bg * kbud + r0 + tid] : r0 + tid;
-      bulk_g2s(Ks + tid * RS, Kl + (size_t)tok * D, D * 2, &bar[0]);
-      bulk_g2s(Vs + tid * RS, Vl + (size_t)tok * D, D * 2, &bar[1]);
-    } else {
-      uint4 z = make_uint4(0, 0, 0, 0);
-#pragma unroll
-      for (int i = 0; i < D / 8; ++i) {
-        *(uint4*)(Ks + tid * RS + i * 8) = z;
-        *(uint4*)(Vs + tid * RS + i * 8) = z;
-      }
-    }
-    if (tid == 0) {
-      mbar_arrive_expect_tx(&bar[0], nrows * D * 2);
-      mbar_arrive_expect_tx(&bar[1], nrows * D * 2);
-    }
-  }
-  // query fragments (A operand): row = head gid (< ALPHA real), k = d
-  constexpr int KS = D / 16;
-  uint32_t qa0[KS], qa2[KS];
-  {
-    const uint16_t* qh = q + (((size_t)l * B + b) * Hq + g * ALPHA + (gid < ALPHA ? gid : 0)) * D;
-#pragma unroll
-    for (int s = 0; s < KS; ++s) {
-      const uint32_t x0 = *(const uint32_t*)(qh + s * 16 + 2 * tig);
-      const uint32_t x2 = *(const uint32_t*)(qh + s * 16 + 8 + 2 * tig);
-      qa0[s] = gid < ALPHA ? x0 : 0u;
-      qa2[s] = gid < ALPHA ? x2 : 0u;
-    }
-  }
-  float mloc = -INFINITY, lloc = 0.f;
-  float p[4][2];  // this lane's scores: 4 n-tiles x 2 rows, head gid
-  if (nrows > 0) {
-    __syncthreads();  // zero-filled padding rows visible
-    mbar_wait(&bar[0], 0);
-    const uint32_t kb = smem_u32(Ks);
-    const float sl2 = scale * LOG2E;
-#pragma unroll
-    for (int rg = 0; rg < 2; ++rg) {
-      float c0[4] = {0, 0, 0, 0}, c1[4] = {0, 0, 0, 0};
-      const int rbase = warp * 32 + rg * 16;
-      const int mi = lane >> 3, ri = lane & 7;
-      const uint32_t a_row = rbase + ri + ((mi & 2) ? 8 : 0);
-      const uint32_t a_col = (mi & 1) ? 8 : 0;
-#pragma unroll
-      for (int s = 0; s < KS; ++s) {
-        uint32_t b0, b1, b2, b3;
-        ldsm_x4(kb + (a_row * RS + s * 16 + a_col) * 2, b0, b1, b2, b3);
-        mma_bf16(c0, qa0[s], qa2[s], b0, b1);
-        mma_bf16(c1, qa0[s], qa2[s], b2, b3);
-      }
-      // c0: rows rbase + 2tig + {0,1}; c1: rows rbase + 8 + 2tig + {0,1}
-      const int rr[4] = {rbase + 2 * tig, rbase + 2 * tig + 1, rbase + 8 + 2 * tig,
-                         rbase + 9 + 2 * tig};
-      const float v[4] = {c0[0], c0[1], c1[0], c1[1]};
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const float s2 = rr[e] < nrows ? v[e] * sl2 : -INFINITY;
-        p[rg * 2 + (e >> 1)][e & 1] = s2;
-        mloc = fmaxf(mloc, s2);
-      }
-    }
-  }
-  // CTA max per head (log2 units)
-  mloc = fmaxf(mloc, __shfl_xor_sync(0xffffffffu, mloc, 1));
-  mloc = fmaxf(mloc, __shfl_xor_sync(0xffffffffu, mloc, 2));
-  if (tig == 0) red_m[warp][gid] = mloc;
-  __syncthreads();
-  const float M = fmaxf(fmaxf(red_m[0][gid], red_m[1][gid]), fmaxf(red_m[2][gid], red_m[3][gid]));
-
-  float o[D / 8][2];
-#pragma unroll
-  for (int i = 0; i < D / 8; ++i) o[i][0] = o[i][1] = 0.f;
-  if (nrows > 0) {
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const float x = (M == -INFINITY) ? 0.f : exp2f(p[i][e] - M);
-        p[i][e] = x;
-        lloc += x;
-      }
-    mbar_wait(&bar[1], 0);
-    const uint32_t vb = smem_u32(Vs);
-#pragma unroll
-    for (int rg = 0; rg < 2; ++rg) {
-      // A = P (heads x 16 rows): a0 = rows 2tig.., a2 = rows 8+2tig..
-      const uint32_t ah0 = pack_bf16(p[rg * 2][0], p[rg * 2][1]);
-      const uint32_t ah2 = pack_bf16(p[rg * 2 + 1][0], p[rg * 2 + 1][1]);
-      const float2 h0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&ah0));
-      const float2 h2 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&ah2));
-      const uint32_t al0 = pack_bf16(p[rg * 2][0] - h0.x, p[rg * 2][1] - h0.y);
-      const uint32_t al2 = pack_bf16(p[rg * 2 + 1][0] - h2.x, p[rg * 2 + 1][1] - h2.y);
-      const int rbase = warp * 32 + rg * 16;
-      const int mi = lane >> 3, ri = lane & 7;
-      const uint32_t b_row = rbase + ri + ((mi & 1) ? 8 : 0);
-      const uint32_t b_col = (mi & 2) ? 8 : 0;
-#pragma unroll
-      for (int dn = 0; dn < D / 16; ++dn) {
-        uint32_t b0, b1, b2, b3;
-        ldsm_x4_t(vb + (b_row * RS + dn * 16 + b_col) * 2, b0, b1, b2, b3);
-        float c[4] = {o[2 * dn][0], o[2 * dn][1], 0.f, 0.f};
-        mma_bf16(c, ah0, ah2, b0, b1);
-        mma_bf16(c, al0, al2, b0, b1);
-        o[2 * dn][0] = c[0];
-        o[2 * dn][1] = c[1];
-        float c2[4] = {o[2 * dn + 1][0], o[2 * dn + 1][1], 0.f, 0.f};
-        mma_bf16(c2, ah0, ah2, b2, b3);
-        mma_bf16(c2, al0, al2, b2, b3);
-        o[2 * dn + 1][0] = c2[0];
-        o[2 * dn + 1][1] = c2[1];
-      }
-    }
-  }
-  // CTA sums: l per head, o per (head, d)
-  lloc += __shfl_xor_sync(0xffffffffu, lloc, 1);
-  lloc += __shfl_xor_sync(0xffffffffu, lloc, 2);
-  if (tig == 0) red_l[warp][gid] = lloc;
-  if (gid < ALPHA) {
-#pragma unroll
-    for (int i = 0; i < D / 8; ++i) {
-      red_o[warp][gid][8 * i + 2 * tig] = o[i][0];
-      red_o[warp][gid][8 * i + 2 * tig + 1] = o[i][1];
-    }
-  }
-  __syncthreads();
-  for (int i = tid; i < ALPHA * D; i += AT_THREADS) {
-    const int j = i / D, d = i % D;
-    const float s = red_o[0][j][d] + red_o[1][j][d] + red_o[2][j][d] + red_o[3][j][d];
-    part_o[((head_base + j) * nsplit + split) * D + d] = s;
-  }
-  if (tid < ALPHA) {
-    const int j = tid;
-    const float mm = fmaxf(fmaxf(red_m[0][j], red_m[1][j]), fmaxf(red_m[2][j], red_m[3][j]));
-    const float ll = red_l[0][j] + red_l[1][j] + red_l[2][j] + red_l[3][j];
-    part_ml[((head_base + j) * nsplit + split) * 2] = nrows > 0 ? mm : -INFINITY;
-    part_ml[((head_base + j) * nsplit + split) * 2 + 1] = nrows > 0 ? ll : 0.f;
-  }
-  const size_t grp = (size_t)lr * B * G + bg;
-  if (last_block_ticket(&cnt[grp], nsplit, &flag))
-    merge_partials<D, ALPHA>(part_o, part_ml, nsplit, head_base, out, lse,
-                             ((size_t)l * B + b) * Hq + g * ALPHA);
-  (void)Hq_;
-}
+#include "attn_bf16.cuh"
 
 // ---------------------------------------------------------------- fp32 / CUDA-core path
 template <int D, int ALPHA>
@@ -294,8 +114,9 @@ __global__ void __launch_bounds__(AT_THREADS) attn_f32_kernel(
     const float* __restrict__ q, const void* const* __restrict__ k_layers,
     const void* const* __restrict__ v_layers, int kv_mode, const int32_t* __restrict__ idx,
     const int32_t* __restrict__ count, int layer_begin, int B, int G, int rows, int kbud,
-    float scale, int nsplit, float* __restrict__ part_o, float* __restrict__ part_ml,
-    unsigned* __restrict__ cnt, float* __restrict__ out, float* __restrict__ lse) {
+    float scale, int nsplit, int segstride, float* __restrict__ part_o,
+    float* __restrict__ part_ml, unsigned* __restrict__ cnt, float* __restrict__ out,
+    float* __restrict__ lse) {
   __shared__ float qs[ALPHA][D];
   __shared__ float ps[ALPHA][AT_ROWS];
   __shared__ int toks[AT_ROWS];
@@ -362,17 +183,17 @@ __global__ void __launch_bounds__(AT_THREADS) attn_f32_kernel(
     const int j = i / D, d = i % D;
     float acc = 0.f;
     for (int r = 0; r < nrows; ++r) acc = fmaf(ps[j][r], Vl[(size_t)toks[r] * D + d], acc);
-    part_o[((head_base + j) * nsplit + split) * D + d] = acc;
+    part_o[((head_base + j) * segstride + split) * D + d] = acc;
   }
   __syncthreads();
   if (tid < ALPHA) {
-    part_ml[((head_base + tid) * nsplit + split) * 2] = nrows > 0 ? mh[tid] * LOG2E : -INFINITY;
-    part_ml[((head_base + tid) * nsplit + split) * 2 + 1] = nrows > 0 ? lh[tid] : 0.f;
+    part_ml[((head_base + tid) * segstride + split) * 2] = nrows > 0 ? mh[tid] * LOG2E : -INFINITY;
+    part_ml[((head_base + tid) * segstride + split) * 2 + 1] = nrows > 0 ? lh[tid] : 0.f;
   }
   const size_t grp = (size_t)lr * B * G + bg;
   if (last_block_ticket(&cnt[grp], nsplit, &flag))
-    merge_partials<D, ALPHA>(part_o, part_ml, nsplit, head_base, out, lse,
-                             ((size_t)l * B + b) * Hq + g * ALPHA);
+    merge_partials<D, ALPHA>(part_o, part_ml, nsplit, segstride, head_base, out, lse,
+                             ((size_t)l * B + b) * Hq + g * ALPHA, AT_THREADS);
 }
 
 __global__ void merge_kernel(const float* __restrict__ o_parts, const float* __restrict__ lse_parts,
@@ -429,25 +250,36 @@ extern "C" int spc_sparse_decode_attn(int dtype, const void* q, const void* cons
   if (dtype != SPC_BF16 && dtype != SPC_F32) return SPC_E_UNSUPPORTED;
   AttnWs w = attn_ws_layout(ws, L, B, Hq, D, k);
   const int nsplit = (k + AT_ROWS - 1) / AT_ROWS;
-  dim3 grid(nsplit, B * G, layer_end - layer_begin);
+  const int n_groups = (layer_end - layer_begin) * B * G;
   cudaStream_t st = as_stream(stream);
+  // persistent bf16 path: 2 CTAs per SM, contiguous chunk-aligned row ranges
+  const int kpad = (k + CH - 1) / CH * CH;  // groups padded to whole chunks
+  const long long v_total = (long long)n_groups * kpad;
+  const int ncta_target = 2 * num_sms();
+  long long rpc = (v_total + ncta_target - 1) / ncta_target;
+  rpc = (rpc + CH - 1) / CH * CH;
+  const int ncta = (int)((v_total + rpc - 1) / rpc);
 #define AT(DD, AA)                                                                              \
   if (D == DD && alpha == AA) {                                                                 \
     if (dtype == SPC_BF16) {                                                                    \
-      const int smem = (int)(2 * sizeof(uint16_t) * AT_ROWS * (DD + 8));                        \
+      const int smem = PSmem<DD, AA>::BYTES;                                                    \
       static bool attr = false;                                                                 \
       if (!attr) {                                                                              \
         cudaFuncSetAttribute(attn_bf16_kernel<DD, AA>,                                          \
                              cudaFuncAttributeMaxDynamicSharedMemorySize, smem);                \
         attr = true;                                                                            \
       }                                                                                         \
-      attn_bf16_kernel<DD, AA><<<grid, AT_THREADS, smem, st>>>(                                 \
+      attn_bf16_kernel<DD, AA><<<ncta, AT2_THREADS, smem, st>>>(                                \
           (const uint16_t*)q, k_layers, v_layers, kv_mode, idx, count, layer_begin, B, G, rows, \
-          k, scale, nsplit, w.part_o, w.part_ml, w.cnt, out, lse);                              \
-    } else                                                                                      \
+          k, kpad, scale, (int)(rpc / CH), n_groups, w.segstride, w.part_o, w.part_ml, w.cnt,   \
+          out,                                                                                  \
+          lse);                                                                                 \
+    } else {                                                                                    \
+      dim3 grid(nsplit, B * G, layer_end - layer_begin);                                        \
       attn_f32_kernel<DD, AA><<<grid, AT_THREADS, 0, st>>>(                                     \
           (const float*)q, k_layers, v_layers, kv_mode, idx, count, layer_begin, B, G, rows, k, \
-          scale, nsplit, w.part_o, w.part_ml, w.cnt, out, lse);                                 \
+          scale, nsplit, w.segstride, w.part_o, w.part_ml, w.cnt, out, lse);                    \
+    }                                                                                           \
     return launched();                                                                          \
   }
   AT(64, 1) AT(64, 2) AT(64, 4) AT(64, 8) AT(128, 1) AT(128, 2) AT(128, 4) AT(128, 8)
@@ -461,4 +293,12 @@ extern "C" int spc_attn_merge(const float* o_parts, const float* lse_parts, int 
   if (P < 1 || n < 1 || D < 1) return SPC_E_SHAPE;
   merge_kernel<<<n, 128, 0, as_stream(stream)>>>(o_parts, lse_parts, P, n, D, out, lse_out);
   return launched();
+}
+
+// Debug only (not part of include/spc.h): route the attention kernel's per-chunk
+// %globaltimer trace of CTA 0 into `buf` (device, >= 256*4 uint64), NULL = off.
+extern "C" int spc_debug_set_trace(void* buf) {
+  unsigned long long* p = (unsigned long long*)buf;
+  cudaError_t e = cudaMemcpyToSymbol(spc::g_trace, &p, sizeof(p));
+  return e == cudaSuccess ? SPC_OK : SPC_E_CUDA;
 }

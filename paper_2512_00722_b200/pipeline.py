@@ -68,7 +68,21 @@ class DecodeStep:
         self.ws_topk = spc.alloc_workspace(spc.topk_workspace(B, G, self.Smax, k), dev)
         self.ws_attn = spc.alloc_workspace(spc.attn_workspace(L, B, Hq, D, k), dev)
         self.parity = 0
-        self.graphs = [None, None]
+        # input sets: address-distinct copies of (kr, K, V) that the step can rotate through
+        # (benchmarks use this instead of an L2 flush); set 0 is the one given above
+        self.sets = [(self.kr, self.k_tab, self.v_tab, [self.k_layers, self.v_layers])]
+        self.cur_set = 0
+        self.graphs = {}
+
+    def add_input_set(self, kr, k_layers, v_layers):
+        """Register another (retrieval keys, K layers, V layers) copy; returns its index."""
+        self.sets.append((kr, spc.ptr_table(list(k_layers), self.dev),
+                          spc.ptr_table(list(v_layers), self.dev), [k_layers, v_layers]))
+        return len(self.sets) - 1
+
+    def use_set(self, i: int):
+        self.cur_set = i
+        self.kr, self.k_tab, self.v_tab, _ = self.sets[i]
 
     # ------------------------------------------------------------------ eager
     def enqueue(self, parity: int, stream=None):
@@ -103,25 +117,31 @@ class DecodeStep:
             self.q_llm.copy_(q_llm, non_blocking=True)
         p = self.parity
         if use_graph:
-            if self.graphs[p] is None:
+            key = (self.cur_set, p)
+            if key not in self.graphs:
                 self.capture()
-            self.graphs[p].replay()
+            self.graphs[key].replay()
         else:
             self.enqueue(p)
         self.parity ^= 1
         return self.idx[p], self.cnt[p]
 
     def capture(self):
-        """Capture the even and odd step as two CUDA graphs (after an eager warm-up)."""
+        """Capture the even and odd step of every input set as CUDA graphs (call after an
+        eager warm-up so kernel attributes are set)."""
+        keep = self.cur_set
         s = torch.cuda.Stream(device=self.dev)
         s.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(s):
-            for p in (0, 1):
-                g = torch.cuda.CUDAGraph()
-                with torch.cuda.graph(g, stream=s):
-                    self.enqueue(p)
-                self.graphs[p] = g
+            for si in range(len(self.sets)):
+                self.use_set(si)
+                for p in (0, 1):
+                    g = torch.cuda.CUDAGraph()
+                    with torch.cuda.graph(g, stream=s):
+                        self.enqueue(p)
+                    self.graphs[(si, p)] = g
         torch.cuda.current_stream().wait_stream(s)
+        self.use_set(keep)
 
     def reset_state(self):
         for c in self.cnt:
