@@ -17,6 +17,7 @@ namespace {
 
 constexpr int DF_THREADS = 1024;
 constexpr int DF_PER = SPC_MAX_K / DF_THREADS;
+constexpr int DF_BM_WORDS = 1 << 14;  // 64 KiB bitmap per list: token ids < 2^19
 
 __device__ __forceinline__ bool contains(const int32_t* a, int n, int x) {
   int lo = 0, hi = n;  // a ascending
@@ -47,9 +48,30 @@ __global__ void __launch_bounds__(DF_THREADS) diff_kernel(
   const int np = min(max(prev_count[row], 0), k), nc = min(max(cur_count[row], 0), k);
   const int32_t* pv = prev_idx + (size_t)row * k;
   const int32_t* cv = cur_idx + (size_t)row * k;
+  // membership bitmaps over token ids (both lists ascending: the last entries bound the ids);
+  // binary search in the sorted lists when the ids exceed the bitmap capacity
+  uint32_t* bm_prev = (uint32_t*)(dsm + 3 * k);
+  uint32_t* bm_cur = bm_prev + DF_BM_WORDS;
+  const int maxtok = max(np ? __ldg(pv + np - 1) : -1, nc ? __ldg(cv + nc - 1) : -1);
+  const bool use_bm = maxtok < DF_BM_WORDS * 32;
+  const int nwords = use_bm ? (maxtok >> 5) + 1 : 0;
+  for (int i = tid; i < nwords; i += DF_THREADS) bm_prev[i] = bm_cur[i] = 0u;
   for (int i = tid; i < np; i += DF_THREADS) sprev[i] = pv[i];
   for (int i = tid; i < nc; i += DF_THREADS) scur[i] = cv[i];
   __syncthreads();
+  if (use_bm) {
+    for (int i = tid; i < np; i += DF_THREADS) atomicOr(&bm_prev[sprev[i] >> 5], 1u << (sprev[i] & 31));
+    for (int i = tid; i < nc; i += DF_THREADS) atomicOr(&bm_cur[scur[i] >> 5], 1u << (scur[i] & 31));
+    __syncthreads();
+  }
+  auto in_prev = [&](int x) {
+    if (x < 0 || x > maxtok) return false;
+    return use_bm ? ((bm_prev[x >> 5] >> (x & 31)) & 1u) != 0u : contains(sprev, np, x);
+  };
+  auto in_cur = [&](int x) {
+    if (x < 0 || x > maxtok) return false;
+    return use_bm ? ((bm_cur[x >> 5] >> (x & 31)) & 1u) != 0u : contains(scur, nc, x);
+  };
   const int per = (k + DF_THREADS - 1) / DF_THREADS;
   const int e0 = tid * per;
 
@@ -59,7 +81,7 @@ __global__ void __launch_bounds__(DF_THREADS) diff_kernel(
 #pragma unroll
   for (int i = 0; i < DF_PER; ++i) {
     const int e = e0 + i;
-    flag[i] = (i < per && e < nc) ? !contains(sprev, np, scur[e]) : 0;
+    flag[i] = (i < per && e < nc) ? !in_prev(scur[e]) : 0;
     cnt += flag[i];
   }
   int pos = block_excl_scan(cnt, wsum, &total);
@@ -78,7 +100,7 @@ __global__ void __launch_bounds__(DF_THREADS) diff_kernel(
 #pragma unroll
     for (int i = 0; i < DF_PER; ++i) {
       const int e = e0 + i;
-      flag[i] = (i < per && e < np) ? !contains(scur, nc, sprev[e]) : 0;
+      flag[i] = (i < per && e < np) ? !in_cur(sprev[e]) : 0;
       cnt += flag[i];
     }
     pos = block_excl_scan(cnt, wsum, &total);
@@ -101,7 +123,7 @@ __global__ void __launch_bounds__(DF_THREADS) diff_kernel(
     for (int i = 0; i < DF_PER; ++i) {
       const int s = e0 + i;
       tok[i] = (i < per && s < k) ? st[s] : -2;
-      flag[i] = tok[i] != -2 && (tok[i] < 0 || !contains(scur, nc, tok[i]));
+      flag[i] = tok[i] != -2 && (tok[i] < 0 || !in_cur(tok[i]));
       cnt += flag[i];
     }
     pos = block_excl_scan(cnt, wsum, &total);
@@ -165,11 +187,11 @@ extern "C" int spc_elastic_diff(const int32_t* prev_idx, const int32_t* prev_cou
   if (slot_tok && !load_slot) return SPC_E_NULL;
   if (B <= 0 || G <= 0) return SPC_E_SHAPE;
   if (k < 1 || k > SPC_MAX_K) return SPC_E_BUDGET;
-  const size_t smem = sizeof(int32_t) * 3 * (size_t)k;
+  const size_t smem = sizeof(int32_t) * 3 * (size_t)k + sizeof(uint32_t) * 2 * DF_BM_WORDS;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(diff_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)(sizeof(int32_t) * 3 * SPC_MAX_K));
+                         (int)(sizeof(int32_t) * 3 * SPC_MAX_K + sizeof(uint32_t) * 2 * DF_BM_WORDS));
     attr = true;
   }
   diff_kernel<<<B * G, DF_THREADS, smem, as_stream(stream)>>>(prev_idx, prev_count, cur_idx,

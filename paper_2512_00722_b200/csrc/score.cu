@@ -15,14 +15,18 @@
 //   GROUP   weights and group max (O5, O6).
 // Per-tile partial max / sums go to the workspace; the last CTA of each group
 // reduces them (order-free: max and integer add), so results are deterministic.
+#include <cooperative_groups.h>
+
 #include "common.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace spc {
 namespace {
 
-constexpr int LG_ROWS = 256;     // key rows per CTA tile (one TMA box height)
-constexpr int LG_THREADS = 64;   // 4 rows per thread
-constexpr int LG_DCHUNK = 64;    // d per TMA box (128 B inner extent, SWIZZLE_128B)
+
+
+
 constexpr int NORM_THREADS = 256;
 constexpr int NORM_PER = 8;      // elements per thread
 constexpr int NORM_TILE = NORM_THREADS * NORM_PER;
@@ -30,187 +34,46 @@ constexpr int GRP_THREADS = 256;
 constexpr int GRP_PER = 4;
 constexpr int GRP_TILE = GRP_THREADS * GRP_PER;
 
-template <int D, int ALPHA>
-struct LgSmem {
-  static constexpr int NCH = D / LG_DCHUNK;
-  static constexpr size_t kbytes = (size_t)NCH * LG_ROWS * 128;  // bf16 rows, 128 B per chunk
-  static constexpr size_t qbytes = (size_t)D * ALPHA * sizeof(float2);
-  static constexpr size_t total = 1024 /*align slack*/ + kbytes + qbytes + 64;
-};
-
-template <int D, int ALPHA>
-__global__ void __launch_bounds__(LG_THREADS) logits_kernel(
-    const __grid_constant__ CUtensorMap kmap, const uint16_t* __restrict__ q,
-    const int32_t* __restrict__ seq_len, int G, int Smax, float scale, float* __restrict__ logits,
-    float* __restrict__ tile_max, unsigned int* __restrict__ counters,
-    float* __restrict__ head_max) {
-  constexpr int NCH = D / LG_DCHUNK;
-  constexpr int Hq_per_g = ALPHA;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* base = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  uint8_t* kbuf = base;
-  float2* qdup = (float2*)(base + LgSmem<D, ALPHA>::kbytes);
-  uint64_t* bar = (uint64_t*)(base + LgSmem<D, ALPHA>::kbytes + LgSmem<D, ALPHA>::qbytes);
-  __shared__ float red[2][ALPHA];
-  __shared__ int flag;
-
-  const int tid = threadIdx.x;
-  const int tile = blockIdx.x, ntiles = gridDim.x;
-  const int bg = blockIdx.y;
-  const int b = bg / G, g = bg % G;
-  const int Hq = G * ALPHA;
-  const int S = seq_len[b];
-  const int t0 = tile * LG_ROWS;
-  const bool active = t0 < S;
-
-  if (tid == 0) {
-    prefetch_tmap(&kmap);
-    for (int c = 0; c < NCH; ++c) mbar_init(&bar[c], 1);
-    fence_mbar_init();
-  }
-  __syncthreads();
-  if (active && tid == 0) {
-    for (int c = 0; c < NCH; ++c) {
-      mbar_arrive_expect_tx(&bar[c], LG_ROWS * 128);
-      tma_load_3d(kbuf + (size_t)c * LG_ROWS * 128, &kmap, c * LG_DCHUNK, t0, bg, &bar[c]);
-    }
-  }
-  // query of this (b, g): alpha heads, duplicated into float2 for FFMA2 row pairs
-  for (int i = tid; i < D * ALPHA; i += LG_THREADS) {
-    int d = i / ALPHA, j = i % ALPHA;
-    float v = __uint_as_float((uint32_t)q[((size_t)b * Hq + g * ALPHA + j) * D + d] << 16);
-    qdup[i] = make_float2(v, v);
-  }
-  __syncthreads();
-
-  float hmax[ALPHA];
-#pragma unroll
-  for (int j = 0; j < ALPHA; ++j) hmax[j] = -INFINITY;
-
-  if (active) {
-    float2 acc[ALPHA][2];
-#pragma unroll
-    for (int j = 0; j < ALPHA; ++j) acc[j][0] = acc[j][1] = make_float2(0.f, 0.f);
-    int r[4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) r[k] = tid + LG_THREADS * k;
-    const uint32_t kbase = smem_u32(kbuf), qbase = smem_u32(qdup);
-
-#pragma unroll 1
-    for (int c = 0; c < NCH; ++c) {
-      mbar_wait(&bar[c], 0);
-      const uint32_t kc = kbase + (uint32_t)c * LG_ROWS * 128;
-#pragma unroll 2
-      for (int u = 0; u < 8; ++u) {  // 16-byte granule = 8 consecutive d
-        uint4 w[4];
-#pragma unroll
-        for (int k = 0; k < 4; ++k)  // SWIZZLE_128B: granule u of row r lives at u ^ (r & 7)
-          w[k] = lds128(kc + r[k] * 128 + ((u ^ (r[k] & 7)) << 4));
-        const uint32_t qd = qbase + (uint32_t)(c * LG_DCHUNK + u * 8) * ALPHA * 8;
-#pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          uint32_t w0 = (&w[0].x)[e >> 1], w1 = (&w[1].x)[e >> 1];
-          uint32_t w2 = (&w[2].x)[e >> 1], w3 = (&w[3].x)[e >> 1];
-          float2 k01, k23;
-          if (e & 1) {
-            k01 = make_float2(bf16hi(w0), bf16hi(w1));
-            k23 = make_float2(bf16hi(w2), bf16hi(w3));
-          } else {
-            k01 = make_float2(bf16lo(w0), bf16lo(w1));
-            k23 = make_float2(bf16lo(w2), bf16lo(w3));
-          }
-#pragma unroll
-          for (int j = 0; j < ALPHA; j += 2) {
-            float2 qq0, qq1;
-            if (ALPHA >= 2) {
-              const float4 q4 = lds128f(qd + (uint32_t)(e * ALPHA + j) * 8);
-              qq0 = make_float2(q4.x, q4.y);
-              qq1 = make_float2(q4.z, q4.w);
-            } else {
-              qq0 = lds64f(qd + (uint32_t)(e * ALPHA + j) * 8);
-            }
-            acc[j][0] = ffma2(k01, qq0, acc[j][0]);
-            acc[j][1] = ffma2(k23, qq0, acc[j][1]);
-            if (ALPHA >= 2) {
-              acc[j + 1][0] = ffma2(k01, qq1, acc[j + 1][0]);
-              acc[j + 1][1] = ffma2(k23, qq1, acc[j + 1][1]);
-            }
-          }
-        }
-      }
-    }
-    // O1 final multiply by scale, store, O2 partial max
-#pragma unroll
-    for (int j = 0; j < ALPHA; ++j) {
-      float s[4] = {__fmul_rn(acc[j][0].x, scale), __fmul_rn(acc[j][0].y, scale),
-                    __fmul_rn(acc[j][1].x, scale), __fmul_rn(acc[j][1].y, scale)};
-      float* out = logits + ((size_t)b * Hq + g * ALPHA + j) * Smax + t0;
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        if (t0 + r[k] < S) {
-          out[r[k]] = s[k];
-          hmax[j] = fmaxf(hmax[j], s[k]);
-        }
-      }
-    }
-  }
-  const int warp = tid >> 5, lane = tid & 31;
-#pragma unroll
-  for (int j = 0; j < ALPHA; ++j) {
-    float m = warp_max(hmax[j]);
-    if (lane == 0) red[warp][j] = m;
-  }
-  __syncthreads();
-  if (tid < ALPHA)
-    tile_max[((size_t)b * Hq + g * ALPHA + tid) * ntiles + tile] = fmaxf(red[0][tid], red[1][tid]);
-  if (last_block_ticket(&counters[bg], ntiles, &flag)) {
-    // reduce partial maxima of the ALPHA heads of this group
-    for (int j = warp; j < ALPHA; j += LG_THREADS / 32) {
-      const float* tm = tile_max + ((size_t)b * Hq + g * ALPHA + j) * ntiles;
-      float m = -INFINITY;
-      for (int i = lane; i < ntiles; i += 32) m = fmaxf(m, __ldcg(tm + i));
-      m = warp_max(m);
-      if (lane == 0) head_max[(size_t)b * Hq + g * ALPHA + j] = m;
-    }
-  }
-  (void)Hq_per_g;
-}
+#include "logits.cuh"
 
 // ---------------------------------------------------------------- NORM (O3, O4)
-__global__ void __launch_bounds__(NORM_THREADS) norm_kernel(
+// One thread-block cluster of NM_CL CTAs per head: each CTA sums its quarter of
+// the (L2-resident) logits row, the partial int64 sums meet in CTA 0 through
+// distributed shared memory (integer addition: exact, order-free).
+constexpr int NM_CL = 4;
+constexpr int NM_T = 512;
+__global__ void __cluster_dims__(NM_CL, 1, 1) __launch_bounds__(NM_T) norm_kernel(
     const float* __restrict__ logits, const float* __restrict__ head_max,
-    const int32_t* __restrict__ seq_len, int Hq, int Smax, long long* __restrict__ tile_sum,
-    unsigned int* __restrict__ counters, int64_t* __restrict__ head_sumfix) {
-  __shared__ long long red[NORM_THREADS / 32];
-  __shared__ int flag;
+    const int32_t* __restrict__ seq_len, int Hq, int Smax, int64_t* __restrict__ head_sumfix) {
+  __shared__ long long red[NM_T / 32];
+  __shared__ long long part;
+  cg::cluster_group cl = cg::this_cluster();
+  const int rank = (int)cl.block_rank();
   const int bh = blockIdx.y, b = bh / Hq;
-  const int tile = blockIdx.x, ntiles = gridDim.x;
   const int S = seq_len[b];
   const float m = head_max[bh];
   const float* row = logits + (size_t)bh * Smax;
+  const int per = (S + NM_CL - 1) / NM_CL;
+  const int s0 = min(S, rank * per), s1 = min(S, s0 + per);
   long long acc = 0;
-  const int t0 = tile * NORM_TILE + threadIdx.x;
-#pragma unroll
-  for (int i = 0; i < NORM_PER; ++i) {
-    int t = t0 + i * NORM_THREADS;
-    if (t < S) acc += fixpoint40(spc_exp_dev(__fsub_rn(__ldcg(row + t), m)));
-  }
+#pragma unroll 4
+  for (int t = s0 + threadIdx.x; t < s1; t += NM_T)
+    acc += fixpoint40(spc_exp_dev(__fsub_rn(__ldcg(row + t), m)));
   acc = warp_sum_ll(acc);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
   __syncthreads();
   if (threadIdx.x == 0) {
     long long s = 0;
-    for (int w = 0; w < NORM_THREADS / 32; ++w) s += red[w];
-    tile_sum[(size_t)bh * ntiles + tile] = s;
+    for (int w = 0; w < NM_T / 32; ++w) s += red[w];
+    part = s;
   }
-  if (last_block_ticket(&counters[bh], ntiles, &flag)) {
-    if (threadIdx.x < 32) {
-      long long s = 0;
-      for (int i = threadIdx.x; i < ntiles; i += 32) s += __ldcg(tile_sum + (size_t)bh * ntiles + i);
-      s = warp_sum_ll(s);
-      if (threadIdx.x == 0) head_sumfix[bh] = s;
-    }
+  cl.sync();
+  if (rank == 0 && threadIdx.x == 0) {
+    long long s = 0;
+    for (int r = 0; r < NM_CL; ++r) s += *cl.map_shared_rank(&part, r);
+    head_sumfix[bh] = s;
   }
+  cl.sync();  // remote reads of `part` done before any CTA exits
 }
 
 // ------------------------------------------------------------- GROUP (O4..O6)
@@ -250,19 +113,25 @@ __global__ void __launch_bounds__(GRP_THREADS) group_kernel(
 }
 
 template <int D, int ALPHA>
-int launch_logits(const CUtensorMap& map, const uint16_t* q, const int32_t* seq_len, int B, int G,
-                  int Smax, float scale, float* logits, float* tile_max, unsigned* counters,
-                  float* head_max, cudaStream_t st) {
-  const size_t smem = LgSmem<D, ALPHA>::total;
+int launch_logits(const uint16_t* kr, const uint16_t* q, const int32_t* seq_len, int B, int G,
+                  int Smax, float scale, float* logits, float* seg_max, int segstride,
+                  unsigned* counters, float* head_max, cudaStream_t st) {
+  const size_t smem = Lg4Smem<D, ALPHA>::BYTES;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(logits_kernel<D, ALPHA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
     attr = true;
   }
-  dim3 grid((Smax + LG_ROWS - 1) / LG_ROWS, B * G);
-  logits_kernel<D, ALPHA><<<grid, LG_THREADS, smem, st>>>(map, q, seq_len, G, Smax, scale, logits,
-                                                          tile_max, counters, head_max);
+  const int tpr = (Smax + LG_TR - 1) / LG_TR;
+  const int ntiles = B * G * tpr;
+  int tpc = (ntiles + num_sms() - 1) / num_sms();
+  if (tpc > tpr) tpc = tpr;  // a CTA spans at most two groups
+  const int ncta = (ntiles + tpc - 1) / tpc;
+  logits_kernel<D, ALPHA><<<ncta, 32 * lg_warps<ALPHA>(), smem, st>>>(kr, q, seq_len, G, Smax,
+                                                                      scale, tpc, tpr,
+                                                    ntiles, logits, seg_max, segstride, counters,
+                                                    head_max);
   return launched();
 }
 
@@ -279,10 +148,12 @@ struct ScoreWs {
   long long* tile_sum;
   unsigned* cnt1;
   unsigned* cnt2;
+  size_t nt1;  // segment stride of tile_max
   size_t bytes;
 };
 ScoreWs score_ws_layout(void* ws, int B, int Hq, int Smax) {
-  const size_t nt1 = (Smax + LG_ROWS - 1) / LG_ROWS, nt2 = (Smax + NORM_TILE - 1) / NORM_TILE;
+  // nt1 bounds the CTA segments of one group in LOGITS (every CTA owns >= 1 tile)
+  const size_t nt1 = (Smax + LG_TR - 1) / LG_TR + 2, nt2 = (Smax + NORM_TILE - 1) / NORM_TILE;
   uint8_t* p = (uint8_t*)ws;
   ScoreWs w;
   size_t off = 0;
@@ -294,6 +165,7 @@ ScoreWs score_ws_layout(void* ws, int B, int Hq, int Smax) {
   off = align_up(off + sizeof(unsigned) * B * Hq, 256);
   w.cnt2 = (unsigned*)(p + off);
   off = align_up(off + sizeof(unsigned) * B * Hq, 256);
+  w.nt1 = nt1;
   w.bytes = off;
   return w;
 }
@@ -327,21 +199,17 @@ extern "C" int spc_score(int dtype, const void* q, const void* kr, const int32_t
   ScoreWs w = score_ws_layout(ws, B, Hq, Smax);
 
   if (phases & SPC_SCORE_LOGITS) {
-    CUtensorMap map;
-    SPC_TRY(make_tmap_3d_bf16(&map, kr, D, Smax, (uint64_t)B * G, LG_DCHUNK, LG_ROWS,
-                              CU_TENSOR_MAP_SWIZZLE_128B));
     const uint16_t* qq = (const uint16_t*)q;
 #define LG(DD, AA)                                                                            \
   if (D == DD && alpha == AA)                                                                 \
-    SPC_TRY((launch_logits<DD, AA>(map, qq, seq_len, B, G, Smax, scale, logits, w.tile_max, \
-                                   w.cnt1, head_max, st)));
+    SPC_TRY((launch_logits<DD, AA>((const uint16_t*)kr, qq, seq_len, B, G, Smax, scale, logits, w.tile_max, \
+                                   (int)w.nt1, w.cnt1, head_max, st)));
     LG(64, 1) LG(64, 2) LG(64, 4) LG(64, 8) LG(128, 1) LG(128, 2) LG(128, 4) LG(128, 8)
 #undef LG
   }
   if (phases & SPC_SCORE_NORM) {
-    dim3 grid((Smax + NORM_TILE - 1) / NORM_TILE, B * Hq);
-    norm_kernel<<<grid, NORM_THREADS, 0, st>>>(logits, head_max, seq_len, Hq, Smax, w.tile_sum,
-                                               w.cnt2, head_sumfix);
+    norm_kernel<<<dim3(NM_CL, B * Hq), NM_T, 0, st>>>(logits, head_max, seq_len, Hq, Smax,
+                                                      head_sumfix);
     SPC_TRY(launched());
   }
   if (phases & SPC_SCORE_GROUP) {

@@ -7,61 +7,33 @@
 // unsigned integers (R20).  The k-th largest composite T is found by radix
 // select; the selection is then exactly {x : composite(x) >= T}.
 //
-// Kernels (rows R = B*G):
-//   hist_kernel     (multi-CTA / row)  2048-bin histogram of the top 11 bits
-//   find_kernel     (1 warp / row)     threshold bin b*, residual rank r
-//   collect_kernel  (multi-CTA / row)  composites of the elements in bin b*
-//   select_kernel   (1 CTA / row)      radix-refine the candidates to T in
-//                                      shared memory, then one ordered pass
-//                                      that emits positions >= T ascending.
-// Degenerate inputs (more than CAND_CAP elements in the threshold bin, e.g.
-// massive exact ties) fall back to refinement passes over the row itself.
+// spc_topk: ONE kernel, one thread-block cluster of CL = 8 CTAs per row.  Each
+// CTA owns a contiguous 1/8 of the row.
+//   1. 2048-bin histogram of the top 11 key bits per CTA (shared atomics);
+//      every CTA sums the 8 histograms through distributed shared memory and
+//      finds the threshold bin and the residual rank redundantly.
+//   2. while more than CAND_CAP elements share the prefix: another 8-bit digit
+//      (distributed histogram over the elements matching the prefix).
+//   3. the matching elements are gathered into CTA 0's shared memory (DSMEM,
+//      warp-aggregated slot claims), radix-refined there to T, and T is
+//      broadcast to the cluster.
+//   4. ordered compaction: each CTA counts its elements >= T, the counts are
+//      exchanged through DSMEM, and each CTA writes its positions ascending at
+//      its offset.  No workspace, no global atomics, no extra launches.
+#include <cooperative_groups.h>
+
 #include "common.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace spc {
 namespace {
 
-constexpr int TK_THREADS = 256;
-constexpr int TK_PER = 16;
-constexpr int TK_TILE = TK_THREADS * TK_PER;
-constexpr int NBIN0 = 2048;          // top digit: 11 bits of the composite
-constexpr int CAND_CAP = 8192;       // candidates kept per row (global and shared)
+constexpr int NBIN0 = 2048;     // top digit: 11 bits of the composite
+constexpr int CAND_CAP = 8192;  // candidates refined in shared memory
 constexpr int SEL_THREADS = 1024;
-constexpr int RANK_MAX = 1024;       // rank by counting below this many candidates
-
-struct RowInfo {
-  int need;   // min(k, len)
-  int len;    // valid elements of the row
-  int r;      // rank still needed inside the prefix (1-based)
-  int cm;     // number of elements matching the prefix
-  int bits;   // prefix length in bits
-  int all;    // 1: every element selected (need == len)
-  unsigned long long prefix;  // composite high bits (left-aligned)
-};
-
-struct TopkWs {
-  unsigned* hist;
-  RowInfo* info;
-  unsigned* ccount;
-  unsigned long long* cand;
-  size_t bytes;
-};
-
-TopkWs topk_ws_layout(void* ws, int R) {
-  uint8_t* p = (uint8_t*)ws;
-  TopkWs w;
-  size_t off = 0;
-  w.hist = (unsigned*)(p + off);
-  off = align_up(off + sizeof(unsigned) * (size_t)R * NBIN0, 256);
-  w.info = (RowInfo*)(p + off);
-  off = align_up(off + sizeof(RowInfo) * (size_t)R, 256);
-  w.ccount = (unsigned*)(p + off);
-  off = align_up(off + sizeof(unsigned) * (size_t)R, 256);
-  w.cand = (unsigned long long*)(p + off);
-  off = align_up(off + sizeof(unsigned long long) * (size_t)R * CAND_CAP, 256);
-  w.bytes = off;
-  return w;
-}
+constexpr int RANK_MAX = 128;   // rank by counting (O(n^2)) only below this many candidates
+constexpr int CL = 8;           // CTAs per row (cluster size)
 
 // composite of position p of a dense row
 __device__ __forceinline__ unsigned long long row_key(const float* row, int p, int len, int force,
@@ -75,32 +47,6 @@ __device__ __forceinline__ int row_len(const int32_t* seq_len, int row, int G, i
   return s < n_cols ? (s < 0 ? 0 : s) : n_cols;
 }
 
-__global__ void __launch_bounds__(TK_THREADS) hist_kernel(const float* __restrict__ val,
-                                                          const int32_t* __restrict__ seq_len, int G,
-                                                          int n_cols, int force,
-                                                          unsigned* __restrict__ hist) {
-  __shared__ unsigned h[NBIN0];
-  const int row = blockIdx.y;
-  const int len = row_len(seq_len, row, G, n_cols);
-  const int t0 = blockIdx.x * TK_TILE;
-  if (t0 >= len) return;
-  for (int i = threadIdx.x; i < NBIN0; i += TK_THREADS) h[i] = 0;
-  __syncthreads();
-  const float* v = val + (size_t)row * n_cols;
-#pragma unroll 4
-  for (int i = 0; i < TK_PER; ++i) {
-    const int p = t0 + i * TK_THREADS + threadIdx.x;
-    if (p < len) {
-      uint32_t vb = (force && p == len - 1) ? 0x7F800000u : __float_as_uint(__ldg(v + p));
-      atomicAdd(&h[vb >> 21], 1u);
-    }
-  }
-  __syncthreads();
-  unsigned* gh = hist + (size_t)row * NBIN0;
-  for (int i = threadIdx.x; i < NBIN0; i += TK_THREADS)
-    if (h[i]) atomicAdd(&gh[i], h[i]);
-}
-
 // Warp-cooperative search from the top bin down: returns (bin, above) with
 // above = sum of counts of bins > bin, above < r <= above + h[bin].
 template <int NB>
@@ -110,7 +56,7 @@ __device__ __forceinline__ void find_bin_warp(const unsigned* h, int r, int* bin
   const int lane = threadIdx.x & 31;
   const int hi = NB - 1 - lane * PER;  // this lane owns bins hi .. hi-PER+1
   unsigned s = 0;
-#pragma unroll 4
+#pragma unroll 8
   for (int i = 0; i < PER; ++i) s += h[hi - i];
   unsigned incl = s;
 #pragma unroll
@@ -133,71 +79,6 @@ __device__ __forceinline__ void find_bin_warp(const unsigned* h, int r, int* bin
     *above_out = (int)run;
   }
   __syncwarp();
-}
-
-__global__ void find_kernel(const unsigned* __restrict__ hist, const int32_t* __restrict__ seq_len,
-                            int G, int n_cols, int k, RowInfo* __restrict__ info,
-                            unsigned* __restrict__ ccount) {
-  const int row = blockIdx.x;
-  __shared__ int s_bin, s_above;
-  const int len = row_len(seq_len, row, G, n_cols);
-  const int need = k < len ? k : len;
-  RowInfo ri;
-  ri.need = need;
-  ri.len = len;
-  ri.all = (need == len);
-  ri.r = 0;
-  ri.cm = 0;
-  ri.bits = 0;
-  ri.prefix = 0;
-  if (!ri.all) {
-    const unsigned* h = hist + (size_t)row * NBIN0;
-    find_bin_warp<NBIN0>(h, need, &s_bin, &s_above);
-    __syncwarp();
-    ri.r = need - s_above;
-    ri.cm = (int)h[s_bin];
-    ri.bits = 11;
-    ri.prefix = (unsigned long long)s_bin << 53;
-  }
-  if (threadIdx.x == 0) {
-    info[row] = ri;
-    ccount[row] = 0;
-  }
-}
-
-__global__ void __launch_bounds__(TK_THREADS) collect_kernel(
-    const float* __restrict__ val, const int32_t* __restrict__ seq_len, int G, int n_cols,
-    int force, int stride, int offset, const RowInfo* __restrict__ info,
-    unsigned* __restrict__ ccount, unsigned long long* __restrict__ cand) {
-  const int row = blockIdx.y;
-  const RowInfo ri = info[row];
-  if (ri.all || ri.cm > CAND_CAP) return;
-  const int len = ri.len;
-  const int t0 = blockIdx.x * TK_TILE;
-  if (t0 >= len) return;
-  const unsigned want = (unsigned)(ri.prefix >> 53);
-  const float* v = val + (size_t)row * n_cols;
-  unsigned long long* c = cand + (size_t)row * CAND_CAP;
-  const int lane = threadIdx.x & 31;
-  for (int i = 0; i < TK_PER; ++i) {
-    const int p = t0 + i * TK_THREADS + threadIdx.x;
-    bool hit = false;
-    unsigned long long key = 0;
-    if (p < len) {
-      key = row_key(v, p, len, force, stride, offset);
-      hit = (unsigned)(key >> 53) == want;
-    }
-    const unsigned m = __ballot_sync(0xffffffffu, hit);
-    if (!m) continue;
-    unsigned base = 0;
-    const int leader = __ffs(m) - 1;
-    if (lane == leader) base = atomicAdd(&ccount[row], (unsigned)__popc(m));
-    base = __shfl_sync(0xffffffffu, base, leader);
-    if (hit) {
-      const unsigned slot = base + __popc(m & ((1u << lane) - 1));
-      if (slot < CAND_CAP) c[slot] = key;
-    }
-  }
 }
 
 // --------------------------------------------------------------- selection core
@@ -296,58 +177,137 @@ struct DenseKey {
   }
 };
 
-__global__ void __launch_bounds__(SEL_THREADS, 1) select_kernel(
-    const float* __restrict__ val, int n_cols, int k, int force, int stride, int offset,
-    const RowInfo* __restrict__ info, const unsigned* __restrict__ ccount,
-    const unsigned long long* __restrict__ cand, int32_t* __restrict__ out_idx,
-    float* __restrict__ out_val, int32_t* __restrict__ out_count,
-    unsigned long long* __restrict__ out_thresh) {
-  extern __shared__ __align__(16) uint8_t sel_raw[];
-  SelSmem& s = *reinterpret_cast<SelSmem*>(sel_raw);
-  __shared__ int s_total;
-  const int row = blockIdx.x, tid = threadIdx.x;
-  const RowInfo ri = info[row];
-  const int len = ri.len;
+struct ClSmem {
+  SelSmem sel;               // CTA 0: gathered candidates + refinement scratch
+  unsigned hist[NBIN0];      // this CTA's histogram (read remotely by the cluster)
+  unsigned rhist[NBIN0];     // cluster-reduced histogram
+  unsigned long long T;      // broadcast threshold
+  int counts[CL];            // selected elements per cluster rank
+  int total;
+};
+
+__global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(SEL_THREADS, 1)
+    topk_cluster_kernel(const float* __restrict__ val, const int32_t* __restrict__ seq_len, int G,
+                        int n_cols, int k, int force, int stride, int offset,
+                        int32_t* __restrict__ out_idx, float* __restrict__ out_val,
+                        int32_t* __restrict__ out_count, unsigned long long* __restrict__ out_thresh) {
+  extern __shared__ __align__(16) uint8_t cl_raw[];
+  ClSmem& s = *reinterpret_cast<ClSmem*>(cl_raw);
+  cg::cluster_group cl = cg::this_cluster();
+  const int rank = (int)cl.block_rank();
+  const int row = blockIdx.y, tid = threadIdx.x, lane = tid & 31;
+  const int len = row_len(seq_len, row, G, n_cols);
+  const int need = k < len ? k : len;
   const float* v = val + (size_t)row * n_cols;
-  DenseKey key{v, len, force, stride, offset};
+  const DenseKey key{v, len, force, stride, offset};
+  const int per = (len + CL - 1) / CL;
+  const int s0 = min(len, rank * per), s1 = min(len, s0 + per);
   unsigned long long T = 0;
-  if (!ri.all) {
-    int cm = ri.cm, r = ri.r, bits = ri.bits;
-    unsigned long long prefix = ri.prefix;
-    if (cm <= CAND_CAP) {
-      const unsigned long long* c = cand + (size_t)row * CAND_CAP;
-      for (int i = tid; i < cm; i += SEL_THREADS) s.cand[0][i] = c[i];
-      __syncthreads();
-    } else {
-      narrow_by_row_scan(s, key, len, prefix, bits, r, cm);
-      cm = s.n[0];
+  if (need < len) {
+    // ---- 1. top-11-bit histogram, reduced over the cluster
+    for (int i = tid; i < NBIN0; i += SEL_THREADS) s.hist[i] = 0;
+    __syncthreads();
+    for (int p = s0 + tid; p < s1; p += SEL_THREADS) atomicAdd(&s.hist[key(p) >> 53], 1u);
+    cl.sync();
+    for (int i = tid; i < NBIN0; i += SEL_THREADS) {
+      unsigned t = 0;
+#pragma unroll
+      for (int r = 0; r < CL; ++r) t += cl.map_shared_rank(s.hist, r)[i];
+      s.rhist[i] = t;
     }
-    refine_in_smem(s, 0, cm, r, bits);
+    __syncthreads();
+    if (tid < 32) find_bin_warp<NBIN0>(s.rhist, need, &s.sel.bin, &s.sel.above);
+    __syncthreads();
+    int r = need - s.sel.above, cm = (int)s.rhist[s.sel.bin], bits = 11;
+    unsigned long long prefix = (unsigned long long)s.sel.bin << 53;
+    cl.sync();  // remote reads of s.hist done before it is reused
+    // ---- 2. distributed refinement while too many elements share the prefix
+    while (cm > CAND_CAP && bits < 64) {
+      const int db = (64 - bits) < 8 ? (64 - bits) : 8;
+      const int shift = 64 - bits - db;
+      const unsigned mask = (1u << db) - 1;
+      for (int i = tid; i < 256; i += SEL_THREADS) s.hist[i] = 0;
+      __syncthreads();
+      for (int p = s0 + tid; p < s1; p += SEL_THREADS) {
+        const unsigned long long x = key(p);
+        if (prefix_match(x, prefix, bits)) atomicAdd(&s.hist[(unsigned)(x >> shift) & mask], 1u);
+      }
+      cl.sync();
+      for (int i = tid; i < 256; i += SEL_THREADS) {
+        unsigned t = 0;
+#pragma unroll
+        for (int q = 0; q < CL; ++q) t += cl.map_shared_rank(s.hist, q)[i];
+        s.rhist[i] = t;
+      }
+      __syncthreads();
+      if (tid < 32) find_bin_warp<256>(s.rhist, r, &s.sel.bin, &s.sel.above);
+      __syncthreads();
+      r -= s.sel.above;
+      cm = (int)s.rhist[s.sel.bin];
+      prefix |= (unsigned long long)s.sel.bin << shift;
+      bits += db;
+      cl.sync();
+    }
+    // ---- 3. gather the matching elements into CTA 0 and refine there
+    if (rank == 0 && tid == 0) s.sel.n[0] = 0;
+    cl.sync();
+    int* n0 = cl.map_shared_rank(&s.sel.n[0], 0);
+    unsigned long long* c0 = cl.map_shared_rank(&s.sel.cand[0][0], 0);
+    for (int p0 = s0; p0 < s1; p0 += SEL_THREADS) {
+      const int p = p0 + tid;
+      unsigned long long x = 0;
+      const bool hit = p < s1 && prefix_match(x = key(p), prefix, bits);
+      const unsigned m = __ballot_sync(0xffffffffu, hit);
+      if (!m) continue;
+      const int leader = __ffs(m) - 1;
+      int base = 0;
+      if (lane == leader) base = atomicAdd(n0, __popc(m));
+      base = __shfl_sync(0xffffffffu, base, leader);
+      if (hit) c0[base + __popc(m & ((1u << lane) - 1))] = x;
+    }
+    cl.sync();
+    if (rank == 0) {
+      refine_in_smem(s.sel, 0, s.sel.n[0], r, bits);
+      if (tid < CL) *cl.map_shared_rank(&s.T, tid) = s.sel.T;
+    }
+    cl.sync();
     T = s.T;
   }
-  // ordered pass: positions with composite >= T, ascending (contiguous segment per thread)
-  const int per = (len + SEL_THREADS - 1) / SEL_THREADS;
-  const int p0 = tid * per, p1 = min(len, p0 + per);
+  // ---- 4. ordered compaction over the cluster
+  const int seg = s1 - s0;
+  const int pt = (seg + SEL_THREADS - 1) / SEL_THREADS;
+  const int q0 = s0 + tid * pt, q1 = min(s1, q0 + pt);
   int cnt = 0;
-  for (int p = p0; p < p1; ++p) cnt += key(p) >= T;
-  int pos = block_excl_scan(cnt, s.wsum, &s_total);
+  for (int p = q0; p < q1; ++p) cnt += key(p) >= T;
+  int pos = block_excl_scan(cnt, s.sel.wsum, &s.total);
+  __syncthreads();
+  if (tid < CL) cl.map_shared_rank(s.counts, tid)[rank] = s.total;
+  cl.sync();
+  int base = 0, all = 0;
+#pragma unroll
+  for (int q = 0; q < CL; ++q) {
+    base += q < rank ? s.counts[q] : 0;
+    all += s.counts[q];
+  }
   int32_t* oi = out_idx + (size_t)row * k;
-  for (int p = p0; p < p1; ++p) {
+  float* ov = out_val ? out_val + (size_t)row * k : nullptr;
+  pos += base;
+  for (int p = q0; p < q1; ++p) {
     const unsigned long long x = key(p);
     if (x >= T) {
       oi[pos] = p;
-      if (out_val) out_val[(size_t)row * k + pos] = __uint_as_float((uint32_t)(x >> 32));
+      if (ov) ov[pos] = __uint_as_float((uint32_t)(x >> 32));
       ++pos;
     }
   }
-  const int total = s_total;
-  for (int i = total + tid; i < k; i += SEL_THREADS) {
-    oi[i] = -1;
-    if (out_val) out_val[(size_t)row * k + i] = 0.0f;
-  }
-  if (tid == 0) {
-    out_count[row] = total;
-    if (out_thresh) out_thresh[row] = ri.all ? 0ull : T;
+  if (rank == CL - 1)
+    for (int i = all + tid; i < k; i += SEL_THREADS) {
+      oi[i] = -1;
+      if (ov) ov[i] = 0.0f;
+    }
+  if (rank == 0 && tid == 0) {
+    out_count[row] = all;
+    if (out_thresh) out_thresh[row] = need < len ? T : 0ull;
   }
 }
 
@@ -447,40 +407,28 @@ extern "C" size_t spc_topk_workspace(int B, int G, int n_cols, int k) {
   (void)n_cols;
   (void)k;
   if (B <= 0 || G <= 0) return 0;
-  return topk_ws_layout(nullptr, B * G).bytes;
+  return 256;  // the cluster kernel needs no global scratch
 }
 
 extern "C" int spc_topk(const float* val, const int32_t* seq_len, int B, int G, int n_cols, int k,
                         int force_last, int id_stride, int id_offset, int32_t* out_idx,
                         float* out_val, int32_t* out_count, uint64_t* out_thresh, void* ws,
                         size_t ws_bytes, spc_stream_t stream) {
+  (void)ws;
+  (void)ws_bytes;
   if (!val || !seq_len || !out_idx || !out_count) return SPC_E_NULL;
   if (B <= 0 || G <= 0 || n_cols <= 0) return SPC_E_SHAPE;
   if (k < 1 || k > SPC_MAX_K) return SPC_E_BUDGET;
   if (n_cols >= SPC_MAX_SEQ || id_stride < 1 || id_offset < 0) return SPC_E_RANGE;
   if ((long long)n_cols * id_stride + id_offset >= 0x7FFFFFFFLL) return SPC_E_RANGE;
-  if (!ws || ws_bytes < spc_topk_workspace(B, G, n_cols, k)) return SPC_E_WORKSPACE;
-  cudaStream_t st = as_stream(stream);
-  const int R = B * G;
-  TopkWs w = topk_ws_layout(ws, R);
-  cudaError_t e = cudaMemsetAsync(w.hist, 0, sizeof(unsigned) * (size_t)R * NBIN0, st);
-  if (e != cudaSuccess) return launched(e);
-  dim3 grid((n_cols + TK_TILE - 1) / TK_TILE, R);
-  hist_kernel<<<grid, TK_THREADS, 0, st>>>(val, seq_len, G, n_cols, force_last, w.hist);
-  SPC_TRY(launched());
-  find_kernel<<<R, 32, 0, st>>>(w.hist, seq_len, G, n_cols, k, w.info, w.ccount);
-  SPC_TRY(launched());
-  collect_kernel<<<grid, TK_THREADS, 0, st>>>(val, seq_len, G, n_cols, force_last, id_stride,
-                                              id_offset, w.info, w.ccount, w.cand);
-  SPC_TRY(launched());
   static bool attr = false;
   if (!attr) {
-    SPC_TRY(set_big_smem((const void*)select_kernel, sizeof(SelSmem)));
+    SPC_TRY(set_big_smem((const void*)topk_cluster_kernel, sizeof(ClSmem)));
     attr = true;
   }
-  select_kernel<<<R, SEL_THREADS, sizeof(SelSmem), st>>>(
-      val, n_cols, k, force_last, id_stride, id_offset, w.info, w.ccount, w.cand, out_idx, out_val,
-      out_count, (unsigned long long*)out_thresh);
+  topk_cluster_kernel<<<dim3(CL, B * G), SEL_THREADS, sizeof(ClSmem), as_stream(stream)>>>(
+      val, seq_len, G, n_cols, k, force_last, id_stride, id_offset, out_idx, out_val, out_count,
+      (unsigned long long*)out_thresh);
   return launched();
 }
 
