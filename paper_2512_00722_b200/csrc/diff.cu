@@ -15,7 +15,7 @@
 namespace spc {
 namespace {
 
-constexpr int DF_THREADS = 1024;
+constexpr int DF_THREADS = 256;
 constexpr int DF_PER = SPC_MAX_K / DF_THREADS;
 constexpr int DF_BM_WORDS = 1 << 14;  // 64 KiB bitmap per list: token ids < 2^19
 

@@ -96,8 +96,11 @@ class SpcOps:
         return t
 
     def _seq(self, st):
-        t = self._buf(st, "seq_loc", (st.B,), torch.int32)
-        t.copy_(torch.tensor(st.local_seq(), dtype=torch.int32), non_blocking=True)
+        key = ("seq_loc", tuple(st.S))
+        t = st.bufs.get(key)
+        if t is None:  # filled once (outside any graph capture)
+            t = st.bufs[key] = torch.tensor(st.local_seq(), dtype=torch.int32,
+                                            device=st.kr.device)
         return t
 
     def _score(self, st, phases, head_max=None, sumfix=None):
