@@ -3,10 +3,11 @@
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config B]
 
-One "step" = spc_score (3 phases) + spc_topk + spc_elastic_diff + spc_sparse_decode_attn over
-all L layers, on one batch of synthetic input, inputs resident in HBM, captured
-as one CUDA graph per step parity.  The L2 is flushed (a 256 MiB write) before every timed
-step, outside the timed interval; each step is timed with CUDA events on the launching stream.
+One "step" = spc_score (LOGITS) + spc_select (NORM, GROUP, top-k, diff) +
+spc_sparse_decode_attn over all L layers, on one batch of synthetic input,
+inputs resident in HBM, captured as one CUDA graph per step parity.  No L2 flush: three
+address-distinct copies of the inputs (each > L2) are rotated step by step; the steps are
+timed with CUDA events on the launching stream.
 
 Prints ONE JSON line (rank 0).  Metric: decode throughput in tokens/s (= batch x N / step time)
 at the BASELINE.json config (default: config B, DeepSeek-R1-Distill-Llama-8B shape, ctx 32K).
@@ -267,26 +268,38 @@ def bench_ours(args):
     cnt_tot = int(st.cnt[st.parity ^ 1].sum().item())
 
     # ---- per-kernel breakdown: eager steps with events between the phases (same stream)
-    phases = ["score", "topk", "diff", "attn"]
+    phases = ["logits", "select", "attn"] if st.fused else ["score", "topk", "diff", "attn"]
     acc = {p: 0.0 for p in phases}
     reps = max(3, min(args.steps, 12))
     for j in range(reps):
         st.use_set(j % NSETS)
-        e = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+        e = [torch.cuda.Event(enable_timing=True) for _ in range(len(phases) + 1)]
         cur, prev = st.parity, st.parity ^ 1
         st.q_ret.copy_(qr[j])
+        # a 2 ms spin first, so the host enqueues every phase before the GPU reaches them:
+        # the events then time the kernels back to back, not the host's launch latency
+        torch.cuda._sleep(4_000_000)
         e[0].record(stream)
-        spc.score(st.q_ret, st.kr, st.seq_len, G, st.scale, st.logits, st.head_max,
-                  st.head_sumfix, st.gs, st.ws_score)
-        e[1].record(stream)
-        spc.topk(st.gs, st.seq_len, k, st.idx[cur], st.cnt[cur], st.ws_topk, force_last=True)
-        e[2].record(stream)
-        spc.elastic_diff(st.idx[prev], st.cnt[prev], st.idx[cur], st.cnt[cur], st.load_tok,
-                         st.n_load)
-        e[3].record(stream)
+        if st.fused:
+            spc.score(st.q_ret, st.kr, st.seq_len, G, st.scale, st.logits, st.head_max,
+                      st.head_sumfix, st.gs, st.ws_score, phases=spc.SCORE_LOGITS)
+            e[1].record(stream)
+            spc.select(st.logits, st.head_max, st.seq_len, G, k, st.head_sumfix, st.gs,
+                       st.idx[cur], st.cnt[cur], st.idx[prev], st.cnt[prev], st.load_tok,
+                       st.n_load, force_last=True)
+        else:
+            spc.score(st.q_ret, st.kr, st.seq_len, G, st.scale, st.logits, st.head_max,
+                      st.head_sumfix, st.gs, st.ws_score)
+            e[1].record(stream)
+            spc.topk(st.gs, st.seq_len, k, st.idx[cur], st.cnt[cur], st.ws_topk,
+                     force_last=True)
+            e[2].record(stream)
+            spc.elastic_diff(st.idx[prev], st.cnt[prev], st.idx[cur], st.cnt[cur],
+                             st.load_tok, st.n_load)
+        e[-2].record(stream)
         spc.sparse_decode_attn(st.q_llm, st.k_tab, st.v_tab, spc.KV_INDEXED, st.idx[cur],
                                st.cnt[cur], st.rows, k, st.scale, st.out, st.lse, st.ws_attn, G)
-        e[4].record(stream)
+        e[-1].record(stream)
         torch.cuda.synchronize()
         for i, p in enumerate(phases):
             acc[p] += e[i].elapsed_time(e[i + 1]) / reps

@@ -155,6 +155,26 @@ int spc_topk_filter(int32_t* idx, const float* val, int32_t* count, const uint64
                     int k, int id_stride, int id_offset, spc_stream_t stream);
 
 /* ------------------------------------------------------------------------
+ * spc_select — the single-device step from the logits to the elastic diff in ONE
+ * launch: spc_score(NORM | GROUP) + spc_topk(id_stride 1, id_offset 0) +
+ * spc_elastic_diff(INDEXED mode, slot_tok = NULL), bit-identical to those
+ * calls in sequence (same definitions O3..O8, same outputs, out_val and
+ * out_thresh not produced).  One thread-block cluster per (b, g) row.
+ * logits/head_max come from spc_score(LOGITS).  prev_idx/prev_count is the
+ * previous step's selection (count 0 on the first step).
+ * Supported: alpha in {1,2,4,8}, 1 <= k <= SPC_MAX_K, Smax <= 131072 and a
+ * multiple of 4 (SPC_E_UNSUPPORTED otherwise: use the separate calls).
+ * prev_idx rows must be ascending (as spc_topk / spc_select write them).
+ * evict_tok / n_evict may be NULL.  Errors: SPC_E_NULL, SPC_E_SHAPE,
+ * SPC_E_BUDGET, SPC_E_UNSUPPORTED, SPC_E_CUDA (launch failure).
+ * ---------------------------------------------------------------------- */
+int spc_select(const float* logits, const float* head_max, const int32_t* seq_len, int B, int Hq,
+               int G, int Smax, int k, int force_last, int64_t* head_sumfix, float* group_score,
+               int32_t* out_idx, int32_t* out_count, const int32_t* prev_idx,
+               const int32_t* prev_count, int32_t* load_tok, int32_t* n_load, int32_t* evict_tok,
+               int32_t* n_evict, spc_stream_t stream);
+
+/* ------------------------------------------------------------------------
  * spc_elastic_diff — elastic loading set difference, O8.
  *
  * Paper §5.4: evict S_last - S_now, load S_now - S_last

@@ -43,9 +43,14 @@ __device__ __forceinline__ float bf16lo(uint32_t w) { return __uint_as_float(w <
 __device__ __forceinline__ float bf16hi(uint32_t w) { return __uint_as_float(w & 0xFFFF0000u); }
 
 // O3, written from DESIGN.md §3: exp for x <= 0 with IEEE RN ops only.
+// n = rint(x * log2 e) by the 1.5 * 2^23 magic-number addition (RN-even, exact for
+// |t| < 2^22, identical to rintf) and its integer read from the sum's bits, so no
+// conversion-pipe instruction (FRND / F2I) is issued.
 __device__ __forceinline__ float spc_exp_dev(float x) {
-  if (x < -87.0f) return 0.0f;
-  const float n = rintf(__fmul_rn(x, __uint_as_float(0x3FB8AA3Bu)));
+  const float t = __fmul_rn(x, __uint_as_float(0x3FB8AA3Bu));
+  const float big = __fadd_rn(t, 12582912.0f);
+  const float n = __fsub_rn(big, 12582912.0f);
+  const int ni = (int)(__float_as_uint(big) - 0x4B400000u);
   float r = __fmaf_rn(-n, __uint_as_float(0x3F317200u), x);
   r = __fmaf_rn(-n, __uint_as_float(0x35BFBE8Eu), r);
   float p = __uint_as_float(0x39500D01u);                 // 1/7!
@@ -56,13 +61,69 @@ __device__ __forceinline__ float spc_exp_dev(float x) {
   p = __fmaf_rn(p, r, __uint_as_float(0x3F000000u));      // 1/2!
   p = __fmaf_rn(p, r, __uint_as_float(0x3F800000u));      // 1/1!
   p = __fmaf_rn(p, r, __uint_as_float(0x3F800000u));      // 1/0!
-  const float two_n = __uint_as_float((uint32_t)((int)n + 127) << 23);
-  return __fmul_rn(p, two_n);
+  const float two_n = __uint_as_float((uint32_t)(ni + 127) << 23);
+  return x < -87.0f ? 0.0f : __fmul_rn(p, two_n);
 }
 
 // trunc(e * 2^40) as int64 for 0 <= e <= 1 (e * 2^40 is exact in fp32).
 __device__ __forceinline__ long long fixpoint40(float e) {
   return __float2ll_rz(__fmul_rn(e, 1099511627776.0f));
+}
+
+// Packed (f32x2) IEEE-RN arithmetic, per element identical to the scalar RN ops.
+__device__ __forceinline__ unsigned long long f2_pack(float a, float b) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ float2 f2_unpack(unsigned long long v) {
+  float2 r;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(v));
+  return r;
+}
+__device__ __forceinline__ unsigned long long f2_fma(unsigned long long a, unsigned long long b,
+                                                     unsigned long long c) {
+  unsigned long long d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ unsigned long long f2_mul(unsigned long long a, unsigned long long b) {
+  unsigned long long d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ unsigned long long f2_add(unsigned long long a, unsigned long long b) {
+  unsigned long long d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ unsigned long long f2_splat(float a) { return f2_pack(a, a); }
+
+// spc_exp_dev on two values at once with f32x2 instructions (same ops, same order,
+// per element bit-identical to spc_exp_dev).
+__device__ __forceinline__ float2 spc_exp2_dev(float x0, float x1) {
+  const unsigned long long x = f2_pack(x0, x1);
+  const unsigned long long t = f2_mul(x, f2_splat(__uint_as_float(0x3FB8AA3Bu)));
+  const unsigned long long big = f2_add(t, f2_splat(12582912.0f));
+  const unsigned long long n = f2_add(big, f2_splat(-12582912.0f));
+  const float2 bigf = f2_unpack(big);
+  const float2 nf = f2_unpack(n);
+  const unsigned long long nn = f2_pack(-nf.x, -nf.y);
+  unsigned long long r = f2_fma(nn, f2_splat(__uint_as_float(0x3F317200u)), x);
+  r = f2_fma(nn, f2_splat(__uint_as_float(0x35BFBE8Eu)), r);
+  unsigned long long p = f2_splat(__uint_as_float(0x39500D01u));
+  p = f2_fma(p, r, f2_splat(__uint_as_float(0x3AB60B61u)));
+  p = f2_fma(p, r, f2_splat(__uint_as_float(0x3C088889u)));
+  p = f2_fma(p, r, f2_splat(__uint_as_float(0x3D2AAAABu)));
+  p = f2_fma(p, r, f2_splat(__uint_as_float(0x3E2AAAABu)));
+  p = f2_fma(p, r, f2_splat(__uint_as_float(0x3F000000u)));
+  p = f2_fma(p, r, f2_splat(__uint_as_float(0x3F800000u)));
+  p = f2_fma(p, r, f2_splat(__uint_as_float(0x3F800000u)));
+  const int n0 = (int)(__float_as_uint(bigf.x) - 0x4B400000u);
+  const int n1 = (int)(__float_as_uint(bigf.y) - 0x4B400000u);
+  const float2 e = f2_unpack(f2_mul(p, f2_pack(__uint_as_float((uint32_t)(n0 + 127) << 23),
+                                               __uint_as_float((uint32_t)(n1 + 127) << 23))));
+  return make_float2(x0 < -87.0f ? 0.0f : e.x, x1 < -87.0f ? 0.0f : e.y);
 }
 
 // Composite key of the O7 order: (bits(v) << 32) | ~uint32(id); larger = earlier.

@@ -1,0 +1,622 @@
+// select.cu — spc_select: NORM + GROUP + top-k + INDEXED elastic diff in ONE launch.
+//
+// Definitions: O3 exp, O4 int64 fixed-point normaliser and
+// reciprocal, O5 weights, O6 group max (P:321/P:328 head-level retrieval), O7
+// top-k by the composite key (bits(v) << 32) | ~uint32(id) (R8, R20), O8 elastic
+// diff against the previous selection.  Bit-identical to
+// spc_score(NORM | GROUP) + spc_topk + spc_elastic_diff (tests/test_gpu_select.py).
+//
+// One thread-block cluster of SCL CTAs per (b, g) row; CTA `rank` owns the token
+// segment [s0, s1) (a multiple of 4 tokens long).  The design minimises
+// distributed-shared-memory bytes (DSMEM moves ~20 B/clk/SM, a cluster barrier
+// costs ~400 clk):
+//   1. NORM: each thread keeps exp(l - m) of its first 4 tokens x alpha heads in
+//      registers; int64 partial sums are pushed to every CTA (alpha x SCL words).
+//   2. GROUP: gs = max_j e_j * r_j -> shared memory segment + group_score.  The
+//      row maximum of gs is exactly max_j r_j (the arg-max token of head j has
+//      e = exp(0) = 1), so pass 0 of the radix select bins the values in a
+//      256-bin window of 8 bins per binade below that maximum (clamped at both
+//      ends) while gs is produced.
+//   3. select: every pass pushes only the NONZERO bins of the local histogram
+//      into every CTA (red.add over DSMEM), one cluster barrier, then every CTA
+//      finds the threshold bin redundantly.  Later passes resolve 8 more key bits
+//      of the threshold bucket.  Stop when the whole bucket is selected
+//      (threshold = bucket's lower end) or it has <= CANDMAX elements: those are
+//      pushed to every CTA and ranked by counting.
+//   4. one pass over the segment classifies each token (selected / new / evicted
+//      using a bitmap of the previous selection built in the prologue), one
+//      packed block scan, one exchange of three counts per CTA, ordered writes.
+#include <cooperative_groups.h>
+
+#include "common.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace spc {
+namespace {
+
+constexpr int ST = 512;         // threads per CTA
+constexpr int SCL = 8;          // CTAs per row (cluster size)
+constexpr int SEGCAP = 16384;   // tokens per CTA segment: rows up to SCL * SEGCAP
+constexpr int NB = 256;         // bins per histogram pass
+constexpr int W0_SHIFT = 20;    // pass-0 bin = value bits >> 20: 8 bins per binade
+constexpr int W0_BITS = 12;     // key bits (sign + exponent + 3 mantissa) fixed by a pass-0 bin
+constexpr int CANDMAX = 128;    // exchange the threshold bucket at this size
+
+// Debug trace (spc_debug_set_select_trace; compiled in with -DSPC_TRACE): thread 0
+// of every CTA of row 0 stamps %globaltimer at phase boundaries: [rank][slot].
+__device__ unsigned long long* g_sel_trace = nullptr;
+__device__ __forceinline__ void sel_mark(int slot) {
+#ifdef SPC_TRACE
+  if (g_sel_trace && blockIdx.y == 0 && threadIdx.x == 0 && slot < 16) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    g_sel_trace[blockIdx.x * 16 + slot] = t;
+  }
+#else
+  (void)slot;
+#endif
+}
+
+struct SelSm {
+  float seg[SEGCAP];                      // group scores of this CTA's segment
+  uint32_t bm_prev[SEGCAP / 32];          // previous selection, segment-relative bitmap
+  unsigned long long cand[SCL][CANDMAX];  // threshold bucket, pushed by every rank
+  uint8_t candp[SCL][CANDMAX];            // ... and whether each was previously selected
+  unsigned hist[NB];                      // this CTA's histogram of the current pass
+  unsigned red[2][NB];                    // cluster sums (pushed by every rank), ping-pong
+  long long part[SCL][8];                 // NORM partial sums pushed by every rank
+  long long wred[ST / 32][8];             // NORM warp partials
+  unsigned long long stats[SCL];          // per rank: above | above&prev | bucket | bucket&prev
+  unsigned long long my_stats;
+  unsigned long long wsc[ST / 32];        // scan scratch
+  unsigned wfind[NB / 32];
+  int candn[SCL];                         // bucket elements pushed by every rank
+  int lpre[3];                            // previous tokens < s0, < s1, < len
+  int csel[SCL], cselp[SCL];              // selected bucket elements per rank (& previous)
+  int find[3];                            // bin, above, count
+  int ncand;
+  unsigned long long T;
+  unsigned long long total;
+};
+
+// composite key of token p given its group-score bits
+__device__ __forceinline__ unsigned long long key_of(uint32_t vb, int p, int len, int force) {
+  return composite((force && p == len - 1) ? 0x7F800000u : vb, p);
+}
+
+// Block-wide exclusive scan of one uint64 per thread (ST threads).
+__device__ __forceinline__ unsigned long long scan_u64(SelSm& s, unsigned long long v) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  unsigned long long incl = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  if (lane == 31) s.wsc[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    const unsigned long long x = lane < ST / 32 ? s.wsc[lane] : 0ull;
+    unsigned long long xi = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long t = __shfl_up_sync(0xffffffffu, xi, o);
+      if (lane >= o) xi += t;
+    }
+    if (lane < ST / 32) s.wsc[lane] = xi - x;
+    if (lane == 31) s.total = xi;
+  }
+  __syncthreads();
+  return s.wsc[warp] + incl - v;
+}
+
+// Push the nonzero bins of the local histogram into red[buf] of every CTA.
+__device__ __forceinline__ void push_hist(SelSm& s, cg::cluster_group& cl, int buf) {
+  const int t = threadIdx.x;
+  if (t < NB) {
+    const unsigned h = s.hist[t];
+    if (h) {
+#pragma unroll
+      for (int q = 0; q < SCL; ++q) atomicAdd(cl.map_shared_rank(&s.red[buf][t], q), h);
+    }
+  }
+}
+
+// After the cluster barrier: bin of the r-th largest element counted from the top of
+// red[buf] -> s.find = {bin, count above it, count in it}.  Clears red[buf].
+__device__ __forceinline__ void find_bin(SelSm& s, int buf, int r) {
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  unsigned c = 0, incl = 0;
+  if (t < NB) {
+    c = s.red[buf][NB - 1 - t];  // thread t holds bin NB-1-t: ascending t = descending bins
+    s.red[buf][NB - 1 - t] = 0u;
+    incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned x = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += x;
+    }
+    if (lane == 31) s.wfind[warp] = incl;
+  }
+  __syncthreads();
+  if (t < NB) {
+    unsigned before = 0;
+    for (int w = 0; w < warp; ++w) before += s.wfind[w];
+    incl += before;
+    if (incl >= (unsigned)r && incl - c < (unsigned)r) {
+      s.find[0] = NB - 1 - t;
+      s.find[1] = (int)(incl - c);
+      s.find[2] = (int)c;
+    }
+  }
+  __syncthreads();
+}
+
+template <int ALPHA, int NC>
+__global__ void __cluster_dims__(SCL, 1, 1) __launch_bounds__(ST, 1) select_kernel(
+    const float* __restrict__ logits, const float* __restrict__ head_max,
+    const int32_t* __restrict__ seq_len, int G, int Smax, int k, int force,
+    int64_t* __restrict__ head_sumfix, float* __restrict__ group_score,
+    int32_t* __restrict__ out_idx, int32_t* __restrict__ out_count,
+    const int32_t* __restrict__ prev_idx, const int32_t* __restrict__ prev_count,
+    int32_t* __restrict__ load_tok, int32_t* __restrict__ n_load, int32_t* __restrict__ evict_tok,
+    int32_t* __restrict__ n_evict) {
+  extern __shared__ __align__(16) uint8_t sel_raw[];
+  SelSm& s = *reinterpret_cast<SelSm*>(sel_raw);
+  cg::cluster_group cl = cg::this_cluster();
+  const int rank = (int)cl.block_rank();
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int bg = blockIdx.y, b = bg / G, g = bg - b * G;
+  const int Hq = G * ALPHA;
+  const int len = min(max(seq_len[b], 0), Smax);
+  const int need = min(k, len);
+  const int per = ((len + SCL - 1) / SCL + 3) & ~3;
+  const int s0 = min(len, rank * per), s1 = min(len, s0 + per);
+  const int nch = (s1 - s0 + 3) >> 2;  // float4 chunks of the segment
+  // this thread's tokens: the contiguous chunks [c0, c1) (ordered output needs only a scan)
+  const int cpt = max(1, (nch + ST - 1) / ST);
+  const int c0 = min(nch, tid * cpt), c1 = min(nch, c0 + cpt);
+  const float* lg = logits + ((size_t)b * Hq + g * ALPHA) * Smax + s0;
+  const int np = min(max(prev_count[bg], 0), k);
+  const int32_t* pv = prev_idx + (size_t)bg * k;
+  sel_mark(0);
+
+  // ---- prologue: logits of the first NC chunks and the previous selection in flight
+  float4 x0[NC][ALPHA];
+#pragma unroll
+  for (int u = 0; u < NC; ++u)
+#pragma unroll
+    for (int j = 0; j < ALPHA; ++j)
+      x0[u][j] = c0 + u < c1 ? __ldg(reinterpret_cast<const float4*>(lg + (size_t)j * Smax) + c0 + u)
+                             : make_float4(0.f, 0.f, 0.f, 0.f);
+  constexpr int PVR = SPC_MAX_K / ST;
+  int pvr[PVR];
+#pragma unroll
+  for (int i = 0; i < PVR; ++i) pvr[i] = tid + i * ST < np ? pv[tid + i * ST] : -1;
+  float m[ALPHA];
+#pragma unroll
+  for (int j = 0; j < ALPHA; ++j) m[j] = head_max[(size_t)b * Hq + g * ALPHA + j];
+  const int nw = (s1 - s0 + 31) >> 5;
+  for (int i = tid; i < nw; i += ST) s.bm_prev[i] = 0u;
+  if (tid < NB) {
+    s.hist[tid] = 0u;
+    s.red[0][tid] = 0u;
+    s.red[1][tid] = 0u;
+  }
+  if (tid < 3) s.lpre[tid] = 0;
+  if (tid < SCL) s.csel[tid] = s.cselp[tid] = 0;
+  if (tid == 0) {
+    s.ncand = 0;
+    s.my_stats = 0ull;
+  }
+  __syncthreads();
+  {  // bitmap of the previous tokens in this segment; prefix counts of the sorted list
+    int c_s0 = 0, c_s1 = 0, c_len = 0;
+#pragma unroll
+    for (int i = 0; i < PVR; ++i) {
+      const int t = pvr[i];
+      if (t >= 0) {
+        if (t >= s0 && t < s1) atomicOr(&s.bm_prev[(t - s0) >> 5], 1u << ((t - s0) & 31));
+        c_s0 += t < s0;
+        c_s1 += t < s1;
+        c_len += t < len;
+      }
+    }
+    c_s0 = __reduce_add_sync(0xffffffffu, c_s0);
+    c_s1 = __reduce_add_sync(0xffffffffu, c_s1);
+    c_len = __reduce_add_sync(0xffffffffu, c_len);
+    if (lane == 0) {
+      if (c_s0) atomicAdd(&s.lpre[0], c_s0);
+      if (c_s1) atomicAdd(&s.lpre[1], c_s1);
+      if (c_len) atomicAdd(&s.lpre[2], c_len);
+    }
+  }
+  sel_mark(10);
+
+  // ---- NORM (O3, O4)
+  long long acc[ALPHA];
+  float e0[NC][ALPHA][4];
+#pragma unroll
+  for (int j = 0; j < ALPHA; ++j) acc[j] = 0;
+#pragma unroll
+  for (int u = 0; u < NC; ++u) {
+    const int p0 = 4 * (c0 + u);  // segment-relative token of e0[u][.][0]
+#pragma unroll
+    for (int j = 0; j < ALPHA; ++j) {
+      const float2 ea = spc_exp2_dev(__fsub_rn(x0[u][j].x, m[j]), __fsub_rn(x0[u][j].y, m[j]));
+      const float2 eb = spc_exp2_dev(__fsub_rn(x0[u][j].z, m[j]), __fsub_rn(x0[u][j].w, m[j]));
+      const float es[4] = {ea.x, ea.y, eb.x, eb.y};
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const float e = (c0 + u < c1 && p0 + c < s1 - s0) ? es[c] : 0.0f;
+        e0[u][j][c] = e;
+        acc[j] += fixpoint40(e);
+      }
+    }
+  }
+  for (int ch = c0 + NC; ch < c1; ++ch) {  // segments longer than 4 * NC * ST tokens
+#pragma unroll
+    for (int j = 0; j < ALPHA; ++j) {
+      const float4 x = __ldg(reinterpret_cast<const float4*>(lg + (size_t)j * Smax) + ch);
+      const float xs[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        if (4 * ch + c < s1 - s0) acc[j] += fixpoint40(spc_exp_dev(__fsub_rn(xs[c], m[j])));
+    }
+  }
+  sel_mark(11);
+#pragma unroll
+  for (int j = 0; j < ALPHA; ++j) {
+    const long long v = warp_sum_ll(acc[j]);
+    if (lane == 0) s.wred[warp][j] = v;
+  }
+  __syncthreads();
+  if (tid < ALPHA) {
+    long long t = 0;
+#pragma unroll
+    for (int w = 0; w < ST / 32; ++w) t += s.wred[w][tid];
+#pragma unroll
+    for (int q = 0; q < SCL; ++q) cl.map_shared_rank(&s.part[0][0], q)[rank * 8 + tid] = t;
+  }
+  sel_mark(12);
+  cl.sync();
+  sel_mark(1);
+
+  // ---- GROUP (O4..O6) + pass-0 histogram
+  float r[ALPHA];
+  float gmax = 0.0f;
+#pragma unroll
+  for (int j = 0; j < ALPHA; ++j) {
+    long long F = 0;
+#pragma unroll
+    for (int q = 0; q < SCL; ++q) F += s.part[q][j];
+    if (rank == 0 && tid == 0) head_sumfix[(size_t)b * Hq + g * ALPHA + j] = F;
+    r[j] = __fdiv_rn(1.0f, __fmul_rn(__ll2float_rn(F), 9.094947017729282379150390625e-13f));
+    gmax = fmaxf(gmax, r[j]);
+  }
+  const int top = (int)(__float_as_uint(gmax) >> W0_SHIFT);
+  const int base0 = top - (NB - 1);
+  float* gso = group_score + (size_t)bg * Smax + s0;
+  const bool cut = need < len;
+#pragma unroll
+  for (int u = 0; u < NC; ++u) {
+    const int ch = c0 + u;
+    if (ch < c1) {
+      float gs[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        float v = __fmul_rn(e0[u][0][c], r[0]);
+#pragma unroll
+        for (int j = 1; j < ALPHA; ++j) v = fmaxf(v, __fmul_rn(e0[u][j][c], r[j]));
+        gs[c] = v;
+        const int p = 4 * ch + c;
+        if (cut && p < s1 - s0) {
+          const unsigned long long key = key_of(__float_as_uint(v), s0 + p, len, force);
+          atomicAdd(&s.hist[min(max((int)(key >> 52) - base0, 0), NB - 1)], 1u);
+        }
+      }
+      const float4 o = make_float4(gs[0], gs[1], gs[2], gs[3]);
+      reinterpret_cast<float4*>(s.seg)[ch] = o;
+      reinterpret_cast<float4*>(gso)[ch] = o;  // tokens past len in the chunk get 0
+    }
+  }
+  for (int ch = c0 + NC; ch < c1; ++ch) {
+    float e[ALPHA][4];
+#pragma unroll
+    for (int j = 0; j < ALPHA; ++j) {
+      const float4 x = __ldg(reinterpret_cast<const float4*>(lg + (size_t)j * Smax) + ch);
+      const float xs[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        e[j][c] = 4 * ch + c < s1 - s0 ? spc_exp_dev(__fsub_rn(xs[c], m[j])) : 0.0f;
+    }
+    float gs[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      float v = __fmul_rn(e[0][c], r[0]);
+#pragma unroll
+      for (int j = 1; j < ALPHA; ++j) v = fmaxf(v, __fmul_rn(e[j][c], r[j]));
+      gs[c] = v;
+      const int p = 4 * ch + c;
+      if (cut && p < s1 - s0) {
+        const unsigned long long key = key_of(__float_as_uint(v), s0 + p, len, force);
+        atomicAdd(&s.hist[min(max((int)(key >> 52) - base0, 0), NB - 1)], 1u);
+      }
+    }
+    const float4 o = make_float4(gs[0], gs[1], gs[2], gs[3]);
+    reinterpret_cast<float4*>(s.seg)[ch] = o;
+    reinterpret_cast<float4*>(gso)[ch] = o;
+  }
+  {  // zero-fill group_score [roundup4(len), Smax)
+    float4* gz = reinterpret_cast<float4*>(group_score + (size_t)bg * Smax);
+    for (int p4 = ((len + 3) >> 2) + rank * ST + tid; p4 < (Smax >> 2); p4 += SCL * ST)
+      gz[p4] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  __syncthreads();
+  sel_mark(2);
+
+  // ---- top-k (O7): selected = {key >= T}; counts of selected tokens (and of those that
+  // were previously selected) in the ranks before this one (b_) and in the row (a_)
+  unsigned long long T = 0ull;
+  int b_sel = 0, b_selp = 0, a_sel = 0, a_selp = 0;
+  if (cut) {
+    push_hist(s, cl, 0);
+    cl.sync();
+    find_bin(s, 0, need);
+    const int bin0 = s.find[0];
+    int rr = need - s.find[1], cm = s.find[2];
+    unsigned long long P = 0ull, xlo = 0ull, xmax = ~0ull;
+    int bits = 1;  // key bit 63 (sign of the value) is always 0
+    if (bin0 == 0) {
+      xmax = ((unsigned long long)(uint32_t)(base0 + 1) << 52) - 1ull;
+    } else if (bin0 == NB - 1) {
+      xlo = (unsigned long long)(uint32_t)top << 52;
+    } else {
+      P = (unsigned long long)(uint32_t)(base0 + bin0) << 52;
+      bits = W0_BITS;
+    }
+    sel_mark(3);
+    int buf = 1;
+    while (cm != rr && cm > CANDMAX) {
+      const int db = min(8, 64 - bits), sh = 64 - bits - db;
+      const unsigned mask = (1u << db) - 1u;
+      if (tid < NB) s.hist[tid] = 0u;
+      __syncthreads();
+      for (int ch = c0; ch < c1; ++ch) {
+        const float4 v = reinterpret_cast<const float4*>(s.seg)[ch];
+        const float vs[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const int p = 4 * ch + c;
+          if (p < s1 - s0) {
+            const unsigned long long x = key_of(__float_as_uint(vs[c]), s0 + p, len, force);
+            if ((x >> (64 - bits)) == (P >> (64 - bits)) && x >= xlo && x <= xmax)
+              atomicAdd(&s.hist[(unsigned)(x >> sh) & mask], 1u);
+          }
+        }
+      }
+      __syncthreads();
+      push_hist(s, cl, buf);
+      cl.sync();
+      find_bin(s, buf, rr);
+      rr -= s.find[1];
+      cm = s.find[2];
+      P |= (unsigned long long)s.find[0] << sh;
+      bits += db;
+      buf ^= 1;
+    }
+    sel_mark(4);
+    // this CTA's counts of tokens above the bucket / in it (each also & previous); the
+    // bucket itself is pushed to every CTA unless it is selected whole (cm == rr)
+    const bool xchg = cm != rr;
+    unsigned long long st4 = 0ull;  // above | above&prev << 16 | bucket << 32 | bucket&prev << 48
+    for (int ch = c0; ch < c1; ++ch) {
+      const float4 v = reinterpret_cast<const float4*>(s.seg)[ch];
+      const float vs[4] = {v.x, v.y, v.z, v.w};
+      const uint32_t pw = s.bm_prev[ch >> 3] >> ((ch & 7) * 4);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int p = 4 * ch + c;
+        if (p < s1 - s0) {
+          const unsigned long long x = key_of(__float_as_uint(vs[c]), s0 + p, len, force);
+          const bool was = (pw >> c) & 1u;
+          const bool peq = (x >> (64 - bits)) == (P >> (64 - bits));
+          const bool above = x > xmax || (x >> (64 - bits)) > (P >> (64 - bits));
+          const bool inb = peq && x >= xlo && x <= xmax;
+          st4 += (unsigned long long)above + ((unsigned long long)(above && was) << 16) +
+                 ((unsigned long long)inb << 32) + ((unsigned long long)(inb && was) << 48);
+          if (inb && xchg) {
+            const int slot = atomicAdd(&s.ncand, 1);
+#pragma unroll
+            for (int q = 0; q < SCL; ++q) {
+              cl.map_shared_rank(&s.cand[rank][slot], q)[0] = x;
+              cl.map_shared_rank(&s.candp[rank][slot], q)[0] = (uint8_t)was;
+            }
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) st4 += __shfl_xor_sync(0xffffffffu, st4, o);
+    if (lane == 0 && st4) atomicAdd(&s.my_stats, st4);
+    __syncthreads();
+    if (tid < SCL) {
+      cl.map_shared_rank(&s.stats[rank], tid)[0] = s.my_stats;
+      cl.map_shared_rank(&s.candn[rank], tid)[0] = xchg ? s.ncand : 0;
+    }
+    cl.sync();
+    sel_mark(9);
+    if (!xchg) {
+      T = P > xlo ? P : xlo;  // the whole bucket is selected: T = its lower end
+#pragma unroll
+      for (int q = 0; q < SCL; ++q) {
+        const unsigned long long sq = s.stats[q];
+        const int sl = (int)(sq & 0xFFFF) + (int)((sq >> 32) & 0xFFFF);
+        const int sp = (int)((sq >> 16) & 0xFFFF) + (int)(sq >> 48);
+        a_sel += sl;
+        a_selp += sp;
+        b_sel += q < rank ? sl : 0;
+        b_selp += q < rank ? sp : 0;
+      }
+    } else {
+      // rank the bucket by counting (4 threads per candidate) after flattening it
+      int nall = 0;
+#pragma unroll
+      for (int q = 0; q < SCL; ++q) nall += s.candn[q];
+      unsigned long long mine = 0ull;
+      int mine_q = 0, mine_p = 0;
+      if (tid < nall) {
+        int i = tid, q = 0;
+        while (i >= s.candn[q]) i -= s.candn[q++];
+        mine = s.cand[q][i];
+        mine_q = q;
+        mine_p = s.candp[q][i];
+      }
+      unsigned long long* flat = &s.cand[SCL - 1][0];
+      __syncthreads();  // every region read before the flat copy overwrites the last one
+      if (tid < nall) flat[tid] = mine;
+      __syncthreads();
+      {
+        const int ci = tid >> 2, part = tid & 3;
+        int larger = 0;
+        if (ci < nall) {
+          const unsigned long long x = flat[ci];
+#pragma unroll 4
+          for (int j = part; j < nall; j += 4) larger += flat[j] > x;
+        }
+        larger += __shfl_xor_sync(0xffffffffu, larger, 1);
+        larger += __shfl_xor_sync(0xffffffffu, larger, 2);
+        if (ci < nall && part == 0 && larger == rr - 1) s.T = flat[ci];
+      }
+      __syncthreads();
+      T = s.T;
+      if (tid < nall && mine >= T) {
+        atomicAdd(&s.csel[mine_q], 1);
+        if (mine_p) atomicAdd(&s.cselp[mine_q], 1);
+      }
+      __syncthreads();
+#pragma unroll
+      for (int q = 0; q < SCL; ++q) {
+        const unsigned long long sq = s.stats[q];
+        const int sl = (int)(sq & 0xFFFF) + s.csel[q];
+        const int sp = (int)((sq >> 16) & 0xFFFF) + s.cselp[q];
+        a_sel += sl;
+        a_selp += sp;
+        b_sel += q < rank ? sl : 0;
+        b_selp += q < rank ? sp : 0;
+      }
+    }
+  } else {
+    // no cut: every token is selected
+    b_sel = s0;
+    a_sel = len;
+    b_selp = s.lpre[0];
+    a_selp = s.lpre[2];
+  }
+  sel_mark(5);
+
+  // ---- ordered writes: selection (O7), new tokens and evictions (O8).  Evicted = previous
+  // tokens not selected; the previous tokens >= len (never selected) are listed last.
+  const int bs = b_sel, bn = b_sel - b_selp, be = s.lpre[0] - b_selp;
+  const int as = a_sel, an = a_sel - a_selp, ae = np - a_selp;
+  const int ntail = np - s.lpre[2];
+  unsigned long long cnt = 0ull;  // selected | new << 21 | evicted << 42
+  for (int ch = c0; ch < c1; ++ch) {
+    const float4 v = reinterpret_cast<const float4*>(s.seg)[ch];
+    const float vs[4] = {v.x, v.y, v.z, v.w};
+    const uint32_t pw = s.bm_prev[ch >> 3] >> ((ch & 7) * 4);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int p = 4 * ch + c;
+      if (p < s1 - s0) {
+        const bool sel = key_of(__float_as_uint(vs[c]), s0 + p, len, force) >= T;
+        const bool was = (pw >> c) & 1u;
+        cnt += (unsigned long long)sel + ((unsigned long long)(sel && !was) << 21) +
+               ((unsigned long long)(!sel && was) << 42);
+      }
+    }
+  }
+  const unsigned long long pos = scan_u64(s, cnt);
+  int32_t* oi = out_idx + (size_t)bg * k;
+  int32_t* lt = load_tok + (size_t)bg * k;
+  int32_t* et = evict_tok ? evict_tok + (size_t)bg * k : nullptr;
+  int ps = bs + (int)(pos & 0x1FFFFF), pn = bn + (int)((pos >> 21) & 0x1FFFFF),
+      pe = be + (int)(pos >> 42);
+  for (int ch = c0; ch < c1; ++ch) {
+    const float4 v = reinterpret_cast<const float4*>(s.seg)[ch];
+    const float vs[4] = {v.x, v.y, v.z, v.w};
+    const uint32_t pw = s.bm_prev[ch >> 3] >> ((ch & 7) * 4);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int p = 4 * ch + c;
+      if (p < s1 - s0) {
+        const int t = s0 + p;
+        const bool sel = key_of(__float_as_uint(vs[c]), t, len, force) >= T;
+        const bool was = (pw >> c) & 1u;
+        if (sel) oi[ps++] = t;
+        if (sel && !was) lt[pn++] = t;
+        if (!sel && was && et) et[pe++] = t;
+      }
+    }
+  }
+  if (rank == SCL - 1) {
+    if (et)
+      for (int i = tid; i < ntail; i += ST) et[ae - ntail + i] = pv[np - ntail + i];
+    for (int i = as + tid; i < k; i += ST) oi[i] = -1;
+    for (int i = an + tid; i < k; i += ST) lt[i] = -1;
+    if (et)
+      for (int i = ae + tid; i < k; i += ST) et[i] = -1;
+  }
+  if (rank == 0 && tid == 0) {
+    out_count[bg] = as;
+    n_load[bg] = an;
+    if (n_evict) n_evict[bg] = ae;
+  }
+  sel_mark(7);
+}
+
+}  // namespace
+}  // namespace spc
+
+using namespace spc;
+
+// debug only (not in include/spc.h): point the -DSPC_TRACE stamps at a device buffer of
+// SCL x 16 uint64, or NULL to stop
+extern "C" int spc_debug_set_select_trace(unsigned long long* buf) {
+  return cudaMemcpyToSymbol(spc::g_sel_trace, &buf, sizeof(buf)) == cudaSuccess ? SPC_OK
+                                                                                 : SPC_E_CUDA;
+}
+
+extern "C" int spc_select(const float* logits, const float* head_max, const int32_t* seq_len, int B,
+                          int Hq, int G, int Smax, int k, int force_last, int64_t* head_sumfix,
+                          float* group_score, int32_t* out_idx, int32_t* out_count,
+                          const int32_t* prev_idx, const int32_t* prev_count, int32_t* load_tok,
+                          int32_t* n_load, int32_t* evict_tok, int32_t* n_evict,
+                          spc_stream_t stream) {
+  if (!logits || !head_max || !seq_len || !head_sumfix || !group_score || !out_idx ||
+      !out_count || !prev_idx || !prev_count || !load_tok || !n_load)
+    return SPC_E_NULL;
+  if (B <= 0 || G <= 0 || Hq <= 0 || Hq % G || Smax <= 0) return SPC_E_SHAPE;
+  if (k < 1 || k > SPC_MAX_K) return SPC_E_BUDGET;
+  if (Smax > SCL * SEGCAP || Smax % 4) return SPC_E_UNSUPPORTED;
+  const int alpha = Hq / G;
+  cudaStream_t st = as_stream(stream);
+#define SEL(AA)                                                                                 \
+  if (alpha == AA) {                                                                            \
+    static bool attr = false;                                                                   \
+    if (!attr) {                                                                                \
+      SPC_TRY(cudaFuncSetAttribute((const void*)select_kernel<AA, (AA > 4 ? 1 : 2)>,                              \
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize,                 \
+                                   (int)sizeof(SelSm)));                                        \
+      attr = true;                                                                              \
+    }                                                                                           \
+    select_kernel<AA, (AA > 4 ? 1 : 2)><<<dim3(SCL, B * G), ST, sizeof(SelSm), st>>>(                             \
+        logits, head_max, seq_len, G, Smax, k, force_last, head_sumfix, group_score, out_idx,   \
+        out_count, prev_idx, prev_count, load_tok, n_load, evict_tok, n_evict);                 \
+    return launched();                                                                          \
+  }
+  SEL(1) SEL(2) SEL(4) SEL(8)
+#undef SEL
+  return SPC_E_UNSUPPORTED;
+}

@@ -186,22 +186,17 @@ struct ClSmem {
   int total;
 };
 
-__global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(SEL_THREADS, 1)
-    topk_cluster_kernel(const float* __restrict__ val, const int32_t* __restrict__ seq_len, int G,
-                        int n_cols, int k, int force, int stride, int offset,
-                        int32_t* __restrict__ out_idx, float* __restrict__ out_val,
-                        int32_t* __restrict__ out_count, unsigned long long* __restrict__ out_thresh) {
-  extern __shared__ __align__(16) uint8_t cl_raw[];
-  ClSmem& s = *reinterpret_cast<ClSmem*>(cl_raw);
-  cg::cluster_group cl = cg::this_cluster();
+// The selection of one row by a cluster: every CTA passes the key functor for its
+// own segment [s0, s1) of the row (key(p) is only called for p in the segment).
+// Writes out_idx/out_val/out_count/out_thresh of the row; returns this CTA's
+// offset and number of selected positions (its part of the ascending list).
+template <class KeyFn>
+__device__ void cluster_select(ClSmem& s, cg::cluster_group& cl, const KeyFn& key, int len, int k,
+                               int s0, int s1, int32_t* oi, float* ov, int32_t* out_count,
+                               unsigned long long* out_thresh, int* my_base, int* my_count) {
   const int rank = (int)cl.block_rank();
-  const int row = blockIdx.y, tid = threadIdx.x, lane = tid & 31;
-  const int len = row_len(seq_len, row, G, n_cols);
+  const int tid = threadIdx.x, lane = tid & 31;
   const int need = k < len ? k : len;
-  const float* v = val + (size_t)row * n_cols;
-  const DenseKey key{v, len, force, stride, offset};
-  const int per = (len + CL - 1) / CL;
-  const int s0 = min(len, rank * per), s1 = min(len, s0 + per);
   unsigned long long T = 0;
   if (need < len) {
     // ---- 1. top-11-bit histogram, reduced over the cluster
@@ -289,8 +284,8 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(SEL_THREADS, 1)
     base += q < rank ? s.counts[q] : 0;
     all += s.counts[q];
   }
-  int32_t* oi = out_idx + (size_t)row * k;
-  float* ov = out_val ? out_val + (size_t)row * k : nullptr;
+  *my_base = base;
+  *my_count = s.counts[rank];
   pos += base;
   for (int p = q0; p < q1; ++p) {
     const unsigned long long x = key(p);
@@ -306,9 +301,29 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(SEL_THREADS, 1)
       if (ov) ov[i] = 0.0f;
     }
   if (rank == 0 && tid == 0) {
-    out_count[row] = all;
-    if (out_thresh) out_thresh[row] = need < len ? T : 0ull;
+    *out_count = all;
+    if (out_thresh) *out_thresh = need < len ? T : 0ull;
   }
+}
+
+__global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(SEL_THREADS, 1)
+    topk_cluster_kernel(const float* __restrict__ val, const int32_t* __restrict__ seq_len, int G,
+                        int n_cols, int k, int force, int stride, int offset,
+                        int32_t* __restrict__ out_idx, float* __restrict__ out_val,
+                        int32_t* __restrict__ out_count, unsigned long long* __restrict__ out_thresh) {
+  extern __shared__ __align__(16) uint8_t cl_raw[];
+  ClSmem& s = *reinterpret_cast<ClSmem*>(cl_raw);
+  cg::cluster_group cl = cg::this_cluster();
+  const int rank = (int)cl.block_rank();
+  const int row = blockIdx.y;
+  const int len = row_len(seq_len, row, G, n_cols);
+  const DenseKey key{val + (size_t)row * n_cols, len, force, stride, offset};
+  const int per = (len + CL - 1) / CL;
+  const int s0 = min(len, rank * per), s1 = min(len, s0 + per);
+  int my_base, my_count;
+  cluster_select(s, cl, key, len, k, s0, s1, out_idx + (size_t)row * k,
+                 out_val ? out_val + (size_t)row * k : nullptr, out_count + row,
+                 out_thresh ? out_thresh + row : nullptr, &my_base, &my_count);
 }
 
 // ------------------------------------------------------------------ merge (O13)

@@ -3,7 +3,8 @@
 Step: spc_score (LOGITS, NORM, GROUP) -> spc_topk (force the
 newest token, R10) -> spc_elastic_diff against the previous step's selection
  -> [SLOTS mode: spc_gather_kv of the new rows into budget slots] ->
-spc_sparse_decode_attn over all L layers (one launch).
+spc_sparse_decode_attn over all L layers (one launch).  In INDEXED mode with
+Smax <= 131072 the NORM..diff calls are the single fused spc_select launch.
 
 The step state (previous selection, slot map) ping-pongs between two buffers,
 so two CUDA graphs (even / odd step) replay the whole step with one launch
@@ -23,11 +24,15 @@ from . import spc
 class DecodeStep:
     def __init__(self, kr: torch.Tensor, k_layers, v_layers, seq_len: torch.Tensor, L: int,
                  Hq: int, k: int, mode: str = "indexed", force_last: bool = True, scale=None,
-                 kv_rows=None, k_src_layers=None, v_src_layers=None):
+                 kv_rows=None, k_src_layers=None, v_src_layers=None, fused=None):
         """kr: retrieval keys [B][G][Smax][D] bf16.  k_layers/v_layers: L tensors [B][G][rows][D]
         (INDEXED: the full caches; SLOTS: the budget buffers [B][G][k][D], with
         k_src_layers/v_src_layers the full caches, device or mapped host)."""
         self.dev = kr.device
+        # fused spc_select (one launch for NORM..diff) where it applies: INDEXED mode and
+        # Smax <= 131072, a multiple of 4; otherwise the separate ABI calls
+        self.fused = (mode == "indexed" and kr.shape[2] <= 131072 and kr.shape[2] % 4 == 0) \
+            if fused is None else fused
         self.B, self.G, self.Smax, self.D = kr.shape
         self.L, self.Hq, self.k = L, Hq, k
         self.alpha = Hq // self.G
@@ -88,13 +93,23 @@ class DecodeStep:
     def enqueue(self, parity: int, stream=None):
         """Enqueue one step writing the selection into idx[parity] (prev = idx[1-parity])."""
         cur, prev = parity, 1 - parity
-        spc.score(self.q_ret, self.kr, self.seq_len, self.G, self.scale, self.logits,
-                  self.head_max, self.head_sumfix, self.gs, self.ws_score, stream=stream)
-        spc.topk(self.gs, self.seq_len, self.k, self.idx[cur], self.cnt[cur], self.ws_topk,
-                 force_last=self.force_last, stream=stream)
-        spc.elastic_diff(self.idx[prev], self.cnt[prev], self.idx[cur], self.cnt[cur],
-                         self.load_tok, self.n_load, slot_tok=self.slot_tok,
-                         load_slot=self.load_slot, stream=stream)
+        if self.fused:
+            # LOGITS, then NORM + GROUP + top-k + diff in one cluster launch (spc_select)
+            spc.score(self.q_ret, self.kr, self.seq_len, self.G, self.scale, self.logits,
+                      self.head_max, self.head_sumfix, self.gs, self.ws_score,
+                      phases=spc.SCORE_LOGITS, stream=stream)
+            spc.select(self.logits, self.head_max, self.seq_len, self.G, self.k,
+                       self.head_sumfix, self.gs, self.idx[cur], self.cnt[cur], self.idx[prev],
+                       self.cnt[prev], self.load_tok, self.n_load, force_last=self.force_last,
+                       stream=stream)
+        else:
+            spc.score(self.q_ret, self.kr, self.seq_len, self.G, self.scale, self.logits,
+                      self.head_max, self.head_sumfix, self.gs, self.ws_score, stream=stream)
+            spc.topk(self.gs, self.seq_len, self.k, self.idx[cur], self.cnt[cur], self.ws_topk,
+                     force_last=self.force_last, stream=stream)
+            spc.elastic_diff(self.idx[prev], self.cnt[prev], self.idx[cur], self.cnt[cur],
+                             self.load_tok, self.n_load, slot_tok=self.slot_tok,
+                             load_slot=self.load_slot, stream=stream)
         if self.mode == "slots":
             spc.gather_kv(self.k_src_tab, self.v_src_tab, self.L, self.B, self.G, self.D,
                           self.src_rows, self.k, self.load_tok, self.load_slot, self.n_load,

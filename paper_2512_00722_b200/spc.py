@@ -27,6 +27,7 @@ EXPORTS = [
     "spc_score_workspace", "spc_score", "spc_topk_workspace", "spc_topk",
     "spc_topk_merge_workspace", "spc_topk_merge", "spc_topk_filter", "spc_elastic_diff",
     "spc_gather_kv", "spc_attn_workspace", "spc_sparse_decode_attn", "spc_attn_merge",
+    "spc_select",
 ]
 
 
@@ -68,6 +69,8 @@ def load_library(path: str = LIB_PATH):
     L.spc_sparse_decode_attn.argtypes = [i32, P, P, P, i32, P, P, i32, i32, i32, i32, i32, i32,
                                          i32, i32, i32, f32, P, P, P, sz, P]
     L.spc_attn_merge.argtypes = [P, P, i32, i32, i32, P, P, P]
+    L.spc_select.argtypes = [P, P, P, i32, i32, i32, i32, i32, i32, P, P, P, P, P, P, P, P, P, P,
+                             P]
     for name in EXPORTS:  # every symbol must resolve (raises AttributeError otherwise)
         getattr(L, name)
     return L
@@ -202,6 +205,17 @@ def sparse_decode_attn(q, k_tab, v_tab, kv_mode: int, idx, count, rows: int, k: 
                                         _p(idx), _p(count), L, layer_begin, layer_end, B, Hq, G, D,
                                         rows, k, float(scale), _p(out), _p(lse), _p(ws),
                                         ws.numel(), _s(stream)), "spc_sparse_decode_attn")
+
+
+def select(logits, head_max, seq_len, G: int, k: int, head_sumfix, group_score, out_idx,
+           out_count, prev_idx, prev_count, load_tok, n_load, evict_tok=None, n_evict=None,
+           force_last: bool = False, stream=None):
+    """spc_select: fused NORM + GROUP + top-k + INDEXED elastic diff (one launch)."""
+    B, Hq, Smax = logits.shape
+    _check(lib().spc_select(_p(logits), _p(head_max), _p(seq_len), B, Hq, G, Smax, k,
+                            int(force_last), _p(head_sumfix), _p(group_score), _p(out_idx),
+                            _p(out_count), _p(prev_idx), _p(prev_count), _p(load_tok),
+                            _p(n_load), _p(evict_tok), _p(n_evict), _s(stream)), "spc_select")
 
 
 def attn_merge(o_parts, lse_parts, out, lse_out=None, stream=None):

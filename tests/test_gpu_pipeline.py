@@ -15,7 +15,7 @@ pytestmark = pytest.mark.gpu
 DEV = "cuda"
 
 
-def build(cfg, seed, mode="indexed", steps=3):
+def build(cfg, seed, mode="indexed", steps=3, fused=None):
     c = synth.CONFIGS[cfg]
     B, G, Hq, D, S, L, k = c["B"], c["G"], c["Hq"], c["D"], c["S"], c["L"], c["k"]
     kr = synth.retrieval_keys(B, G, S, D, seed=seed, device=DEV)
@@ -30,7 +30,8 @@ def build(cfg, seed, mode="indexed", steps=3):
                         mode="slots", k_src_layers=[kc[l] for l in range(L)],
                         v_src_layers=[vc[l] for l in range(L)])
     else:
-        st = DecodeStep(kr, [kc[l] for l in range(L)], [vc[l] for l in range(L)], seq, L, Hq, k)
+        st = DecodeStep(kr, [kc[l] for l in range(L)], [vc[l] for l in range(L)], seq, L, Hq, k,
+                        fused=fused)
     return c, st, kr, kc, vc, qr, ql
 
 
@@ -40,10 +41,11 @@ def oracle_step(oracle, c, kr_h, q_h, S, scale):
     return idx, cnt
 
 
-@pytest.mark.parametrize("mode,use_graph", [("indexed", False), ("indexed", True),
-                                            ("slots", True)])
-def test_pipeline_config_a(oracle, mode, use_graph):
-    c, st, kr, kc, vc, qr, ql = build("A", synth.BASE_SEED, mode)
+@pytest.mark.parametrize("mode,use_graph,fused", [("indexed", False, None), ("indexed", True, None),
+                                                  ("indexed", True, False), ("slots", True, None)])
+def test_pipeline_config_a(oracle, mode, use_graph, fused):
+    c, st, kr, kc, vc, qr, ql = build("A", synth.BASE_SEED, mode, fused=fused)
+    assert st.fused == (mode == "indexed" and fused is None)
     S, scale = c["S"], st.scale
     kr_h = synth.bf16_bits(kr)
     kh, vh = synth.bf16_bits(kc), synth.bf16_bits(vc)

@@ -78,3 +78,59 @@ def test_score_config_b_full_size(oracle):
     q = synth.retrieval_queries(1, 1, c["Hq"], c["G"], c["D"], seed=synth.BASE_SEED + 1,
                                 device="cuda")[0]
     check(oracle, q.cpu(), kr.cpu(), [c["S"]], c["G"], f32(1 / math.sqrt(c["D"])))
+
+
+def test_exp_and_fixpoint_sweep_through_norm_group(oracle):
+    """O3/O4 on a sweep of the whole exp domain: every 256th float32 in [-87.5, 0] plus the
+    edge values, as one head's logits with head max 0.  The group score of a single-head
+    group is e * r per token, so every exp value is checked bit-exactly (NORM and GROUP
+    of spc_score, and the fused spc_select), and the int64 normaliser checks every
+    fixed-point conversion's sum."""
+    hi = np.frombuffer(np.float32(-87.5).tobytes(), np.uint32)[0]
+    bits = np.arange(0x80000000, hi + 1, 256, dtype=np.uint64).astype(np.uint32)
+    edge = np.array([0.0, -0.0, -87.0, np.nextafter(np.float32(-87), np.float32(0)),
+                     np.nextafter(np.float32(-87), np.float32(-100)), -1e-45, -1e-38, -0.5,
+                     -0.6931472, -1.0, -2.0, -86.99], np.float32)
+    x = np.concatenate([bits.view(np.float32), edge])
+    S = (len(x) + 3) // 4 * 4
+    lg = np.full((1, 1, S), -100.0, np.float32)
+    lg[0, 0, :len(x)] = x
+    n = len(x)
+    hm = np.zeros((1, 1), np.float32)
+    oF = oracle.norm(lg, hm, [n])
+    ogs = oracle.group(lg, hm, oF, [n], 1)
+    dev = torch.device("cuda")
+    lg_d, hm_d = torch.from_numpy(lg).to(dev), torch.from_numpy(hm).to(dev)
+    seq = torch.tensor([n], dtype=torch.int32, device=dev)
+    F = torch.zeros((1, 1), dtype=torch.int64, device=dev)
+    gs = torch.zeros((1, 1, S), dtype=torch.float32, device=dev)
+    ws = spc.alloc_workspace(spc.score_workspace(1, 1, S), dev)
+    q = torch.zeros((1, 1, 64), dtype=torch.bfloat16, device=dev)
+    kr = torch.zeros((1, 1, S, 64), dtype=torch.bfloat16, device=dev)
+    spc.score(q, kr, seq, 1, 1.0, lg_d, hm_d, F, gs, ws, phases=spc.SCORE_NORM | spc.SCORE_GROUP)
+    torch.cuda.synchronize()
+    assert np.array_equal(F.cpu().numpy(), oF)
+    assert np.array_equal(gs.cpu().numpy().view(np.uint32), ogs.view(np.uint32))
+
+
+def test_exp_sweep_through_fused_select(oracle):
+    """The same exp/fixed-point check through spc_select's register-cached NORM/GROUP."""
+    S = 131072
+    rng = np.random.default_rng(11)
+    x = -rng.random(S).astype(np.float32) * 88.0
+    x[:64] = np.array([0.0, -0.0, -87.0, -1e-45, -1e-38, -0.5, -86.999] + [-1.0] * 57, np.float32)
+    lg = x.reshape(1, 1, S).copy()
+    hm = np.zeros((1, 1), np.float32)
+    oF = oracle.norm(lg, hm, [S])
+    ogs = oracle.group(lg, hm, oF, [S], 1)
+    dev = torch.device("cuda")
+    z = lambda *s, dt=torch.int32: torch.zeros(s, dtype=dt, device=dev)  # noqa: E731
+    F, gs = z(1, 1, dt=torch.int64), z(1, 1, S, dt=torch.float32)
+    k = 2048
+    spc.select(torch.from_numpy(lg).to(dev), torch.from_numpy(hm).to(dev),
+               torch.tensor([S], dtype=torch.int32, device=dev), 1, k, F, gs, z(1, 1, k),
+               z(1, 1), torch.full((1, 1, k), -1, dtype=torch.int32, device=dev), z(1, 1),
+               z(1, 1, k), z(1, 1))
+    torch.cuda.synchronize()
+    assert np.array_equal(F.cpu().numpy(), oF)
+    assert np.array_equal(gs.cpu().numpy().view(np.uint32), ogs.view(np.uint32))

@@ -203,3 +203,131 @@ def test_gather_kv_bytes_exact(oracle):
                 for i in range(nl[r]):
                     assert torch.equal(kbc[l, b, g, ls[r, i]], kcc[l, b, g, lt[r, i]])
                     assert torch.equal(vbc[l, b, g, ls[r, i]], vcc[l, b, g, lt[r, i]])
+
+
+@pytest.mark.parametrize("alpha,G,S,k", [(4, 8, 32768, 2048), (2, 3, 5000, 700), (8, 1, 300, 512),
+                                         (1, 4, 20000, 64)])
+def test_fused_select_equals_separate_calls(oracle, alpha, G, S, k):
+    """spc_select (one launch) is bit-identical to spc_score(NORM|GROUP) + spc_topk +
+    spc_elastic_diff, and to the oracle, over two consecutive steps."""
+    B, D = 2, 128
+    Hq = alpha * G
+    kr = synth.retrieval_keys(B, G, S, D, seed=alpha + S, device=DEV)
+    qs = synth.retrieval_queries(2, B, Hq, G, D, seed=alpha + S, device=DEV)
+    seq = torch.tensor([S, max(1, S // 3)], dtype=torch.int32, device=DEV)
+    f32, i32 = torch.float32, torch.int32
+    mk = lambda *s, dt=f32: torch.zeros(s, dtype=dt, device=DEV)
+    ws = spc.alloc_workspace(spc.score_workspace(B, Hq, S), DEV)
+    wt = spc.alloc_workspace(spc.topk_workspace(B, G, S, k), DEV)
+    prev_a, prevc_a = torch.full((B, G, k), -1, dtype=i32, device=DEV), mk(B, G, dt=i32)
+    prev_b, prevc_b = prev_a.clone(), prevc_a.clone()
+    for step in range(2):
+        lg, hm = mk(B, Hq, S), mk(B, Hq)
+        spc.score(qs[step], kr, seq, G, 0.088, lg, hm, mk(B, Hq, dt=torch.int64), mk(B, G, S), ws,
+                  phases=spc.SCORE_LOGITS)
+        # separate calls
+        Fa, gsa = mk(B, Hq, dt=torch.int64), mk(B, G, S)
+        spc.score(qs[step], kr, seq, G, 0.088, lg, hm, Fa, gsa, ws,
+                  phases=spc.SCORE_NORM | spc.SCORE_GROUP)
+        ia, ca = mk(B, G, k, dt=i32), mk(B, G, dt=i32)
+        spc.topk(gsa, seq, k, ia, ca, wt, force_last=True)
+        lta, nla, eta, nea = mk(B, G, k, dt=i32), mk(B, G, dt=i32), mk(B, G, k, dt=i32), mk(B, G, dt=i32)
+        spc.elastic_diff(prev_a, prevc_a, ia, ca, lta, nla, evict_tok=eta, n_evict=nea)
+        # fused
+        Fb, gsb = mk(B, Hq, dt=torch.int64), mk(B, G, S) - 1
+        ib, cb = mk(B, G, k, dt=i32), mk(B, G, dt=i32)
+        ltb, nlb, etb, neb = mk(B, G, k, dt=i32), mk(B, G, dt=i32), mk(B, G, k, dt=i32), mk(B, G, dt=i32)
+        spc.select(lg, hm, seq, G, k, Fb, gsb, ib, cb, prev_b, prevc_b, ltb, nlb, etb, neb,
+                   force_last=True)
+        torch.cuda.synchronize()
+        for x, y in ((Fa, Fb), (ia, ib), (ca, cb), (lta, ltb), (nla, nlb), (eta, etb), (nea, neb)):
+            assert torch.equal(x, y)
+        assert torch.equal(gsa.view(torch.int32), gsb.view(torch.int32))
+        oidx, _, ocnt, _ = oracle.topk(gsa.cpu().numpy(), seq.cpu().tolist(), k, force_last=True)
+        assert np.array_equal(ib.cpu().numpy(), oidx)
+        prev_a, prevc_a, prev_b, prevc_b = ia, ca, ib, cb
+
+
+def _select_both(lg, hm, seq, G, k, prev=None, force=True):
+    """Run the separate calls and spc_select on the same logits; assert bit-identity."""
+    B, Hq, S = lg.shape
+    f32, i32 = torch.float32, torch.int32
+    mk = lambda *s, dt=f32: torch.zeros(s, dtype=dt, device=DEV)  # noqa: E731
+    if prev is None:
+        prev = (torch.full((B, G, k), -1, dtype=i32, device=DEV), mk(B, G, dt=i32))
+    ws = spc.alloc_workspace(spc.score_workspace(B, Hq, S), DEV)
+    wt = spc.alloc_workspace(spc.topk_workspace(B, G, S, k), DEV)
+    q = torch.zeros((B, Hq, 64), dtype=torch.bfloat16, device=DEV)
+    kr = torch.zeros((B, G, S, 64), dtype=torch.bfloat16, device=DEV)
+    Fa, gsa = mk(B, Hq, dt=torch.int64), mk(B, G, S)
+    spc.score(q, kr, seq, G, 1.0, lg, hm, Fa, gsa, ws, phases=spc.SCORE_NORM | spc.SCORE_GROUP)
+    ia, ca = mk(B, G, k, dt=i32), mk(B, G, dt=i32)
+    spc.topk(gsa, seq, k, ia, ca, wt, force_last=force)
+    outs_a = [mk(B, G, k, dt=i32), mk(B, G, dt=i32), mk(B, G, k, dt=i32), mk(B, G, dt=i32)]
+    spc.elastic_diff(prev[0], prev[1], ia, ca, outs_a[0], outs_a[1], evict_tok=outs_a[2],
+                     n_evict=outs_a[3])
+    Fb, gsb = mk(B, Hq, dt=torch.int64) - 7, mk(B, G, S) - 1
+    ib, cb = mk(B, G, k, dt=i32) - 5, mk(B, G, dt=i32)
+    outs_b = [mk(B, G, k, dt=i32) - 3, mk(B, G, dt=i32), mk(B, G, k, dt=i32) - 3, mk(B, G, dt=i32)]
+    spc.select(lg, hm, seq, G, k, Fb, gsb, ib, cb, prev[0], prev[1], outs_b[0], outs_b[1],
+               outs_b[2], outs_b[3], force_last=force)
+    torch.cuda.synchronize()
+    assert torch.equal(Fa, Fb)
+    assert torch.equal(gsa.view(torch.int32), gsb.view(torch.int32))
+    assert torch.equal(ia, ib) and torch.equal(ca, cb)
+    for x, y in zip(outs_a, outs_b):
+        assert torch.equal(x, y)
+    return gsa, ia, ca
+
+
+def _logits_case(kind, B, Hq, S, seed):
+    g = torch.Generator(device="cpu").manual_seed(seed)
+    if kind == "flat":            # every score equal: clamped top bin, ties broken by id bits
+        lg = torch.zeros((B, Hq, S))
+    elif kind == "two_level":     # a few spikes over a flat floor: tiny threshold buckets
+        lg = torch.zeros((B, Hq, S))
+        lg[:, :, torch.randperm(S, generator=g)[:S // 50]] = 3.0
+    elif kind == "quantised":     # 17 distinct logits: large exact-tie buckets
+        lg = torch.randint(0, 17, (B, Hq, S), generator=g).float() * 0.25
+    elif kind == "wide":          # scores spanning > 32 binades below the max (bottom clamp)
+        lg = -torch.rand((B, Hq, S), generator=g) * 80.0
+        lg[:, :, 0] = 0.0
+    else:                         # smooth random
+        lg = torch.randn((B, Hq, S), generator=g) * 2.0
+    return lg.to(DEV)
+
+
+@pytest.mark.parametrize("kind", ["flat", "two_level", "quantised", "wide", "randn"])
+@pytest.mark.parametrize("alpha,G,S,k,lens", [(4, 2, 8192, 1024, [8192, 3001]),
+                                              (2, 1, 1000, 1000, [999]),
+                                              (1, 3, 40000, 2048, [40000, 1]),
+                                              (8, 1, 4096, 300, [0])])
+def test_fused_select_adversarial(oracle, kind, alpha, G, S, k, lens):
+    B, Hq = len(lens), alpha * G
+    lg = _logits_case(kind, B, Hq, S, seed=S + alpha)
+    seq = torch.tensor(lens, dtype=torch.int32, device=DEV)
+    hm = torch.zeros((B, Hq), device=DEV)
+    for b, n in enumerate(lens):
+        if n > 0:
+            hm[b] = lg[b, :, :n].max(-1).values
+    gs, idx, cnt = _select_both(lg, hm, seq, G, k)
+    oidx, _, ocnt, _ = oracle.topk(gs.cpu().numpy(), lens, k, force_last=True)
+    assert np.array_equal(idx.cpu().numpy(), oidx) and np.array_equal(cnt.cpu().numpy(), ocnt)
+    # a second step against this selection (elastic diff with a non-empty previous list)
+    lg2 = lg + 0.01 * _logits_case("randn", B, Hq, S, seed=S + 1)
+    hm2 = torch.zeros((B, Hq), device=DEV)
+    for b, n in enumerate(lens):
+        if n > 0:
+            hm2[b] = lg2[b, :, :n].max(-1).values
+    _select_both(lg2, hm2, seq, G, k, prev=(idx, cnt))
+
+
+def test_fused_select_rejects_unsupported():
+    B, G, Hq, k = 1, 1, 4, 64
+    for S in (131076, 1001):  # beyond 8 * 16384 tokens; not a multiple of 4
+        lg = torch.zeros((B, Hq, S), device=DEV)
+        z = lambda *s, dt=torch.int32: torch.zeros(s, dtype=dt, device=DEV)  # noqa: E731
+        with pytest.raises(spc.SpcError):
+            spc.select(lg, z(B, Hq, dt=torch.float32), torch.tensor([S], dtype=torch.int32,
+                       device=DEV), G, k, z(B, Hq, dt=torch.int64), z(B, G, S, dt=torch.float32),
+                       z(B, G, k), z(B, G), z(B, G, k), z(B, G), z(B, G, k), z(B, G))

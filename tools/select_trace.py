@@ -1,0 +1,51 @@
+"""Phase timeline of spc_select (config B, row 0) from a -DSPC_TRACE build.  Not a bench."""
+import ctypes
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+from paper_2512_00722_b200 import build, spc, synth  # noqa: E402
+
+out = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libspc_trace.so")
+if not os.path.exists(out):
+    build.build(out=out, defines=["SPC_TRACE"])
+spc._lib = spc.load_library(out)
+lib = spc._lib
+lib.spc_debug_set_select_trace.argtypes = [ctypes.c_void_p]
+cfg = sys.argv[1] if len(sys.argv) > 1 else "B"
+c = synth.CONFIGS[cfg]
+B, G, Hq, D, S, k = c["B"], c["G"], c["Hq"], c["D"], c["S"], c["k"]
+dev = torch.device("cuda")
+kr = synth.retrieval_keys(B, G, S, D, seed=1, device=dev)
+qs = synth.retrieval_queries(4, B, Hq, G, D, seed=1, device=dev)
+seq = torch.full((B,), S, dtype=torch.int32, device=dev)
+f32, i32 = torch.float32, torch.int32
+z = lambda *s, dt=f32: torch.zeros(s, dtype=dt, device=dev)  # noqa: E731
+lg, hm, F, gs = z(B, Hq, S), z(B, Hq), z(B, Hq, dt=torch.int64), z(B, G, S)
+ws = spc.alloc_workspace(spc.score_workspace(B, Hq, S), dev)
+idx = [z(B, G, k, dt=i32) for _ in range(2)]
+cnt = [z(B, G, dt=i32) for _ in range(2)]
+lt, nl = z(B, G, k, dt=i32), z(B, G, dt=i32)
+tr = torch.zeros(8 * 16, dtype=torch.int64, device=dev)
+names = ["start", "norm", "group", "pass0", "passes", "T", "counts", "end", "x_comp", "x_sync",
+         "bitmap", "exp", "push"]
+for step in range(4):
+    spc.score(qs[step], kr, seq, G, 0.088, lg, hm, F, gs, ws, phases=spc.SCORE_LOGITS)
+    torch.cuda.synchronize()
+    tr.zero_()
+    lib.spc_debug_set_select_trace(ctypes.c_void_p(tr.data_ptr()) if step == 3 else None)
+    e = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    e[0].record()
+    spc.select(lg, hm, seq, G, k, F, gs, idx[step % 2], cnt[step % 2], idx[1 - step % 2],
+               cnt[1 - step % 2], lt, nl, force_last=True)
+    e[1].record()
+    torch.cuda.synchronize()
+    print(f"step {step}: {e[0].elapsed_time(e[1]) * 1e3:.1f} us")
+t = tr.view(8, 16).cpu().numpy().astype("float64")
+t0 = t[:, 0][t[:, 0] > 0].min()
+print("rank " + " ".join(f"{n:>8s}" for n in names))
+for r in range(8):
+    print(f"{r:4d} " + " ".join(f"{(t[r, i] - t0) / 1e3:8.2f}" if t[r, i] > 0 else "       -"
+                                for i in range(len(names))))
