@@ -38,7 +38,9 @@ struct AttnWs {
   size_t bytes;
 };
 AttnWs attn_ws_layout(void* ws, int L, int B, int Hq, int D, int k) {
-  const size_t ns = (k + 63) / 64 + 2;  // >= both the split count and the persistent segments
+  // >= the split count of the fp32 path and (CTA segments of a group) x 4 warps of the
+  // persistent bf16 path
+  const size_t ns = 4 * ((k + 63) / 64 + 2);
   uint8_t* p = (uint8_t*)ws;
   AttnWs w;
   size_t off = 0;
@@ -69,16 +71,6 @@ __device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t&
                : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
                : "r"(addr));
 }
-// D = A(16x16 bf16, row) * B(16x8 bf16, col) + D, fp32 accumulate; a1 = a3 = 0.
-__device__ __forceinline__ void mma_bf16(float (&c)[4], uint32_t a0, uint32_t a2, uint32_t b0,
-                                         uint32_t b1) {
-  asm volatile(
-      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, "
-      "{%8, %9}, {%0, %1, %2, %3};"
-      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
-      : "r"(a0), "r"(0u), "r"(a2), "r"(0u), "r"(b0), "r"(b1));
-}
-
 // Merge the nsplit partials of one (layer, b, g) with the LSE rule (O12); run by
 // the last CTA of the group.  m is in log2 units.
 template <int D, int ALPHA>
@@ -108,6 +100,58 @@ __device__ void merge_partials(const float* part_o, const float* part_ml, int ns
 
 #include "attn_bf16.cuh"
 
+// One CTA per (layer, b, g): merges the per-warp partials the bf16 kernel wrote for the
+// group's CTA segments (O12) into out / lse.  The (m, l) of every partial are staged in
+// shared memory and turned into weights w_p = exp2(m_p - M) once per head; each thread
+// then forms one output element from independent (unrolled) loads of the o partials.
+constexpr int MG_MAXP = 4 * (SPC_MAX_K / 64 + 2);
+template <int D, int ALPHA>
+__global__ void __launch_bounds__(ALPHA * D) merge_groups_kernel(
+    const float* __restrict__ part_o, const float* __restrict__ part_ml, int B, int G, int kpad,
+    int cpc, int segstride, int layer_begin, float* __restrict__ out, float* __restrict__ lse) {
+  spc_pdl_entry();
+  __shared__ float w[ALPHA][MG_MAXP];
+  __shared__ float inv_den[ALPHA];
+  const int grp = blockIdx.x, BG = B * G, Hq = G * ALPHA;
+  const int lr = grp / BG, bg = grp - lr * BG, b = bg / G, g = bg - b * G;
+  const int cpg = kpad / CH;
+  const int first = (grp * cpg) / cpc, last = (grp * cpg + cpg - 1) / cpc;
+  const int np = min((last - first + 1) * NWARP, segstride);
+  const size_t head_base = ((size_t)lr * B + b) * Hq + g * ALPHA;
+  const size_t out_base = ((size_t)(layer_begin + lr) * B + b) * Hq + g * ALPHA;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (warp < ALPHA) {  // warp j: weights and normaliser of head j
+    const float* ml = part_ml + (head_base + warp) * segstride * 2;
+    float M = -INFINITY;
+    for (int p = lane; p < np; p += 32) M = fmaxf(M, __ldcg(ml + 2 * p));
+    M = warp_max(M);
+    float den = 0.f;
+    for (int p = lane; p < np; p += 32) {
+      const float m = __ldcg(ml + 2 * p);
+      const float wp = m == -INFINITY ? 0.f : exp2f(m - M);
+      w[warp][p] = wp;
+      den += wp * __ldcg(ml + 2 * p + 1);
+    }
+    den = warp_sum(den);
+    if (lane == 0) {
+      inv_den[warp] = den > 0.f ? 1.f / den : 0.f;
+      if (lse) lse[out_base + warp] = den > 0.f ? (M + log2f(den)) * LN2 : -INFINITY;
+    }
+  }
+  __syncthreads();
+  const int j = tid / D, d = tid - (tid / D) * D;
+  const float* po = part_o + (head_base + j) * segstride * D + d;
+  float num = 0.f;
+  int p = 0;
+  for (; p + 4 <= np; p += 4) {
+    const float o0 = __ldcg(po + (size_t)p * D), o1 = __ldcg(po + (size_t)(p + 1) * D);
+    const float o2 = __ldcg(po + (size_t)(p + 2) * D), o3 = __ldcg(po + (size_t)(p + 3) * D);
+    num += w[j][p] * o0 + w[j][p + 1] * o1 + w[j][p + 2] * o2 + w[j][p + 3] * o3;
+  }
+  for (; p < np; ++p) num += w[j][p] * __ldcg(po + (size_t)p * D);
+  out[(out_base + j) * D + d] = num * inv_den[j];
+}
+
 // ---------------------------------------------------------------- fp32 / CUDA-core path
 template <int D, int ALPHA>
 __global__ void __launch_bounds__(AT_THREADS) attn_f32_kernel(
@@ -117,6 +161,7 @@ __global__ void __launch_bounds__(AT_THREADS) attn_f32_kernel(
     float scale, int nsplit, int segstride, float* __restrict__ part_o,
     float* __restrict__ part_ml, unsigned* __restrict__ cnt, float* __restrict__ out,
     float* __restrict__ lse) {
+  spc_pdl_entry();
   __shared__ float qs[ALPHA][D];
   __shared__ float ps[ALPHA][AT_ROWS];
   __shared__ int toks[AT_ROWS];
@@ -199,6 +244,7 @@ __global__ void __launch_bounds__(AT_THREADS) attn_f32_kernel(
 __global__ void merge_kernel(const float* __restrict__ o_parts, const float* __restrict__ lse_parts,
                              int P, int n, int D, float* __restrict__ out,
                              float* __restrict__ lse_out) {
+  spc_pdl_entry();
   const int row = blockIdx.x;
   float M = -INFINITY;
   for (int p = 0; p < P; ++p) M = fmaxf(M, lse_parts[(size_t)p * n + row]);
@@ -252,10 +298,10 @@ extern "C" int spc_sparse_decode_attn(int dtype, const void* q, const void* cons
   const int nsplit = (k + AT_ROWS - 1) / AT_ROWS;
   const int n_groups = (layer_end - layer_begin) * B * G;
   cudaStream_t st = as_stream(stream);
-  // persistent bf16 path: 2 CTAs per SM, contiguous chunk-aligned row ranges
+  // persistent bf16 path: AT2_CTAS_PER_SM CTAs per SM, contiguous chunk-aligned row ranges
   const int kpad = (k + CH - 1) / CH * CH;  // groups padded to whole chunks
   const long long v_total = (long long)n_groups * kpad;
-  const int ncta_target = 2 * num_sms();
+  const int ncta_target = AT2_CTAS_PER_SM * num_sms();
   long long rpc = (v_total + ncta_target - 1) / ncta_target;
   rpc = (rpc + CH - 1) / CH * CH;
   const int ncta = (int)((v_total + rpc - 1) / rpc);
@@ -269,14 +315,17 @@ extern "C" int spc_sparse_decode_attn(int dtype, const void* q, const void* cons
                              cudaFuncAttributeMaxDynamicSharedMemorySize, smem);                \
         attr = true;                                                                            \
       }                                                                                         \
-      attn_bf16_kernel<DD, AA><<<ncta, AT2_THREADS, smem, st>>>(                                \
+      (void)launch_k(attn_bf16_kernel<DD, AA>, dim3(ncta), dim3(AT2_THREADS), smem, st,      \
           (const uint16_t*)q, k_layers, v_layers, kv_mode, idx, count, layer_begin, B, G, rows, \
           k, kpad, scale, (int)(rpc / CH), n_groups, w.segstride, w.part_o, w.part_ml, w.cnt,   \
-          out,                                                                                  \
-          lse);                                                                                 \
+          out, lse);                                                                            \
+      SPC_TRY(launched());                                                                      \
+      (void)launch_k(merge_groups_kernel<DD, AA>, dim3(n_groups), dim3(AA * DD), 0, st,         \
+          (const float*)w.part_o, (const float*)w.part_ml, B, G, kpad, (int)(rpc / CH),         \
+          w.segstride, layer_begin, out, lse);                                                  \
     } else {                                                                                    \
       dim3 grid(nsplit, B * G, layer_end - layer_begin);                                        \
-      attn_f32_kernel<DD, AA><<<grid, AT_THREADS, 0, st>>>(                                     \
+      (void)launch_k(attn_f32_kernel<DD, AA>, dim3(grid), dim3(AT_THREADS), 0, st,                                      \
           (const float*)q, k_layers, v_layers, kv_mode, idx, count, layer_begin, B, G, rows, k, \
           scale, nsplit, w.segstride, w.part_o, w.part_ml, w.cnt, out, lse);                    \
     }                                                                                           \
@@ -291,7 +340,7 @@ extern "C" int spc_attn_merge(const float* o_parts, const float* lse_parts, int 
                               float* out, float* lse_out, spc_stream_t stream) {
   if (!o_parts || !lse_parts || !out) return SPC_E_NULL;
   if (P < 1 || n < 1 || D < 1) return SPC_E_SHAPE;
-  merge_kernel<<<n, 128, 0, as_stream(stream)>>>(o_parts, lse_parts, P, n, D, out, lse_out);
+  (void)launch_k(merge_kernel, dim3(n), dim3(128), 0, as_stream(stream), o_parts, lse_parts, P, n, D, out, lse_out);
   return launched();
 }
 

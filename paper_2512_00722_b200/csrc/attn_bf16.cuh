@@ -16,20 +16,37 @@
 // tops out near 1.8 TB/s (per-request cost of the TMA unit); a single producer
 // warp issuing the 16-byte copies is issue-bound (~3.3 TB/s).
 //
-// Math per warp and chunk (mma.sync m16n8k16, fp32 accumulate):
-//   S = Q K^T   A = Q (rows 0-7 = heads, alpha real), B = K rows (ldmatrix)
-//   O += P V    A = [P_hi ; P_lo] (rows 0-7 = bf16(P), rows 8-15 = bf16(P - P_hi)),
-//               so one mma accumulates both halves of a ~16-bit-mantissa P;
-//               O = O_hi + O_lo at the end.  B = V rows (ldmatrix.trans).
-// Online softmax in registers; the O rescale is skipped when no head's running
-// max moved.  At the end of a group segment the 4 warps merge (the only CTA
-// barriers) and write one (m, l, o) partial; the last CTA of a group merges the
-// group's segments with the LSE rule (O12).
+// Math per warp and chunk (mma.sync m16n8k16, fp32 accumulate), both products
+// transposed so the 16 K/V rows fill the M dimension:
+//   S^T = K Q^T   A = the chunk's 16 K rows (ldmatrix), B = Q^T (n = head; heads
+//                 >= alpha are zero).  8 HMMA per chunk for D = 128.
+//   O^T += V^T P  A = V^T (ldmatrix.trans of the V rows, one m-tile per 16 dims),
+//                 B = P (k = row, n = column): columns n < alpha hold bf16(P) of head
+//                 n, columns alpha <= n < 2 alpha hold bf16(P - bf16(P)) (the lo part),
+//                 so one MMA accumulates both halves of a ~16-bit-mantissa P; alpha = 8
+//                 fills all 8 columns with hi parts and runs the lo parts as a second
+//                 MMA.  The S^T accumulator fragment is moved into the B-fragment
+//                 layout with two movmatrix.trans.  O = O_hi + O_lo at the flush.
+// Online softmax in registers (each lane tracks the two heads of its columns); the
+// O rescale is skipped when no head's running max moved.  At the end of a group
+// segment every warp writes its own (m, l, o) partial with plain stores -- no CTA
+// barrier, fence or ticket inside the kernel, so no warp's load stream ever waits
+// for another (a CTA-wide flush measured ~5-8 us of stalled loads per group end) --
+// and merge_groups_kernel (next launch, PDL) merges each group's partials with the
+// LSE rule (O12).
 #pragma once
 
 constexpr int CH = 64;      // rows per chunk (4 warps x 16)
 constexpr int WR = 16;      // rows per warp per chunk
-constexpr int NSTAGE = 3;   // per-warp ring depth (chunks in flight: NSTAGE - 1)
+#ifndef SPC_ATTN_NSTAGE
+#define SPC_ATTN_NSTAGE 3
+#endif
+#ifndef SPC_ATTN_CTAS
+#define SPC_ATTN_CTAS 2
+#endif
+constexpr int NSTAGE = SPC_ATTN_NSTAGE;  // per-warp ring depth (chunks in flight: NSTAGE - 1)
+// 8 warps/SM.  (3 CTAs x 2 stages measured slower: 70 vs 62 us for config B.)
+constexpr int AT2_CTAS_PER_SM = SPC_ATTN_CTAS;
 constexpr int NWARP = 4;
 constexpr int AT2_THREADS = NWARP * 32;
 constexpr int TRING = 8;    // per-warp ring of prefetched chunk metadata
@@ -63,6 +80,11 @@ template <int N>
 __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
+__device__ __forceinline__ uint32_t movm_t(uint32_t a) {
+  uint32_t d;
+  asm volatile("movmatrix.sync.aligned.m8n8.trans.b16 %0, %1;" : "=r"(d) : "r"(a));
+  return d;
+}
 // D = A(16x16 bf16, row) * B(16x8 bf16, col) + D with all four A registers.
 __device__ __forceinline__ void mma_bf16_4(float (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2,
                                            uint32_t a3, uint32_t b0, uint32_t b1) {
@@ -76,10 +98,11 @@ __device__ __forceinline__ void mma_bf16_4(float (&c)[4], uint32_t a0, uint32_t 
 // Debug trace (spc_debug_set_trace; compiled in with -DSPC_TRACE): CTA 0 warp 0
 // stamps %globaltimer per chunk: [i][0] rows of chunk i+2 issued, [i][1] chunk i
 // landed, [i][2] chunk i computed.
+// Also: lane 0 of every warp stamps its start / end at g_trace[1024 + (cta * 4 + warp) * 2].
 __device__ unsigned long long* g_trace = nullptr;
 __device__ __forceinline__ void trace(int i, int slot) {
 #ifdef SPC_TRACE
-  if (g_trace && blockIdx.x == 0 && threadIdx.x == 0 && i < 256) {
+  if (g_trace && blockIdx.x == 105 && threadIdx.x == 0 && i < 256) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
     g_trace[i * 4 + slot] = t;
@@ -87,6 +110,17 @@ __device__ __forceinline__ void trace(int i, int slot) {
 #else
   (void)i;
   (void)slot;
+#endif
+}
+__device__ __forceinline__ void trace_warp(int which) {
+#ifdef SPC_TRACE
+  if (g_trace && (threadIdx.x & 31) == 0 && blockIdx.x < 1024) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    g_trace[1024 + (blockIdx.x * 4 + (threadIdx.x >> 5)) * 2 + which] = t;
+  }
+#else
+  (void)which;
 #endif
 }
 
@@ -107,13 +141,14 @@ struct ChunkIt {
 };
 
 template <int D, int ALPHA>
-__global__ void __launch_bounds__(AT2_THREADS, 2) attn_bf16_kernel(
+__global__ void __launch_bounds__(AT2_THREADS, AT2_CTAS_PER_SM) attn_bf16_kernel(
     const uint16_t* __restrict__ q, const void* const* __restrict__ k_layers,
     const void* const* __restrict__ v_layers, int kv_mode, const int32_t* __restrict__ idx,
     const int32_t* __restrict__ count, int layer_begin, int B, int G, int rows, int kbud, int kpad,
     float scale, int cpc, int n_groups, int segstride, float* __restrict__ part_o,
     float* __restrict__ part_ml, unsigned* __restrict__ cnt, float* __restrict__ out,
     float* __restrict__ lse) {
+  spc_pdl_entry();
   using SM = PSmem<D, ALPHA>;
   constexpr int RS = SM::RS;
   constexpr int KS = D / 16;
@@ -121,7 +156,6 @@ __global__ void __launch_bounds__(AT2_THREADS, 2) attn_bf16_kernel(
   constexpr int NG = 32 / VPR;     // lane groups (rows per warp-wide copy instruction)
   constexpr int RPL = WR / NG;     // rows per lane group per chunk
   extern __shared__ __align__(128) uint8_t at_smem[];
-  __shared__ int flag;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int gid = lane >> 2, tig = lane & 3;
   const int BG = B * G, Hq = G * ALPHA;
@@ -129,6 +163,7 @@ __global__ void __launch_bounds__(AT2_THREADS, 2) attn_bf16_kernel(
   const int c_begin = blockIdx.x * cpc;  // first (global) chunk of this CTA
   const int n_chunks = min(cpc, n_groups * cpg - c_begin);
   if (n_chunks <= 0) return;
+  trace_warp(0);
   ChunkIt it0;
   it0.grp = c_begin / cpg;
   it0.rc = c_begin - it0.grp * cpg;
@@ -208,7 +243,8 @@ __global__ void __launch_bounds__(AT2_THREADS, 2) attn_bf16_kernel(
       }
     }
   };
-  // query fragments (A operand, row = head gid) of group grp
+  // query fragments: the B operand of S^T = K Q^T (k = dim, n = head gid; heads >= ALPHA
+  // are zero): b0 = Q[gid][16k + 2tig ..], b1 = Q[gid][16k + 8 + 2tig ..]
   uint32_t qa0[KS], qa2[KS], qn0[KS], qn2[KS];
   auto load_q = [&](int lr, int bg, uint32_t (&a0)[KS], uint32_t (&a2)[KS]) {
     const int b = bg / G, g = bg - (bg / G) * G;
@@ -223,24 +259,38 @@ __global__ void __launch_bounds__(AT2_THREADS, 2) attn_bf16_kernel(
     }
   };
 
-  // ---- prologue: metadata of chunks 0 .. MAHEAD+1, rows of chunks 0 and 1
+  // ---- prologue: metadata of chunks 0 .. MAHEAD+NSTAGE-2, rows of chunks 0 .. NSTAGE-2
   for (int j = 0; j < MAHEAD; ++j) fetch_meta(j);
   cp_async_commit();
   cp_async_wait<0>();
   __syncwarp();
-  issue_rows(0);
-  fetch_meta(MAHEAD);
-  cp_async_commit();
-  issue_rows(1);
-  fetch_meta(MAHEAD + 1);
-  cp_async_commit();
+#pragma unroll
+  for (int j = 0; j < NSTAGE - 1; ++j) {
+    issue_rows(j);
+    fetch_meta(MAHEAD + j);
+    cp_async_commit();
+  }
   load_q(it0.lr, it0.bg, qa0, qa2);
 
-  const float sl2 = scale * LOG2E;
-  float m_run = -INFINITY, l_run = 0.f;
-  float o[D / 8][4];  // [n-tile][c0..c3]: c0,c1 = hi half (heads), c2,c3 = lo half
+  // P columns n = 2 tig + slot of this lane: mode 0 = hi part of head hd[slot], 1 = lo
+  // part, 2 = zero column.  The S^T values of head h sit in lane (gid, h / 2), slot h % 2.
+  constexpr bool LOSEP = ALPHA == 8;
+  constexpr int NACC = LOSEP ? 2 : 1;
+  const int srcl = LOSEP ? lane : ((lane & ~3) | (ALPHA == 4 ? (tig & 1) : 0));
+  int cmode[2], hd[2];
 #pragma unroll
-  for (int i = 0; i < D / 8; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+  for (int sl = 0; sl < 2; ++sl) {
+    const int n = 2 * tig + sl;
+    cmode[sl] = LOSEP ? 0 : (n < ALPHA ? 0 : (n < 2 * ALPHA ? 1 : 2));
+    hd[sl] = LOSEP ? n : n % ALPHA;
+  }
+  const float sl2 = scale * LOG2E;
+  float m_run[2] = {-INFINITY, -INFINITY}, l_run[2] = {0.f, 0.f};
+  float o[NACC][D / 16][4];  // O^T[16 mt + gid (+8)][column 2 tig (+1)]
+#pragma unroll
+  for (int a = 0; a < NACC; ++a)
+#pragma unroll
+    for (int i = 0; i < D / 16; ++i) o[a][i][0] = o[a][i][1] = o[a][i][2] = o[a][i][3] = 0.f;
   const int mi = lane >> 3, ri = lane & 7;
   const uint32_t a_off = (uint32_t)(((ri + ((mi & 2) ? 8 : 0)) * RS + ((mi & 1) ? 8 : 0)) * 2);
   const uint32_t b_off = (uint32_t)(((ri + ((mi & 1) ? 8 : 0)) * RS + ((mi & 2) ? 8 : 0)) * 2);
@@ -248,141 +298,142 @@ __global__ void __launch_bounds__(AT2_THREADS, 2) attn_bf16_kernel(
   int s_cur = 0;
 
   for (int i = 0; i < n_chunks; ++i) {
-    // commit group G_i = {rows of chunk i+2, meta of chunk i+2+MAHEAD};
-    // the meta of chunk i+2 is in G_{i-MAHEAD} (or the prologue)
-    cp_async_wait<2>();
+    // commit group G_i = {rows of chunk i+NSTAGE-1, meta of chunk i+NSTAGE-1+MAHEAD};
+    // the meta of chunk i+NSTAGE-1 is in G_{i-MAHEAD} (or the prologue)
+    cp_async_wait<NSTAGE - 1>();
     __syncwarp();
-    issue_rows(i + 2);
-    fetch_meta(i + 2 + MAHEAD);
+    issue_rows(i + NSTAGE - 1);
+    fetch_meta(i + NSTAGE - 1 + MAHEAD);
     cp_async_commit();
     trace(i, 0);
     const ChunkIt cc = it_cur;
     const bool grp_end = (i == n_chunks - 1) || (cc.rc == cpg - 1);
     it_cur.next(cpg, BG);
     if (grp_end && i + 1 < n_chunks) load_q(it_cur.lr, it_cur.bg, qn0, qn2);  // next group, early
-    cp_async_wait<2>();  // rows of chunk i (G_{i-2}) landed
+    cp_async_wait<NSTAGE - 1>();  // rows of chunk i landed
     __syncwarp();
     trace(i, 1);
+#ifdef SPC_ATTN_NOMATH  // debug builds only: time the load pipeline alone
+    const int nv_w = 0;
+#else
     const int nv_w = nv_ring[s_cur] - warp * WR;  // valid rows of this warp in the chunk
+#endif
     const uint32_t st = wsb + (uint32_t)s_cur * SM::STAGE;
     if (nv_w > 0) {
-      // ---- S = Q K^T for this warp's 16 rows: two n8 tiles, two accumulator chains each
-      float c0[4] = {0, 0, 0, 0}, c1[4] = {0, 0, 0, 0}, d0[4] = {0, 0, 0, 0},
-            d1[4] = {0, 0, 0, 0};
+      // ---- S^T = K Q^T for this warp's 16 rows: two accumulator chains
+      float ce[4] = {0, 0, 0, 0}, co[4] = {0, 0, 0, 0};
 #pragma unroll
-      for (int k = 0; k < KS; k += 2) {
-        uint32_t b0, b1, b2, b3, e0, e1, e2, e3;
-        ldsm_x4(st + a_off + k * 32, b0, b1, b2, b3);
-        ldsm_x4(st + a_off + (k + 1) * 32, e0, e1, e2, e3);
-        mma_bf16(c0, qa0[k], qa2[k], b0, b1);
-        mma_bf16(c1, qa0[k], qa2[k], b2, b3);
-        mma_bf16(d0, qa0[k + 1], qa2[k + 1], e0, e1);
-        mma_bf16(d1, qa0[k + 1], qa2[k + 1], e2, e3);
+      for (int kk = 0; kk < KS; kk += 2) {
+        uint32_t a0, a1, a2, a3, e0, e1, e2, e3;
+        ldsm_x4(st + b_off + kk * 32, a0, a1, a2, a3);
+        ldsm_x4(st + b_off + (kk + 1) * 32, e0, e1, e2, e3);
+        mma_bf16_4(ce, a0, a1, a2, a3, qa0[kk], qa2[kk]);
+        mma_bf16_4(co, e0, e1, e2, e3, qa0[kk + 1], qa2[kk + 1]);
       }
-      const int rr0 = 2 * tig;
-      float sv[4] = {rr0 < nv_w ? (c0[0] + d0[0]) * sl2 : -INFINITY,
-                     rr0 + 1 < nv_w ? (c0[1] + d0[1]) * sl2 : -INFINITY,
-                     rr0 + 8 < nv_w ? (c1[0] + d1[0]) * sl2 : -INFINITY,
-                     rr0 + 9 < nv_w ? (c1[1] + d1[1]) * sl2 : -INFINITY};
-      float mx = fmaxf(fmaxf(sv[0], sv[1]), fmaxf(sv[2], sv[3]));
-      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
-      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
-      const float m_new = fmaxf(m_run, mx);  // finite: row 0 of this warp is valid
-      if (__any_sync(0xffffffffu, m_new > m_run)) {
-        const float corr = exp2f(m_run - m_new);
-        l_run *= corr;
-#pragma unroll
-        for (int d = 0; d < D / 8; ++d) {
-          o[d][0] *= corr;
-          o[d][1] *= corr;
-          o[d][2] *= corr;
-          o[d][3] *= corr;
-        }
-        m_run = m_new;
-      }
-      float p[4];
+      // values of this lane's columns: [row gid: slot 0, slot 1; row gid + 8: slot 0, slot 1]
+      const float raw[4] = {ce[0] + co[0], ce[1] + co[1], ce[2] + co[2], ce[3] + co[3]};
+      float sv[4];
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
-        p[e] = exp2f(sv[e] - m_run);
-        l_run += p[e];
+        const int from = ALPHA == 1 ? (e & 2) : e;  // alpha = 1: both columns are head 0
+        const float x = LOSEP ? raw[e] : __shfl_sync(0xffffffffu, raw[from], srcl);
+        sv[e] = (e < 2 ? gid : gid + 8) < nv_w ? x * sl2 : -INFINITY;
       }
-      // ---- O += P V with A = [P_hi ; P_lo]
-      const uint32_t ah0 = pack_bf16(p[0], p[1]), ah2 = pack_bf16(p[2], p[3]);
-      const float2 h0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&ah0));
-      const float2 h2 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&ah2));
-      const uint32_t al0 = pack_bf16(p[0] - h0.x, p[1] - h0.y);
-      const uint32_t al2 = pack_bf16(p[2] - h2.x, p[3] - h2.y);
-      const uint32_t vst = st + SM::KV_BYTES + b_off;
+      float mx0 = fmaxf(sv[0], sv[2]), mx1 = fmaxf(sv[1], sv[3]);
 #pragma unroll
-      for (int dn = 0; dn < D / 16; ++dn) {
-        uint32_t b0, b1, b2, b3;
-        ldsm_x4_t(vst + dn * 32, b0, b1, b2, b3);
-        mma_bf16_4(o[2 * dn], ah0, al0, ah2, al2, b0, b1);
-        mma_bf16_4(o[2 * dn + 1], ah0, al0, ah2, al2, b2, b3);
+      for (int sh = 4; sh < 32; sh <<= 1) {
+        mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, sh));
+        mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, sh));
+      }
+      const float mn0 = fmaxf(m_run[0], mx0), mn1 = fmaxf(m_run[1], mx1);  // finite: row 0 valid
+      if (__any_sync(0xffffffffu, mn0 > m_run[0] || mn1 > m_run[1])) {
+        const float c0 = exp2f(m_run[0] - mn0), c1 = exp2f(m_run[1] - mn1);
+        l_run[0] *= c0;
+        l_run[1] *= c1;
+#pragma unroll
+        for (int a = 0; a < NACC; ++a)
+#pragma unroll
+          for (int d = 0; d < D / 16; ++d) {
+            o[a][d][0] *= c0;
+            o[a][d][1] *= c1;
+            o[a][d][2] *= c0;
+            o[a][d][3] *= c1;
+          }
+        m_run[0] = mn0;
+        m_run[1] = mn1;
+      }
+      float ph[4], pl[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float pe = exp2f(sv[e] - m_run[e & 1]);
+        l_run[e & 1] += pe;
+        const float h = __bfloat162float(__float2bfloat16_rn(pe));
+        const float lo = pe - h;
+        const int md = cmode[e & 1];
+        ph[e] = LOSEP ? h : (md == 0 ? h : (md == 1 ? lo : 0.f));
+        pl[e] = lo;
+      }
+      // ---- O^T += V^T P: P's accumulator fragment -> B fragments by two transposes
+      const uint32_t pb0 = movm_t(pack_bf16(ph[0], ph[1])), pb1 = movm_t(pack_bf16(ph[2], ph[3]));
+      uint32_t pl0 = 0u, pl1 = 0u;
+      if (LOSEP) {
+        pl0 = movm_t(pack_bf16(pl[0], pl[1]));
+        pl1 = movm_t(pack_bf16(pl[2], pl[3]));
+      }
+      const uint32_t vst = st + SM::KV_BYTES + a_off;
+#pragma unroll
+      for (int mt = 0; mt < D / 16; ++mt) {
+        uint32_t a0, a1, a2, a3;
+        ldsm_x4_t(vst + mt * 32, a0, a1, a2, a3);
+        mma_bf16_4(o[0][mt], a0, a1, a2, a3, pb0, pb1);
+        if (LOSEP) mma_bf16_4(o[NACC - 1][mt], a0, a1, a2, a3, pl0, pl1);
       }
     }
     trace(i, 2);
-    // ---- flush at the end of this CTA's segment of the group
+    // ---- flush at the end of this CTA's segment of the group: every warp writes its own
+    // (m, l, o) partial with plain stores (no barrier, fence or ticket, so the load
+    // streams of the other warps never stall); merge_groups_kernel combines them (O12)
     if (grp_end) {
-      __syncwarp();  // this warp's ldmatrix reads of stage s_cur are done: reuse it as scratch
-      float* sm_m = (float*)(wbase + (size_t)s_cur * SM::STAGE);  // [8]
-      float* sm_l = sm_m + 8;                                     // [8]
-      float* sm_o = sm_m + 64;                                    // [ALPHA][D]
-      float lsum = l_run;
-      lsum += __shfl_xor_sync(0xffffffffu, lsum, 1);
-      lsum += __shfl_xor_sync(0xffffffffu, lsum, 2);
-      if (tig == 0) {
-        sm_m[gid] = m_run;
-        sm_l[gid] = lsum;
-      }
-      if (gid < ALPHA) {
+      float lsum[2] = {l_run[0], l_run[1]};
 #pragma unroll
-        for (int d = 0; d < D / 8; ++d) {
-          sm_o[gid * D + 8 * d + 2 * tig] = o[d][0] + o[d][2];
-          sm_o[gid * D + 8 * d + 2 * tig + 1] = o[d][1] + o[d][3];
-        }
+      for (int sh = 4; sh < 32; sh <<= 1) {
+        lsum[0] += __shfl_xor_sync(0xffffffffu, lsum[0], sh);
+        lsum[1] += __shfl_xor_sync(0xffffffffu, lsum[1], sh);
       }
-      __syncthreads();
       const int b = cc.bg / G, g = cc.bg - (cc.bg / G) * G;
       const int first = (cc.grp * cpg) / cpc;
-      const int last = (cc.grp * cpg + cpg - 1) / cpc;
-      const int seg = blockIdx.x - first;
+      const int part = (blockIdx.x - first) * NWARP + warp;
       const size_t head_base = ((size_t)cc.lr * B + b) * Hq + g * ALPHA;
-      for (int t = tid; t < ALPHA * D; t += AT2_THREADS) {
-        const int j = t / D, d = t % D;
-        float M = -INFINITY;
+      // O[head][d] = hi column + lo column (lane tig ^ 2 for alpha 4, tig ^ 1 for alpha 2,
+      // the other slot for alpha 1, the second accumulator for alpha 8)
+      constexpr int PX = ALPHA == 4 ? 2 : 1;
 #pragma unroll
-        for (int w = 0; w < NWARP; ++w)
-          M = fmaxf(M, ((const float*)(at_smem + (size_t)w * SM::WARP_BYTES +
-                                       (size_t)s_cur * SM::STAGE))[j]);
-        float acc = 0.f, lacc = 0.f;
-        if (M != -INFINITY) {
+      for (int d = 0; d < D / 16; ++d)
 #pragma unroll
-          for (int w = 0; w < NWARP; ++w) {
-            const float* ws_ =
-                (const float*)(at_smem + (size_t)w * SM::WARP_BYTES + (size_t)s_cur * SM::STAGE);
-            const float mw = ws_[j];
-            if (mw == -INFINITY) continue;
-            const float f = exp2f(mw - M);
-            acc += f * ws_[64 + j * D + d];
-            lacc += f * ws_[8 + j];
+        for (int r = 0; r < 4; ++r) {
+          float v = o[0][d][r];
+          if (LOSEP) v += o[NACC - 1][d][r];
+          else if (ALPHA == 1) v = o[0][d][r & 2] + o[0][d][(r & 2) + 1];
+          else v += __shfl_xor_sync(0xffffffffu, v, PX);
+          const int sl = r & 1;
+          if (cmode[sl] == 0 && (ALPHA != 1 || sl == 0))
+            part_o[((head_base + hd[sl]) * segstride + part) * D + 16 * d + gid + (r >= 2 ? 8 : 0)] = v;
+        }
+      if (gid == 0) {
+#pragma unroll
+        for (int sl = 0; sl < 2; ++sl)
+          if (cmode[sl] == 0 && (ALPHA != 1 || sl == 0)) {
+            float* ml = part_ml + ((head_base + hd[sl]) * segstride + part) * 2;
+            ml[0] = m_run[sl];
+            ml[1] = lsum[sl];
           }
-        }
-        part_o[((head_base + j) * segstride + seg) * D + d] = acc;
-        if (d == 0) {
-          part_ml[((head_base + j) * segstride + seg) * 2] = M;
-          part_ml[((head_base + j) * segstride + seg) * 2 + 1] = lacc;
-        }
       }
-      if (last_block_ticket(&cnt[cc.grp], last - first + 1, &flag))
-        merge_partials<D, ALPHA>(part_o, part_ml, last - first + 1, segstride, head_base, out, lse,
-                                 ((size_t)(layer_begin + cc.lr) * B + b) * Hq + g * ALPHA,
-                                 AT2_THREADS);
-      __syncthreads();  // scratch (stage s_cur) reads done before the ring refills it
-      m_run = -INFINITY;
-      l_run = 0.f;
+      m_run[0] = m_run[1] = -INFINITY;
+      l_run[0] = l_run[1] = 0.f;
 #pragma unroll
-      for (int d = 0; d < D / 8; ++d) o[d][0] = o[d][1] = o[d][2] = o[d][3] = 0.f;
+      for (int a = 0; a < NACC; ++a)
+#pragma unroll
+        for (int d = 0; d < D / 16; ++d) o[a][d][0] = o[a][d][1] = o[a][d][2] = o[a][d][3] = 0.f;
       if (i + 1 < n_chunks) {
 #pragma unroll
         for (int k = 0; k < KS; ++k) {
@@ -393,5 +444,6 @@ __global__ void __launch_bounds__(AT2_THREADS, 2) attn_bf16_kernel(
     }
     s_cur = s_cur == NSTAGE - 1 ? 0 : s_cur + 1;
   }
+  trace_warp(1);
   cp_async_wait<0>();
 }

@@ -8,6 +8,7 @@
 #include <stdint.h>
 
 #include <atomic>
+#include <cstdlib>
 
 #include "../../include/spc.h"
 
@@ -32,6 +33,34 @@ inline int launched(cudaError_t pre = cudaSuccess) {
   } while (0)
 
 inline cudaStream_t as_stream(spc_stream_t s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// Programmatic dependent launch: every libspc kernel starts with spc_pdl_entry()
+// (griddepcontrol.wait before ANY global memory access, then launch_dependents), so a
+// kernel launched with the PDL attribute behind another kernel only overlaps its launch
+// and CTA scheduling with the predecessor's tail; memory semantics stay stream-ordered.
+// SPC_PDL=0 in the environment launches without the attribute.
+inline bool pdl_enabled() {
+  static const int v = [] {
+    const char* e = std::getenv("SPC_PDL");
+    return (e && e[0] == '0') ? 0 : 1;
+  }();
+  return v != 0;
+}
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                            cudaStream_t st, Args... args) {
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 int num_sms();
 // Encode a tiled TMA descriptor (driver entry point fetched through cudart).
@@ -39,6 +68,10 @@ int make_tmap_3d_bf16(CUtensorMap* map, const void* base, uint64_t d0, uint64_t 
                       uint32_t box0, uint32_t box1, CUtensorMapSwizzle swz);
 
 // --------------------------------------------------------------- device side
+__device__ __forceinline__ void spc_pdl_entry() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
 __device__ __forceinline__ float bf16lo(uint32_t w) { return __uint_as_float(w << 16); }
 __device__ __forceinline__ float bf16hi(uint32_t w) { return __uint_as_float(w & 0xFFFF0000u); }
 
@@ -264,7 +297,9 @@ __device__ __forceinline__ int block_excl_scan(int v, int* wsum, int* total) {
 // resets the counter to 0 so the workspace stays reusable.
 __device__ __forceinline__ bool last_block_ticket(unsigned int* counter, unsigned int total,
                                                   int* smem_flag) {
+#ifndef SPC_DEBUG_NOFENCE  // timing experiments only: unsafe without the fence
   __threadfence();
+#endif
   __syncthreads();
   if (threadIdx.x == 0) {
     unsigned int t = atomicAdd(counter, 1u);

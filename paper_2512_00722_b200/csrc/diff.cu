@@ -38,6 +38,7 @@ __global__ void __launch_bounds__(DF_THREADS) diff_kernel(
     const int32_t* __restrict__ cur_idx, const int32_t* __restrict__ cur_count, int k,
     int32_t* __restrict__ slot_tok, int32_t* __restrict__ load_tok, int32_t* __restrict__ load_slot,
     int32_t* __restrict__ n_load, int32_t* __restrict__ evict_tok, int32_t* __restrict__ n_evict) {
+  spc_pdl_entry();
   extern __shared__ int32_t dsm[];
   int32_t* sprev = dsm;       // [k]
   int32_t* scur = dsm + k;    // [k]
@@ -151,6 +152,7 @@ __global__ void __launch_bounds__(256) gather_kernel(
     int Smax, int kbud, int row_vecs, int layer_begin, const int32_t* __restrict__ load_tok,
     const int32_t* __restrict__ load_slot, const int32_t* __restrict__ n_load,
     void* const* __restrict__ k_buf, void* const* __restrict__ v_buf) {
+  spc_pdl_entry();
   // grid: x = chunks of the budget, y = B*G row, z = layer
   const int bg = blockIdx.y;
   const int l = layer_begin + blockIdx.z;
@@ -194,7 +196,7 @@ extern "C" int spc_elastic_diff(const int32_t* prev_idx, const int32_t* prev_cou
                          (int)(sizeof(int32_t) * 3 * SPC_MAX_K + sizeof(uint32_t) * 2 * DF_BM_WORDS));
     attr = true;
   }
-  diff_kernel<<<B * G, DF_THREADS, smem, as_stream(stream)>>>(prev_idx, prev_count, cur_idx,
+  (void)launch_k(diff_kernel, dim3(B * G), dim3(DF_THREADS), smem, as_stream(stream), prev_idx, prev_count, cur_idx,
                                                               cur_count, k, slot_tok, load_tok,
                                                               load_slot, n_load, evict_tok, n_evict);
   return launched();
@@ -215,7 +217,7 @@ extern "C" int spc_gather_kv(int dtype, const void* const* k_src, const void* co
   if ((D * esz) % 16 || D * esz / 16 > 32 || 32 % (D * esz / 16)) return SPC_E_UNSUPPORTED;
   const int row_vecs = D * esz / 16;
   dim3 grid((k + 63) / 64, B * G, layer_end - layer_begin);
-  gather_kernel<uint4><<<grid, 256, 0, as_stream(stream)>>>(k_src, v_src, B, G, Smax, k, row_vecs,
+  (void)launch_k(gather_kernel<uint4>, dim3(grid), dim3(256), 0, as_stream(stream), k_src, v_src, B, G, Smax, k, row_vecs,
                                                             layer_begin, load_tok, load_slot, n_load,
                                                             k_buf, v_buf);
   return launched();

@@ -47,6 +47,7 @@ __global__ void __launch_bounds__(32 * lg_warps<ALPHA>(), 1) logits_kernel(
     const int32_t* __restrict__ seq_len, int G, int Smax, float scale, int tpc, int tpr,
     int ntiles, float* __restrict__ logits, float* __restrict__ seg_max, int segstride,
     unsigned int* __restrict__ counters, float* __restrict__ head_max) {
+  spc_pdl_entry();
   using SM = Lg4Smem<D, ALPHA>;
   constexpr int NCH = SM::NCH, DCH = SM::DCH, LG_W = SM::LG_W, LG_T = 32 * LG_W;
   constexpr int GPR = DCH / 8;         // 16-byte granules per row and step

@@ -45,6 +45,7 @@ constexpr int NM_T = 512;
 __global__ void __cluster_dims__(NM_CL, 1, 1) __launch_bounds__(NM_T) norm_kernel(
     const float* __restrict__ logits, const float* __restrict__ head_max,
     const int32_t* __restrict__ seq_len, int Hq, int Smax, int64_t* __restrict__ head_sumfix) {
+  spc_pdl_entry();
   __shared__ long long red[NM_T / 32];
   __shared__ long long part;
   cg::cluster_group cl = cg::this_cluster();
@@ -82,6 +83,7 @@ __global__ void __launch_bounds__(GRP_THREADS) group_kernel(
     const float* __restrict__ logits, const float* __restrict__ head_max,
     const int64_t* __restrict__ head_sumfix, const int32_t* __restrict__ seq_len, int G, int Smax,
     float* __restrict__ group_score) {
+  spc_pdl_entry();
   const int bg = blockIdx.y, b = bg / G, g = bg % G;
   const int Hq = G * ALPHA;
   const int S = seq_len[b];
@@ -128,7 +130,7 @@ int launch_logits(const uint16_t* kr, const uint16_t* q, const int32_t* seq_len,
   int tpc = (ntiles + num_sms() - 1) / num_sms();
   if (tpc > tpr) tpc = tpr;  // a CTA spans at most two groups
   const int ncta = (ntiles + tpc - 1) / tpc;
-  logits_kernel<D, ALPHA><<<ncta, 32 * lg_warps<ALPHA>(), smem, st>>>(kr, q, seq_len, G, Smax,
+  (void)launch_k(logits_kernel<D, ALPHA>, dim3(ncta), dim3(32 * lg_warps<ALPHA>()), smem, st, kr, q, seq_len, G, Smax,
                                                                       scale, tpc, tpr,
                                                     ntiles, logits, seg_max, segstride, counters,
                                                     head_max);
@@ -139,7 +141,7 @@ template <int ALPHA>
 int launch_group(const float* logits, const float* head_max, const int64_t* sumfix,
                  const int32_t* seq_len, int B, int G, int Smax, float* gs, cudaStream_t st) {
   dim3 grid((Smax + GRP_TILE - 1) / GRP_TILE, B * G);
-  group_kernel<ALPHA><<<grid, GRP_THREADS, 0, st>>>(logits, head_max, sumfix, seq_len, G, Smax, gs);
+  (void)launch_k(group_kernel<ALPHA>, dim3(grid), dim3(GRP_THREADS), 0, st, logits, head_max, sumfix, seq_len, G, Smax, gs);
   return launched();
 }
 
@@ -208,7 +210,7 @@ extern "C" int spc_score(int dtype, const void* q, const void* kr, const int32_t
 #undef LG
   }
   if (phases & SPC_SCORE_NORM) {
-    norm_kernel<<<dim3(NM_CL, B * Hq), NM_T, 0, st>>>(logits, head_max, seq_len, Hq, Smax,
+    (void)launch_k(norm_kernel, dim3(dim3(NM_CL, B * Hq)), dim3(NM_T), 0, st, logits, head_max, seq_len, Hq, Smax,
                                                       head_sumfix);
     SPC_TRY(launched());
   }

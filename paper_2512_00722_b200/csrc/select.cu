@@ -44,14 +44,14 @@ constexpr int W0_BITS = 12;     // key bits (sign + exponent + 3 mantissa) fixed
 constexpr int CANDMAX = 128;    // exchange the threshold bucket at this size
 
 // Debug trace (spc_debug_set_select_trace; compiled in with -DSPC_TRACE): thread 0
-// of every CTA of row 0 stamps %globaltimer at phase boundaries: [rank][slot].
+// of every CTA of rows 0..63 stamps %globaltimer at phase boundaries: [row][rank][slot].
 __device__ unsigned long long* g_sel_trace = nullptr;
 __device__ __forceinline__ void sel_mark(int slot) {
 #ifdef SPC_TRACE
-  if (g_sel_trace && blockIdx.y == 0 && threadIdx.x == 0 && slot < 16) {
+  if (g_sel_trace && blockIdx.y < 64 && threadIdx.x == 0 && slot < 16) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-    g_sel_trace[blockIdx.x * 16 + slot] = t;
+    g_sel_trace[(blockIdx.y * SCL + blockIdx.x) * 16 + slot] = t;
   }
 #else
   (void)slot;
@@ -162,6 +162,7 @@ __global__ void __cluster_dims__(SCL, 1, 1) __launch_bounds__(ST, 1) select_kern
     const int32_t* __restrict__ prev_idx, const int32_t* __restrict__ prev_count,
     int32_t* __restrict__ load_tok, int32_t* __restrict__ n_load, int32_t* __restrict__ evict_tok,
     int32_t* __restrict__ n_evict) {
+  spc_pdl_entry();
   extern __shared__ __align__(16) uint8_t sel_raw[];
   SelSm& s = *reinterpret_cast<SelSm*>(sel_raw);
   cg::cluster_group cl = cg::this_cluster();
@@ -582,7 +583,7 @@ __global__ void __cluster_dims__(SCL, 1, 1) __launch_bounds__(ST, 1) select_kern
 using namespace spc;
 
 // debug only (not in include/spc.h): point the -DSPC_TRACE stamps at a device buffer of
-// SCL x 16 uint64, or NULL to stop
+// 64 x SCL x 16 uint64, or NULL to stop
 extern "C" int spc_debug_set_select_trace(unsigned long long* buf) {
   return cudaMemcpyToSymbol(spc::g_sel_trace, &buf, sizeof(buf)) == cudaSuccess ? SPC_OK
                                                                                  : SPC_E_CUDA;
@@ -611,9 +612,10 @@ extern "C" int spc_select(const float* logits, const float* head_max, const int3
                                    (int)sizeof(SelSm)));                                        \
       attr = true;                                                                              \
     }                                                                                           \
-    select_kernel<AA, (AA > 4 ? 1 : 2)><<<dim3(SCL, B * G), ST, sizeof(SelSm), st>>>(                             \
-        logits, head_max, seq_len, G, Smax, k, force_last, head_sumfix, group_score, out_idx,   \
-        out_count, prev_idx, prev_count, load_tok, n_load, evict_tok, n_evict);                 \
+    (void)launch_k(select_kernel<AA, (AA > 4 ? 1 : 2)>, dim3(SCL, B * G), dim3(ST),             \
+                   sizeof(SelSm), st, logits, head_max, seq_len, G, Smax, k, force_last,         \
+                   head_sumfix, group_score, out_idx, out_count, prev_idx, prev_count, load_tok, \
+                   n_load, evict_tok, n_evict);                                                  \
     return launched();                                                                          \
   }
   SEL(1) SEL(2) SEL(4) SEL(8)

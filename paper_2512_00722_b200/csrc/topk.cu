@@ -311,6 +311,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(SEL_THREADS, 1)
                         int n_cols, int k, int force, int stride, int offset,
                         int32_t* __restrict__ out_idx, float* __restrict__ out_val,
                         int32_t* __restrict__ out_count, unsigned long long* __restrict__ out_thresh) {
+  spc_pdl_entry();
   extern __shared__ __align__(16) uint8_t cl_raw[];
   ClSmem& s = *reinterpret_cast<ClSmem*>(cl_raw);
   cg::cluster_group cl = cg::this_cluster();
@@ -344,6 +345,7 @@ __global__ void __launch_bounds__(SEL_THREADS, 1) merge_kernel(
     const float* __restrict__ cval, const int32_t* __restrict__ cpos,
     const int32_t* __restrict__ ccnt, int P, int R, int k,
     unsigned long long* __restrict__ out_thresh) {
+  spc_pdl_entry();
   extern __shared__ __align__(16) uint8_t sel_raw[];
   SelSmem& s = *reinterpret_cast<SelSmem*>(sel_raw);
   __shared__ int off[65];
@@ -370,6 +372,7 @@ __global__ void __launch_bounds__(SEL_THREADS, 1) merge_kernel(
 __global__ void __launch_bounds__(SEL_THREADS) filter_kernel(
     int32_t* __restrict__ idx, const float* __restrict__ val, int32_t* __restrict__ count,
     const unsigned long long* __restrict__ thresh, int k, int stride, int offset) {
+  spc_pdl_entry();
   __shared__ int wsum[SEL_THREADS / 32];
   __shared__ int total;
   const int row = blockIdx.x, tid = threadIdx.x;
@@ -441,7 +444,7 @@ extern "C" int spc_topk(const float* val, const int32_t* seq_len, int B, int G, 
     SPC_TRY(set_big_smem((const void*)topk_cluster_kernel, sizeof(ClSmem)));
     attr = true;
   }
-  topk_cluster_kernel<<<dim3(CL, B * G), SEL_THREADS, sizeof(ClSmem), as_stream(stream)>>>(
+  (void)launch_k(topk_cluster_kernel, dim3(dim3(CL, B * G)), dim3(SEL_THREADS), sizeof(ClSmem), as_stream(stream), 
       val, seq_len, G, n_cols, k, force_last, id_stride, id_offset, out_idx, out_val, out_count,
       (unsigned long long*)out_thresh);
   return launched();
@@ -467,7 +470,7 @@ extern "C" int spc_topk_merge(const float* cand_val, const int32_t* cand_pos,
     SPC_TRY(set_big_smem((const void*)merge_kernel, sizeof(SelSmem)));
     attr = true;
   }
-  merge_kernel<<<R, SEL_THREADS, sizeof(SelSmem), as_stream(stream)>>>(
+  (void)launch_k(merge_kernel, dim3(R), dim3(SEL_THREADS), sizeof(SelSmem), as_stream(stream), 
       cand_val, cand_pos, cand_count, P, R, k, (unsigned long long*)out_thresh);
   return launched();
 }
@@ -478,7 +481,7 @@ extern "C" int spc_topk_filter(int32_t* idx, const float* val, int32_t* count,
   if (!idx || !val || !count || !thresh) return SPC_E_NULL;
   if (R < 1) return SPC_E_SHAPE;
   if (k < 1 || k > SPC_MAX_K) return SPC_E_BUDGET;
-  filter_kernel<<<R, SEL_THREADS, 0, as_stream(stream)>>>(
+  (void)launch_k(filter_kernel, dim3(R), dim3(SEL_THREADS), 0, as_stream(stream), 
       idx, val, count, (const unsigned long long*)thresh, k, id_stride, id_offset);
   return launched();
 }

@@ -7,7 +7,16 @@ import sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
 
-from paper_2512_00722_b200 import spc, synth  # noqa: E402
+from paper_2512_00722_b200 import build, spc, synth  # noqa: E402
+
+_lib_arg = [a for a in sys.argv if a.startswith("--lib=")]
+if _lib_arg:  # a debug build of libspc (tools/ only)
+    spc._lib = spc.load_library(_lib_arg[0][6:])
+elif "--nomath" in sys.argv:  # the kernel's load pipeline alone (debug build, tools/ only)
+    _so = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libspc_nomath.so")
+    if not os.path.exists(_so):
+        build.build(out=_so, defines=["SPC_ATTN_NOMATH"])
+    spc._lib = spc.load_library(_so)
 
 dev = torch.device("cuda")
 L, B, G, Hq, D, S, k = 32, 1, 8, 32, 128, 32768, 2048
@@ -70,3 +79,15 @@ t = timeit(lambda: bb.copy_(a))
 print(f"torch copy 1 GiB                           {t*1e6:8.1f} us  {2*a.numel()/t/1e9:8.1f} GB/s (r+w)")
 t = timeit(lambda: a.sum(dtype=torch.int64) if False else torch.sum(a.view(torch.int64)))
 print(f"torch sum 1 GiB (read only)                {t*1e6:8.1f} us  {a.numel()/t/1e9:8.1f} GB/s")
+# V allocation shifted by an odd multiple of 256 B relative to K (HBM channel/bank aliasing test)
+for shift_bytes in (0, 256 * 4099, (1 << 20) + 256 * 3):
+    big = torch.empty(vc.numel() + shift_bytes // 2 + 64, dtype=vc.dtype, device=dev)
+    vs = big[shift_bytes // 2: shift_bytes // 2 + vc.numel()].view_as(vc)
+    vs.copy_(vc)
+    vtab_s = spc.ptr_table([vs[l] for l in range(L)], dev)
+    idx = cases["random sorted rows, density 0.0625"]
+    t = timeit(lambda: spc.sparse_decode_attn(q, ktab, vtab_s, spc.KV_INDEXED, idx, cnt, S, k, 0.088,
+                                              out, lse, ws, G))
+    print(f"attn  V shifted by {shift_bytes:9d} B, dens 1/16      {t*1e6:8.1f} us  {nbytes/t/1e9:8.1f} GB/s"
+          f"  (K-V offset mod 2 MiB = {(vs.data_ptr() - kc.data_ptr()) % (2 << 20)})")
+    del big, vs

@@ -28,7 +28,7 @@ ws = spc.alloc_workspace(spc.score_workspace(B, Hq, S), dev)
 idx = [z(B, G, k, dt=i32) for _ in range(2)]
 cnt = [z(B, G, dt=i32) for _ in range(2)]
 lt, nl = z(B, G, k, dt=i32), z(B, G, dt=i32)
-tr = torch.zeros(8 * 16, dtype=torch.int64, device=dev)
+tr = torch.zeros(64 * 8 * 16, dtype=torch.int64, device=dev)
 names = ["start", "norm", "group", "pass0", "passes", "T", "counts", "end", "x_comp", "x_sync",
          "bitmap", "exp", "push"]
 for step in range(4):
@@ -43,9 +43,15 @@ for step in range(4):
     e[1].record()
     torch.cuda.synchronize()
     print(f"step {step}: {e[0].elapsed_time(e[1]) * 1e3:.1f} us")
-t = tr.view(8, 16).cpu().numpy().astype("float64")
-t0 = t[:, 0][t[:, 0] > 0].min()
+t = tr.view(64, 8, 16).cpu().numpy().astype("float64")
+rows = int((t[:, 0, 0] > 0).sum())
+t0 = t[:rows, :, 0].min()
 print("rank " + " ".join(f"{n:>8s}" for n in names))
 for r in range(8):
-    print(f"{r:4d} " + " ".join(f"{(t[r, i] - t0) / 1e3:8.2f}" if t[r, i] > 0 else "       -"
+    print(f"{r:4d} " + " ".join(f"{(t[0, r, i] - t0) / 1e3:8.2f}" if t[0, r, i] > 0 else "       -"
                                 for i in range(len(names))))
+print("row  start_min start_max  end_max   (us from the first CTA start)")
+for row in range(rows):
+    st = t[row, :, 0]
+    en = t[row, :, 7]
+    print(f"{row:3d} {(st.min() - t0) / 1e3:9.2f} {(st.max() - t0) / 1e3:9.2f} {(en.max() - t0) / 1e3:9.2f}")
