@@ -100,58 +100,6 @@ __device__ void merge_partials(const float* part_o, const float* part_ml, int ns
 
 #include "attn_bf16.cuh"
 
-// One CTA per (layer, b, g): merges the per-warp partials the bf16 kernel wrote for the
-// group's CTA segments (O12) into out / lse.  The (m, l) of every partial are staged in
-// shared memory and turned into weights w_p = exp2(m_p - M) once per head; each thread
-// then forms one output element from independent (unrolled) loads of the o partials.
-constexpr int MG_MAXP = 4 * (SPC_MAX_K / 64 + 2);
-template <int D, int ALPHA>
-__global__ void __launch_bounds__(ALPHA * D) merge_groups_kernel(
-    const float* __restrict__ part_o, const float* __restrict__ part_ml, int B, int G, int kpad,
-    int cpc, int segstride, int layer_begin, float* __restrict__ out, float* __restrict__ lse) {
-  spc_pdl_entry();
-  __shared__ float w[ALPHA][MG_MAXP];
-  __shared__ float inv_den[ALPHA];
-  const int grp = blockIdx.x, BG = B * G, Hq = G * ALPHA;
-  const int lr = grp / BG, bg = grp - lr * BG, b = bg / G, g = bg - b * G;
-  const int cpg = kpad / CH;
-  const int first = (grp * cpg) / cpc, last = (grp * cpg + cpg - 1) / cpc;
-  const int np = min((last - first + 1) * NWARP, segstride);
-  const size_t head_base = ((size_t)lr * B + b) * Hq + g * ALPHA;
-  const size_t out_base = ((size_t)(layer_begin + lr) * B + b) * Hq + g * ALPHA;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  if (warp < ALPHA) {  // warp j: weights and normaliser of head j
-    const float* ml = part_ml + (head_base + warp) * segstride * 2;
-    float M = -INFINITY;
-    for (int p = lane; p < np; p += 32) M = fmaxf(M, __ldcg(ml + 2 * p));
-    M = warp_max(M);
-    float den = 0.f;
-    for (int p = lane; p < np; p += 32) {
-      const float m = __ldcg(ml + 2 * p);
-      const float wp = m == -INFINITY ? 0.f : exp2f(m - M);
-      w[warp][p] = wp;
-      den += wp * __ldcg(ml + 2 * p + 1);
-    }
-    den = warp_sum(den);
-    if (lane == 0) {
-      inv_den[warp] = den > 0.f ? 1.f / den : 0.f;
-      if (lse) lse[out_base + warp] = den > 0.f ? (M + log2f(den)) * LN2 : -INFINITY;
-    }
-  }
-  __syncthreads();
-  const int j = tid / D, d = tid - (tid / D) * D;
-  const float* po = part_o + (head_base + j) * segstride * D + d;
-  float num = 0.f;
-  int p = 0;
-  for (; p + 4 <= np; p += 4) {
-    const float o0 = __ldcg(po + (size_t)p * D), o1 = __ldcg(po + (size_t)(p + 1) * D);
-    const float o2 = __ldcg(po + (size_t)(p + 2) * D), o3 = __ldcg(po + (size_t)(p + 3) * D);
-    num += w[j][p] * o0 + w[j][p + 1] * o1 + w[j][p + 2] * o2 + w[j][p + 3] * o3;
-  }
-  for (; p < np; ++p) num += w[j][p] * __ldcg(po + (size_t)p * D);
-  out[(out_base + j) * D + d] = num * inv_den[j];
-}
-
 // ---------------------------------------------------------------- fp32 / CUDA-core path
 template <int D, int ALPHA>
 __global__ void __launch_bounds__(AT_THREADS) attn_f32_kernel(
@@ -319,10 +267,6 @@ extern "C" int spc_sparse_decode_attn(int dtype, const void* q, const void* cons
           (const uint16_t*)q, k_layers, v_layers, kv_mode, idx, count, layer_begin, B, G, rows, \
           k, kpad, scale, (int)(rpc / CH), n_groups, w.segstride, w.part_o, w.part_ml, w.cnt,   \
           out, lse);                                                                            \
-      SPC_TRY(launched());                                                                      \
-      (void)launch_k(merge_groups_kernel<DD, AA>, dim3(n_groups), dim3(AA * DD), 0, st,         \
-          (const float*)w.part_o, (const float*)w.part_ml, B, G, kpad, (int)(rpc / CH),         \
-          w.segstride, layer_begin, out, lse);                                                  \
     } else {                                                                                    \
       dim3 grid(nsplit, B * G, layer_end - layer_begin);                                        \
       (void)launch_k(attn_f32_kernel<DD, AA>, dim3(grid), dim3(AT_THREADS), 0, st,                                      \

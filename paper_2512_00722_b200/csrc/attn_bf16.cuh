@@ -124,6 +124,65 @@ __device__ __forceinline__ void trace_warp(int which) {
 #endif
 }
 
+// LSE merge (O12) of the np partials of one group by one CTA of NT threads, latency-
+// friendly: the weights w_p = exp2(m_p - M) of every head are computed once into shared
+// scratch (sm: >= ALPHA * (np + 1) floats), then each thread issues all the loads of
+// its R output elements at once.
+template <int D, int ALPHA, int NT>
+__device__ void merge_group_fast(const float* __restrict__ part_o,
+                                 const float* __restrict__ part_ml, int np, int segstride,
+                                 size_t head_base, float* __restrict__ out,
+                                 float* __restrict__ lse, size_t out_base, float* sm) {
+  constexpr int R = (ALPHA * D + NT - 1) / NT;  // outputs per thread (the last may be idle)
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  float* w = sm;                  // [ALPHA][np]
+  float* inv = sm + ALPHA * np;   // [ALPHA]
+  for (int j = warp; j < ALPHA; j += NT / 32) {
+    const float* ml = part_ml + (head_base + j) * segstride * 2;
+    float M = -INFINITY;
+    for (int p = lane; p < np; p += 32) M = fmaxf(M, __ldcg(ml + 2 * p));
+    M = warp_max(M);
+    float den = 0.f;
+    for (int p = lane; p < np; p += 32) {
+      const float m = __ldcg(ml + 2 * p);
+      const float wp = m == -INFINITY ? 0.f : exp2f(m - M);
+      w[j * np + p] = wp;
+      den += wp * __ldcg(ml + 2 * p + 1);
+    }
+    den = warp_sum(den);
+    if (lane == 0) {
+      inv[j] = den > 0.f ? 1.f / den : 0.f;
+      if (lse) lse[out_base + j] = den > 0.f ? (M + log2f(den)) * 0.6931471805599453f : -INFINITY;
+    }
+  }
+  __syncthreads();
+  float num[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) num[r] = 0.f;
+  for (int p0 = 0; p0 < np; p0 += 4) {
+    float v[R][4];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int i = min(tid + r * NT, ALPHA * D - 1), j = i / D, d = i - (i / D) * D;
+      const float* po = part_o + ((head_base + j) * segstride + p0) * D + d;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[r][u] = p0 + u < np ? __ldcg(po + (size_t)u * D) : 0.f;
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int j = min(tid + r * NT, ALPHA * D - 1) / D;
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (p0 + u < np) num[r] += w[j * np + p0 + u] * v[r][u];
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int i = tid + r * NT, j = i / D, d = i - (i / D) * D;
+    if (i < ALPHA * D) out[(out_base + j) * D + d] = num[r] * inv[j];
+  }
+}
+
 // Position of a chunk, advanced incrementally (no division on the hot path):
 // group index, chunk within the group, and the group's (layer, b*G+g).
 struct ChunkIt {
@@ -446,4 +505,29 @@ __global__ void __launch_bounds__(AT2_THREADS, AT2_CTAS_PER_SM) attn_bf16_kernel
   }
   trace_warp(1);
   cp_async_wait<0>();
+  // ---- after the CTA's last chunk (no loads left to stall): one ticket per group this
+  // CTA covered; the CTA completing a group merges its partials with the LSE rule (O12)
+  __shared__ int merge_flag;
+  const int g_first = c_begin / cpg, g_last = (c_begin + n_chunks - 1) / cpg;
+  __syncthreads();  // every warp's partial stores are issued
+  if (tid == 0) __threadfence();  // ... and visible before the tickets
+  for (int gq = g_first; gq <= g_last; ++gq) {
+    const int nseg = (gq * cpg + cpg - 1) / cpc - (gq * cpg) / cpc + 1;
+    if (tid == 0) {
+      const unsigned t = atomicAdd(&cnt[gq], 1u);
+      merge_flag = t == (unsigned)nseg - 1;
+      if (t == (unsigned)nseg - 1) {
+        cnt[gq] = 0u;  // the workspace stays reusable
+        __threadfence();
+      }
+    }
+    __syncthreads();
+    if (merge_flag) {
+      const int lr = gq / BG, bgq = gq - (gq / BG) * BG, b = bgq / G, g = bgq - (bgq / G) * G;
+      merge_group_fast<D, ALPHA, AT2_THREADS>(
+          part_o, part_ml, nseg * NWARP, segstride, ((size_t)lr * B + b) * Hq + g * ALPHA, out,
+          lse, ((size_t)(layer_begin + lr) * B + b) * Hq + g * ALPHA, (float*)at_smem);
+    }
+    __syncthreads();  // merge_flag is rewritten for the next group
+  }
 }

@@ -91,3 +91,17 @@ for shift_bytes in (0, 256 * 4099, (1 << 20) + 256 * 3):
     print(f"attn  V shifted by {shift_bytes:9d} B, dens 1/16      {t*1e6:8.1f} us  {nbytes/t/1e9:8.1f} GB/s"
           f"  (K-V offset mod 2 MiB = {(vs.data_ptr() - kc.data_ptr()) % (2 << 20)})")
     del big, vs
+# back-to-back launches (no flush in between: each launch still reads 268 MB > L2)
+idx = cases["random sorted rows, density 0.0625"]
+fn = run(idx)
+for _ in range(3):
+    fn()
+torch.cuda.synchronize()
+a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+a.record()
+for _ in range(10):
+    fn()
+b.record()
+torch.cuda.synchronize()
+t = a.elapsed_time(b) * 1e-3 / 10
+print(f"attn  10 back-to-back launches, dens 1/16     {t*1e6:8.1f} us  {nbytes/t/1e9:8.1f} GB/s")
