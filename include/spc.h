@@ -162,7 +162,7 @@ int spc_topk_filter(int32_t* idx, const float* val, int32_t* count, const uint64
  * out_thresh not produced).  One thread-block cluster per (b, g) row.
  * logits/head_max come from spc_score(LOGITS).  prev_idx/prev_count is the
  * previous step's selection (count 0 on the first step).
- * Supported: alpha in {1,2,4,8}, 1 <= k <= SPC_MAX_K, Smax <= 131072 and a
+ * Supported: alpha in {1,2,4,8}, 1 <= k <= SPC_MAX_K, Smax <= 135168 and a
  * multiple of 4 (SPC_E_UNSUPPORTED otherwise: use the separate calls).
  * prev_idx rows must be ascending (as spc_topk / spc_select write them).
  * evict_tok / n_evict may be NULL.  Errors: SPC_E_NULL, SPC_E_SHAPE,

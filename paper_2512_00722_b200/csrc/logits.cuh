@@ -19,14 +19,22 @@
 // CTA of a group (ticket) reduces the segments to head_max (O2: exact).
 #pragma once
 
-constexpr int LG_RPT = 4;                 // rows per lane (2 FFMA2 row pairs)
+#ifndef SPC_LG_RPT
+#define SPC_LG_RPT 4
+#endif
+#ifndef SPC_LG_WARPS
+#define SPC_LG_WARPS 6
+#endif
+constexpr int LG_RPT = SPC_LG_RPT;        // rows per lane (LG_RPT / 2 FFMA2 row pairs)
 constexpr int LG_TR = 32 * LG_RPT;        // rows per tile
 constexpr int LG_DCH = 64;                // d per pipeline step
 constexpr int LG_RS = LG_DCH * 2 + 16;    // padded shared row: 144 B (conflict-free LDS.128)
-constexpr int LG_STAGE = LG_TR * LG_RS;   // 18 KiB
+constexpr int LG_STAGE = LG_TR * LG_RS;   // 18 KiB at 4 rows per lane
 constexpr int LG_NST = 2;                 // per-warp ring depth: one step loads while one computes
 template <int ALPHA>
-constexpr int lg_warps() { return ALPHA >= 8 ? 5 : 6; }  // warps per CTA (one CTA per SM)
+constexpr int lg_warps() {  // warps per CTA (one CTA per SM), bounded by the shared ring
+  return ALPHA >= 8 ? SPC_LG_WARPS * 5 / 6 : SPC_LG_WARPS;
+}
 
 template <int D, int ALPHA>
 struct Lg4Smem {

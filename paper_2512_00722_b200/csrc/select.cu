@@ -37,7 +37,7 @@ namespace {
 
 constexpr int ST = 512;         // threads per CTA
 constexpr int SCL = 8;          // CTAs per row (cluster size)
-constexpr int SEGCAP = 16384;   // tokens per CTA segment: rows up to SCL * SEGCAP
+constexpr int SEGCAP = 16896;   // tokens per CTA segment: rows up to SCL * SEGCAP = 135168
 constexpr int NB = 256;         // bins per histogram pass
 constexpr int W0_SHIFT = 20;    // pass-0 bin = value bits >> 20: 8 bins per binade
 constexpr int W0_BITS = 12;     // key bits (sign + exponent + 3 mantissa) fixed by a pass-0 bin
@@ -256,15 +256,27 @@ __global__ void __cluster_dims__(SCL, 1, 1) __launch_bounds__(ST, 1) select_kern
       }
     }
   }
-  for (int ch = c0 + NC; ch < c1; ++ch) {  // segments longer than 4 * NC * ST tokens
+  // segments longer than 4 * NC * ST tokens: stream the rest two chunks at a time (both
+  // chunks' loads in flight before the first exp)
+  for (int ch = c0 + NC; ch < c1; ch += 2) {
+    float4 x[2][ALPHA];
 #pragma unroll
-    for (int j = 0; j < ALPHA; ++j) {
-      const float4 x = __ldg(reinterpret_cast<const float4*>(lg + (size_t)j * Smax) + ch);
-      const float xs[4] = {x.x, x.y, x.z, x.w};
+    for (int u = 0; u < 2; ++u)
 #pragma unroll
-      for (int c = 0; c < 4; ++c)
-        if (4 * ch + c < s1 - s0) acc[j] += fixpoint40(spc_exp_dev(__fsub_rn(xs[c], m[j])));
-    }
+      for (int j = 0; j < ALPHA; ++j)
+        x[u][j] = ch + u < c1 ? __ldg(reinterpret_cast<const float4*>(lg + (size_t)j * Smax) + ch + u)
+                              : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int u = 0; u < 2; ++u)
+#pragma unroll
+      for (int j = 0; j < ALPHA; ++j) {
+        const float2 ea = spc_exp2_dev(__fsub_rn(x[u][j].x, m[j]), __fsub_rn(x[u][j].y, m[j]));
+        const float2 eb = spc_exp2_dev(__fsub_rn(x[u][j].z, m[j]), __fsub_rn(x[u][j].w, m[j]));
+        const float es[4] = {ea.x, ea.y, eb.x, eb.y};
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+          if (ch + u < c1 && 4 * (ch + u) + c < s1 - s0) acc[j] += fixpoint40(es[c]);
+      }
   }
   sel_mark(11);
 #pragma unroll
@@ -322,32 +334,45 @@ __global__ void __cluster_dims__(SCL, 1, 1) __launch_bounds__(ST, 1) select_kern
       reinterpret_cast<float4*>(gso)[ch] = o;  // tokens past len in the chunk get 0
     }
   }
-  for (int ch = c0 + NC; ch < c1; ++ch) {
-    float e[ALPHA][4];
+  for (int ch0 = c0 + NC; ch0 < c1; ch0 += 2) {
+    float4 x[2][ALPHA];
 #pragma unroll
-    for (int j = 0; j < ALPHA; ++j) {
-      const float4 x = __ldg(reinterpret_cast<const float4*>(lg + (size_t)j * Smax) + ch);
-      const float xs[4] = {x.x, x.y, x.z, x.w};
+    for (int u = 0; u < 2; ++u)
 #pragma unroll
-      for (int c = 0; c < 4; ++c)
-        e[j][c] = 4 * ch + c < s1 - s0 ? spc_exp_dev(__fsub_rn(xs[c], m[j])) : 0.0f;
-    }
-    float gs[4];
+      for (int j = 0; j < ALPHA; ++j)
+        x[u][j] = ch0 + u < c1
+                      ? __ldg(reinterpret_cast<const float4*>(lg + (size_t)j * Smax) + ch0 + u)
+                      : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      float v = __fmul_rn(e[0][c], r[0]);
+    for (int u = 0; u < 2; ++u) {
+      const int ch = ch0 + u;
+      if (ch >= c1) break;
+      float e[ALPHA][4];
 #pragma unroll
-      for (int j = 1; j < ALPHA; ++j) v = fmaxf(v, __fmul_rn(e[j][c], r[j]));
-      gs[c] = v;
-      const int p = 4 * ch + c;
-      if (cut && p < s1 - s0) {
-        const unsigned long long key = key_of(__float_as_uint(v), s0 + p, len, force);
-        atomicAdd(&s.hist[min(max((int)(key >> 52) - base0, 0), NB - 1)], 1u);
+      for (int j = 0; j < ALPHA; ++j) {
+        const float2 ea = spc_exp2_dev(__fsub_rn(x[u][j].x, m[j]), __fsub_rn(x[u][j].y, m[j]));
+        const float2 eb = spc_exp2_dev(__fsub_rn(x[u][j].z, m[j]), __fsub_rn(x[u][j].w, m[j]));
+        const float es[4] = {ea.x, ea.y, eb.x, eb.y};
+#pragma unroll
+        for (int c = 0; c < 4; ++c) e[j][c] = 4 * ch + c < s1 - s0 ? es[c] : 0.0f;
       }
+      float gs[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        float v = __fmul_rn(e[0][c], r[0]);
+#pragma unroll
+        for (int j = 1; j < ALPHA; ++j) v = fmaxf(v, __fmul_rn(e[j][c], r[j]));
+        gs[c] = v;
+        const int p = 4 * ch + c;
+        if (cut && p < s1 - s0) {
+          const unsigned long long key = key_of(__float_as_uint(v), s0 + p, len, force);
+          atomicAdd(&s.hist[min(max((int)(key >> 52) - base0, 0), NB - 1)], 1u);
+        }
+      }
+      const float4 o = make_float4(gs[0], gs[1], gs[2], gs[3]);
+      reinterpret_cast<float4*>(s.seg)[ch] = o;
+      reinterpret_cast<float4*>(gso)[ch] = o;
     }
-    const float4 o = make_float4(gs[0], gs[1], gs[2], gs[3]);
-    reinterpret_cast<float4*>(s.seg)[ch] = o;
-    reinterpret_cast<float4*>(gso)[ch] = o;
   }
   {  // zero-fill group_score [roundup4(len), Smax)
     float4* gz = reinterpret_cast<float4*>(group_score + (size_t)bg * Smax);

@@ -4,7 +4,7 @@ Step: spc_score (LOGITS, NORM, GROUP) -> spc_topk (force the
 newest token, R10) -> spc_elastic_diff against the previous step's selection
  -> [SLOTS mode: spc_gather_kv of the new rows into budget slots] ->
 spc_sparse_decode_attn over all L layers (one launch).  In INDEXED mode with
-Smax <= 131072 the NORM..diff calls are the single fused spc_select launch.
+Smax <= 135168 the NORM..diff calls are the single fused spc_select launch.
 
 The step state (previous selection, slot map) ping-pongs between two buffers,
 so two CUDA graphs (even / odd step) replay the whole step with one launch
@@ -30,8 +30,8 @@ class DecodeStep:
         k_src_layers/v_src_layers the full caches, device or mapped host)."""
         self.dev = kr.device
         # fused spc_select (one launch for NORM..diff) where it applies: INDEXED mode and
-        # Smax <= 131072, a multiple of 4; otherwise the separate ABI calls
-        self.fused = (mode == "indexed" and kr.shape[2] <= 131072 and kr.shape[2] % 4 == 0) \
+        # Smax <= 135168, a multiple of 4; otherwise the separate ABI calls
+        self.fused = (mode == "indexed" and kr.shape[2] <= 135168 and kr.shape[2] % 4 == 0) \
             if fused is None else fused
         self.B, self.G, self.Smax, self.D = kr.shape
         self.L, self.Hq, self.k = L, Hq, k

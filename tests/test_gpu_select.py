@@ -324,7 +324,7 @@ def test_fused_select_adversarial(oracle, kind, alpha, G, S, k, lens):
 
 def test_fused_select_rejects_unsupported():
     B, G, Hq, k = 1, 1, 4, 64
-    for S in (131076, 1001):  # beyond 8 * 16384 tokens; not a multiple of 4
+    for S in (135172, 1001):  # beyond 8 * 16896 tokens; not a multiple of 4
         lg = torch.zeros((B, Hq, S), device=DEV)
         z = lambda *s, dt=torch.int32: torch.zeros(s, dtype=dt, device=DEV)  # noqa: E731
         with pytest.raises(spc.SpcError):
