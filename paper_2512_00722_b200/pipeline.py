@@ -90,12 +90,16 @@ class DecodeStep:
         self.kr, self.k_tab, self.v_tab, _ = self.sets[i]
 
     # ------------------------------------------------------------------ eager
-    def enqueue(self, parity: int, stream=None):
-        """Enqueue one step writing the selection into idx[parity] (prev = idx[1-parity])."""
+    def enqueue(self, parity: int, stream=None, q_ret=None, q_llm=None):
+        """Enqueue one step writing the selection into idx[parity] (prev = idx[1-parity]).
+        q_ret / q_llm: read the step's queries in place from these tensors instead of the
+        step's own input buffers."""
         cur, prev = parity, 1 - parity
+        q_ret = self.q_ret if q_ret is None else q_ret
+        q_llm = self.q_llm if q_llm is None else q_llm
         if self.fused:
             # LOGITS, then NORM + GROUP + top-k + diff in one cluster launch (spc_select)
-            spc.score(self.q_ret, self.kr, self.seq_len, self.G, self.scale, self.logits,
+            spc.score(q_ret, self.kr, self.seq_len, self.G, self.scale, self.logits,
                       self.head_max, self.head_sumfix, self.gs, self.ws_score,
                       phases=spc.SCORE_LOGITS, stream=stream)
             spc.select(self.logits, self.head_max, self.seq_len, self.G, self.k,
@@ -103,7 +107,7 @@ class DecodeStep:
                        self.cnt[prev], self.load_tok, self.n_load, force_last=self.force_last,
                        stream=stream)
         else:
-            spc.score(self.q_ret, self.kr, self.seq_len, self.G, self.scale, self.logits,
+            spc.score(q_ret, self.kr, self.seq_len, self.G, self.scale, self.logits,
                       self.head_max, self.head_sumfix, self.gs, self.ws_score, stream=stream)
             spc.topk(self.gs, self.seq_len, self.k, self.idx[cur], self.cnt[cur], self.ws_topk,
                      force_last=self.force_last, stream=stream)
@@ -116,11 +120,11 @@ class DecodeStep:
                           self.k_tab, self.v_tab,
                           dtype=spc.BF16 if self.kv_dtype == torch.bfloat16 else spc.F32,
                           stream=stream)
-            spc.sparse_decode_attn(self.q_llm, self.k_tab, self.v_tab, spc.KV_SLOTS, None,
+            spc.sparse_decode_attn(q_llm, self.k_tab, self.v_tab, spc.KV_SLOTS, None,
                                    self.cnt[cur], self.k, self.k, self.scale, self.out, self.lse,
                                    self.ws_attn, self.G, stream=stream)
         else:
-            spc.sparse_decode_attn(self.q_llm, self.k_tab, self.v_tab, spc.KV_INDEXED,
+            spc.sparse_decode_attn(q_llm, self.k_tab, self.v_tab, spc.KV_INDEXED,
                                    self.idx[cur], self.cnt[cur], self.rows, self.k, self.scale,
                                    self.out, self.lse, self.ws_attn, self.G, stream=stream)
 
@@ -157,6 +161,25 @@ class DecodeStep:
                     self.graphs[(si, p)] = g
         torch.cuda.current_stream().wait_stream(s)
         self.use_set(keep)
+
+    def capture_sequence(self, items):
+        """One CUDA graph per step of a fixed input sequence: items[i] = (input set, q_ret,
+        q_llm); step i runs with parity i % 2 (call reset_state() before replaying from step
+        0).  The kernels read each step's queries in place: no staging copies."""
+        graphs = []
+        keep = self.cur_set
+        s = torch.cuda.Stream(device=self.dev)
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            for i, (si, qr, ql) in enumerate(items):
+                self.use_set(si)
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=s):
+                    self.enqueue(i % 2, q_ret=qr, q_llm=ql)
+                graphs.append(g)
+        torch.cuda.current_stream().wait_stream(s)
+        self.use_set(keep)
+        return graphs
 
     def reset_state(self):
         for c in self.cnt:
