@@ -99,9 +99,20 @@ __device__ __forceinline__ float spc_exp_dev(float x) {
 }
 
 // trunc(e * 2^40) as int64 for 0 <= e <= 1 (e * 2^40 is exact in fp32).
+#ifdef SPC_FIXPOINT_INT
+// from the bits: (1.mantissa) * 2^(E - 127 - 23 + 40), shifted with truncation (ALU pipe)
+__device__ __forceinline__ long long fixpoint40(float e) {
+  const uint32_t u = __float_as_uint(e);
+  const int sh = (int)(u >> 23) - 110;
+  const unsigned long long m = (unsigned long long)((u & 0x7FFFFFu) | 0x800000u);
+  const unsigned long long v = sh >= 0 ? m << sh : (sh > -64 ? m >> -sh : 0ull);
+  return u == 0u ? 0ll : (long long)v;
+}
+#else
 __device__ __forceinline__ long long fixpoint40(float e) {
   return __float2ll_rz(__fmul_rn(e, 1099511627776.0f));
 }
+#endif
 
 // Packed (f32x2) IEEE-RN arithmetic, per element identical to the scalar RN ops.
 __device__ __forceinline__ unsigned long long f2_pack(float a, float b) {

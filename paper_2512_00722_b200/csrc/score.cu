@@ -5,16 +5,18 @@
 // the weights (MQA P:331).
 //
 // Three kernels (phases), each HBM- or L2-streaming:
-//   LOGITS  streams the bf16 key cache once (the dominant bytes).  TMA 3-D tile
-//           loads (256 rows x 64 d, 128B swizzle, one mbarrier per d-chunk) into
-//           shared memory; one thread owns 4 key rows and runs alpha sequential
-//           fp32 FMA chains per row (bit-exact O1), two rows at a time with the
-//           packed sm_100 FFMA2 (fma.rn.f32x2: per-lane IEEE fma, order kept).
-//           The key row feeds all alpha query heads of its group (no repeat_kv).
-//   NORM    exp + exact int64 fixed-point sums (O3, O4), L2-resident logits.
+//   LOGITS  streams the bf16 key cache once (the dominant bytes): persistent CTAs,
+//           per-warp cp.async rings into padded shared rows; one lane owns 4 key
+//           rows and runs alpha sequential fp32 FMA chains per row (bit-exact O1),
+//           two rows at a time with the packed sm_100 FFMA2 (fma.rn.f32x2: per-lane
+//           IEEE fma, order kept).  The key row feeds all alpha query heads of its
+//           group (no repeat_kv).  See logits.cuh.
+//   NORM    exp + exact int64 fixed-point sums (O3, O4): grid-wide float4 streaming,
+//           per-CTA partials added with 64-bit atomics (exact, order-free).
 //   GROUP   weights and group max (O5, O6).
-// Per-tile partial max / sums go to the workspace; the last CTA of each group
-// reduces them (order-free: max and integer add), so results are deterministic.
+// Partial maxima / sums go to the workspace; the last CTA of each group or head
+// (ticket) publishes them (order-free: max and integer add), so results are
+// deterministic and the workspace is left zero-filled.
 #include <cooperative_groups.h>
 
 #include "common.cuh"
@@ -37,44 +39,57 @@ constexpr int GRP_TILE = GRP_THREADS * GRP_PER;
 #include "logits.cuh"
 
 // ---------------------------------------------------------------- NORM (O3, O4)
-// One thread-block cluster of NM_CL CTAs per head: each CTA sums its quarter of
-// the (L2-resident) logits row, the partial int64 sums meet in CTA 0 through
-// distributed shared memory (integer addition: exact, order-free).
-constexpr int NM_CL = 4;
-constexpr int NM_T = 512;
-__global__ void __cluster_dims__(NM_CL, 1, 1) __launch_bounds__(NM_T) norm_kernel(
+// Grid (blocks per head, B*Hq).  Each thread streams float4 chunks of its head's row
+// (two chunks in flight), exp as f32x2 pairs; the CTA's int64 partial is added to the
+// head's workspace accumulator with a 64-bit atomic (integer addition: exact, order-
+// free); the last CTA of the head (ticket) publishes head_sumfix and re-zeroes it.
+constexpr int NM_T = 256;
+template <bool VEC>
+__global__ void __launch_bounds__(NM_T) norm_kernel(
     const float* __restrict__ logits, const float* __restrict__ head_max,
-    const int32_t* __restrict__ seq_len, int Hq, int Smax, int64_t* __restrict__ head_sumfix) {
+    const int32_t* __restrict__ seq_len, int Hq, int Smax, unsigned long long* __restrict__ acc_ws,
+    unsigned* __restrict__ tickets, int64_t* __restrict__ head_sumfix) {
   spc_pdl_entry();
   __shared__ long long red[NM_T / 32];
-  __shared__ long long part;
-  cg::cluster_group cl = cg::this_cluster();
-  const int rank = (int)cl.block_rank();
+  __shared__ int flag;
   const int bh = blockIdx.y, b = bh / Hq;
-  const int S = seq_len[b];
+  const int S = min(max(seq_len[b], 0), Smax);
   const float m = head_max[bh];
   const float* row = logits + (size_t)bh * Smax;
-  const int per = (S + NM_CL - 1) / NM_CL;
-  const int s0 = min(S, rank * per), s1 = min(S, s0 + per);
   long long acc = 0;
-#pragma unroll 4
-  for (int t = s0 + threadIdx.x; t < s1; t += NM_T)
-    acc += fixpoint40(spc_exp_dev(__fsub_rn(__ldcg(row + t), m)));
+  if (VEC) {
+    const int nch = S >> 2;  // whole float4 chunks; the tail is done below
+    const float4* r4 = reinterpret_cast<const float4*>(row);
+    const int stride = gridDim.x * NM_T;
+    for (int c = blockIdx.x * NM_T + threadIdx.x; c < nch; c += 2 * stride) {
+      const float4 x0 = __ldcg(r4 + c);
+      const float4 x1 = c + stride < nch ? __ldcg(r4 + c + stride) : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+      const float2 a0 = spc_exp2_dev(__fsub_rn(x0.x, m), __fsub_rn(x0.y, m));
+      const float2 a1 = spc_exp2_dev(__fsub_rn(x0.z, m), __fsub_rn(x0.w, m));
+      const float2 b0 = spc_exp2_dev(__fsub_rn(x1.x, m), __fsub_rn(x1.y, m));
+      const float2 b1 = spc_exp2_dev(__fsub_rn(x1.z, m), __fsub_rn(x1.w, m));
+      acc += fixpoint40(a0.x) + fixpoint40(a0.y) + fixpoint40(a1.x) + fixpoint40(a1.y) +
+             fixpoint40(b0.x) + fixpoint40(b0.y) + fixpoint40(b1.x) + fixpoint40(b1.y);
+    }
+    if (blockIdx.x == 0)
+      for (int t = (nch << 2) + threadIdx.x; t < S; t += NM_T)
+        acc += fixpoint40(spc_exp_dev(__fsub_rn(__ldcg(row + t), m)));
+  } else {
+    for (int t = blockIdx.x * NM_T + threadIdx.x; t < S; t += gridDim.x * NM_T)
+      acc += fixpoint40(spc_exp_dev(__fsub_rn(__ldcg(row + t), m)));
+  }
   acc = warp_sum_ll(acc);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
   __syncthreads();
   if (threadIdx.x == 0) {
-    long long s = 0;
-    for (int w = 0; w < NM_T / 32; ++w) s += red[w];
-    part = s;
+    long long sum = 0;
+    for (int w = 0; w < NM_T / 32; ++w) sum += red[w];
+    if (sum) atomicAdd(acc_ws + bh, (unsigned long long)sum);
   }
-  cl.sync();
-  if (rank == 0 && threadIdx.x == 0) {
-    long long s = 0;
-    for (int r = 0; r < NM_CL; ++r) s += *cl.map_shared_rank(&part, r);
-    head_sumfix[bh] = s;
+  if (last_block_ticket(&tickets[bh], gridDim.x, &flag) && threadIdx.x == 0) {
+    head_sumfix[bh] = (int64_t)__ldcg(acc_ws + bh);
+    acc_ws[bh] = 0ull;
   }
-  cl.sync();  // remote reads of `part` done before any CTA exits
 }
 
 // ------------------------------------------------------------- GROUP (O4..O6)
@@ -99,18 +114,21 @@ __global__ void __launch_bounds__(GRP_THREADS) group_kernel(
   float* out = group_score + (size_t)bg * Smax;
   const int t0 = blockIdx.x * GRP_TILE + threadIdx.x;
 #pragma unroll
-  for (int i = 0; i < GRP_PER; ++i) {
-    const int t = t0 + i * GRP_THREADS;
-    if (t >= Smax) break;
-    float gs = 0.0f;
-    if (t < S) {
+  for (int i = 0; i < GRP_PER; i += 2) {  // tokens t and t + GRP_THREADS as an f32x2 pair
+    const int ta = t0 + i * GRP_THREADS, tb = ta + GRP_THREADS;
+    if (ta >= Smax) break;
+    float ga = 0.0f, gb = 0.0f;
 #pragma unroll
-      for (int j = 0; j < ALPHA; ++j) {
-        const float p = __fmul_rn(spc_exp_dev(__fsub_rn(__ldcg(lg + (size_t)j * Smax + t), m[j])), r[j]);
-        gs = j ? fmaxf(gs, p) : p;
-      }
+    for (int j = 0; j < ALPHA; ++j) {
+      const float xa = ta < S ? __ldcg(lg + (size_t)j * Smax + ta) : m[j];
+      const float xb = tb < S ? __ldcg(lg + (size_t)j * Smax + tb) : m[j];
+      const float2 e = spc_exp2_dev(__fsub_rn(xa, m[j]), __fsub_rn(xb, m[j]));
+      const float pa = __fmul_rn(e.x, r[j]), pb = __fmul_rn(e.y, r[j]);
+      ga = j ? fmaxf(ga, pa) : pa;
+      gb = j ? fmaxf(gb, pb) : pb;
     }
-    out[t] = gs;
+    out[ta] = ta < S ? ga : 0.0f;
+    if (tb < Smax) out[tb] = tb < S ? gb : 0.0f;
   }
 }
 
@@ -210,8 +228,16 @@ extern "C" int spc_score(int dtype, const void* q, const void* kr, const int32_t
 #undef LG
   }
   if (phases & SPC_SCORE_NORM) {
-    (void)launch_k(norm_kernel, dim3(dim3(NM_CL, B * Hq)), dim3(NM_T), 0, st, logits, head_max, seq_len, Hq, Smax,
-                                                      head_sumfix);
+    // enough CTAs per head to fill the GPU twice, each with >= 8 float4 chunks per thread
+    const int want = (2 * num_sms() + B * Hq - 1) / (B * Hq);
+    const int cap = (Smax + 8 * 4 * NM_T - 1) / (8 * 4 * NM_T);
+    const int nb = max(1, min(want, cap));
+    if (Smax % 4 == 0)
+      (void)launch_k(norm_kernel<true>, dim3(nb, B * Hq), dim3(NM_T), 0, st, logits, head_max,
+                     seq_len, Hq, Smax, (unsigned long long*)w.tile_sum, w.cnt2, head_sumfix);
+    else
+      (void)launch_k(norm_kernel<false>, dim3(nb, B * Hq), dim3(NM_T), 0, st, logits, head_max,
+                     seq_len, Hq, Smax, (unsigned long long*)w.tile_sum, w.cnt2, head_sumfix);
     SPC_TRY(launched());
   }
   if (phases & SPC_SCORE_GROUP) {
