@@ -27,7 +27,10 @@
 #endif
 constexpr int LG_RPT = SPC_LG_RPT;        // rows per lane (LG_RPT / 2 FFMA2 row pairs)
 constexpr int LG_TR = 32 * LG_RPT;        // rows per tile
-constexpr int LG_DCH = 64;                // d per pipeline step
+#ifndef SPC_LG_DCH
+#define SPC_LG_DCH 64
+#endif
+constexpr int LG_DCH = SPC_LG_DCH;        // d per pipeline step
 constexpr int LG_RS = LG_DCH * 2 + 16;    // padded shared row: 144 B (conflict-free LDS.128)
 constexpr int LG_STAGE = LG_TR * LG_RS;   // 18 KiB at 4 rows per lane
 constexpr int LG_NST = 2;                 // per-warp ring depth: one step loads while one computes

@@ -134,3 +134,12 @@ def test_exp_sweep_through_fused_select(oracle):
     torch.cuda.synchronize()
     assert np.array_equal(F.cpu().numpy(), oF)
     assert np.array_equal(gs.cpu().numpy().view(np.uint32), ogs.view(np.uint32))
+
+
+@pytest.mark.parametrize("Smax,lens", [(1001, [1001, 3, 999]), (20001, [20001, 7777, 1])])
+def test_score_smax_not_multiple_of_4(oracle, Smax, lens):
+    """NORM's scalar path (rows not float4-aligned), single- and multi-block per head."""
+    B, G, alpha, D = len(lens), 2, 4, 128
+    kr = synth.retrieval_keys(B, G, Smax, D, seed=Smax)
+    q = synth.retrieval_queries(1, B, alpha * G, G, D, seed=Smax)[0]
+    check(oracle, q, kr, lens, G, f32(1 / math.sqrt(D)))
