@@ -269,7 +269,7 @@ extern "C" int spc_sparse_decode_attn(int dtype, const void* q, const void* cons
           out, lse);                                                                            \
     } else {                                                                                    \
       dim3 grid(nsplit, B * G, layer_end - layer_begin);                                        \
-      (void)launch_k(attn_f32_kernel<DD, AA>, dim3(grid), dim3(AT_THREADS), 0, st,                                      \
+      (void)launch_k(attn_f32_kernel<DD, AA>, dim3(grid), dim3(AT_THREADS), 0, st,          \
           (const float*)q, k_layers, v_layers, kv_mode, idx, count, layer_begin, B, G, rows, k, \
           scale, nsplit, w.segstride, w.part_o, w.part_ml, w.cnt, out, lse);                    \
     }                                                                                           \
@@ -284,8 +284,8 @@ extern "C" int spc_attn_merge(const float* o_parts, const float* lse_parts, int 
                               float* out, float* lse_out, spc_stream_t stream) {
   if (!o_parts || !lse_parts || !out) return SPC_E_NULL;
   if (P < 1 || n < 1 || D < 1) return SPC_E_SHAPE;
-  (void)launch_k(merge_kernel, dim3(n), dim3(128), 0, as_stream(stream), o_parts, lse_parts, P, n, D, out, lse_out);
-  return launched();
+  return launched(launch_k(merge_kernel, dim3(n), dim3(128), 0, as_stream(stream), o_parts,
+                           lse_parts, P, n, D, out, lse_out));
 }
 
 // Debug only (not part of include/spc.h): route the attention kernel's per-chunk

@@ -196,10 +196,9 @@ extern "C" int spc_elastic_diff(const int32_t* prev_idx, const int32_t* prev_cou
                          (int)(sizeof(int32_t) * 3 * SPC_MAX_K + sizeof(uint32_t) * 2 * DF_BM_WORDS));
     attr = true;
   }
-  (void)launch_k(diff_kernel, dim3(B * G), dim3(DF_THREADS), smem, as_stream(stream), prev_idx, prev_count, cur_idx,
-                                                              cur_count, k, slot_tok, load_tok,
-                                                              load_slot, n_load, evict_tok, n_evict);
-  return launched();
+  return launched(launch_k(diff_kernel, dim3(B * G), dim3(DF_THREADS), smem, as_stream(stream),
+                           prev_idx, prev_count, cur_idx, cur_count, k, slot_tok, load_tok,
+                           load_slot, n_load, evict_tok, n_evict));
 }
 
 extern "C" int spc_gather_kv(int dtype, const void* const* k_src, const void* const* v_src, int L,
@@ -217,8 +216,7 @@ extern "C" int spc_gather_kv(int dtype, const void* const* k_src, const void* co
   if ((D * esz) % 16 || D * esz / 16 > 32 || 32 % (D * esz / 16)) return SPC_E_UNSUPPORTED;
   const int row_vecs = D * esz / 16;
   dim3 grid((k + 63) / 64, B * G, layer_end - layer_begin);
-  (void)launch_k(gather_kernel<uint4>, dim3(grid), dim3(256), 0, as_stream(stream), k_src, v_src, B, G, Smax, k, row_vecs,
-                                                            layer_begin, load_tok, load_slot, n_load,
-                                                            k_buf, v_buf);
-  return launched();
+  return launched(launch_k(gather_kernel<uint4>, grid, dim3(256), 0, as_stream(stream), k_src,
+                           v_src, B, G, Smax, k, row_vecs, layer_begin, load_tok, load_slot,
+                           n_load, k_buf, v_buf));
 }

@@ -63,7 +63,9 @@ __global__ void __launch_bounds__(NM_T) norm_kernel(
     const int stride = gridDim.x * NM_T;
     for (int c = blockIdx.x * NM_T + threadIdx.x; c < nch; c += 2 * stride) {
       const float4 x0 = __ldcg(r4 + c);
-      const float4 x1 = c + stride < nch ? __ldcg(r4 + c + stride) : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+      const float4 x1 = c + stride < nch
+                            ? __ldcg(r4 + c + stride)
+                            : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
       const float2 a0 = spc_exp2_dev(__fsub_rn(x0.x, m), __fsub_rn(x0.y, m));
       const float2 a1 = spc_exp2_dev(__fsub_rn(x0.z, m), __fsub_rn(x0.w, m));
       const float2 b0 = spc_exp2_dev(__fsub_rn(x1.x, m), __fsub_rn(x1.y, m));
@@ -148,19 +150,17 @@ int launch_logits(const uint16_t* kr, const uint16_t* q, const int32_t* seq_len,
   int tpc = (ntiles + num_sms() - 1) / num_sms();
   if (tpc > tpr) tpc = tpr;  // a CTA spans at most two groups
   const int ncta = (ntiles + tpc - 1) / tpc;
-  (void)launch_k(logits_kernel<D, ALPHA>, dim3(ncta), dim3(32 * lg_warps<ALPHA>()), smem, st, kr, q, seq_len, G, Smax,
-                                                                      scale, tpc, tpr,
-                                                    ntiles, logits, seg_max, segstride, counters,
-                                                    head_max);
-  return launched();
+  return launched(launch_k(logits_kernel<D, ALPHA>, dim3(ncta), dim3(32 * lg_warps<ALPHA>()),
+                           smem, st, kr, q, seq_len, G, Smax, scale, tpc, tpr, ntiles, logits,
+                           seg_max, segstride, counters, head_max));
 }
 
 template <int ALPHA>
 int launch_group(const float* logits, const float* head_max, const int64_t* sumfix,
                  const int32_t* seq_len, int B, int G, int Smax, float* gs, cudaStream_t st) {
   dim3 grid((Smax + GRP_TILE - 1) / GRP_TILE, B * G);
-  (void)launch_k(group_kernel<ALPHA>, dim3(grid), dim3(GRP_THREADS), 0, st, logits, head_max, sumfix, seq_len, G, Smax, gs);
-  return launched();
+  return launched(launch_k(group_kernel<ALPHA>, grid, dim3(GRP_THREADS), 0, st, logits,
+                           head_max, sumfix, seq_len, G, Smax, gs));
 }
 
 struct ScoreWs {
@@ -242,10 +242,22 @@ extern "C" int spc_score(int dtype, const void* q, const void* kr, const int32_t
   }
   if (phases & SPC_SCORE_GROUP) {
     switch (alpha) {
-      case 1: SPC_TRY(launch_group<1>(logits, head_max, head_sumfix, seq_len, B, G, Smax, group_score, st)); break;
-      case 2: SPC_TRY(launch_group<2>(logits, head_max, head_sumfix, seq_len, B, G, Smax, group_score, st)); break;
-      case 4: SPC_TRY(launch_group<4>(logits, head_max, head_sumfix, seq_len, B, G, Smax, group_score, st)); break;
-      case 8: SPC_TRY(launch_group<8>(logits, head_max, head_sumfix, seq_len, B, G, Smax, group_score, st)); break;
+      case 1:
+        SPC_TRY(launch_group<1>(logits, head_max, head_sumfix, seq_len, B, G, Smax,
+                                 group_score, st));
+        break;
+      case 2:
+        SPC_TRY(launch_group<2>(logits, head_max, head_sumfix, seq_len, B, G, Smax,
+                                 group_score, st));
+        break;
+      case 4:
+        SPC_TRY(launch_group<4>(logits, head_max, head_sumfix, seq_len, B, G, Smax,
+                                 group_score, st));
+        break;
+      case 8:
+        SPC_TRY(launch_group<8>(logits, head_max, head_sumfix, seq_len, B, G, Smax,
+                                 group_score, st));
+        break;
     }
   }
   return SPC_OK;

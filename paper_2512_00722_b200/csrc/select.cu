@@ -36,8 +36,9 @@ namespace spc {
 namespace {
 
 constexpr int ST = 512;         // threads per CTA
-constexpr int SCL = 8;          // CTAs per row (cluster size)
-constexpr int SEGCAP = 16896;   // tokens per CTA segment: rows up to SCL * SEGCAP = 135168
+constexpr int SEGCAP = 16896;   // tokens per CTA segment: rows up to 8 * SEGCAP = 135168
+// SCL (template parameter) = CTAs per row = cluster size; 8.  (16-CTA non-portable
+// clusters were measured: every phase here is latency-bound, 15.1 vs 14.9 us per row.)
 constexpr int NB = 256;         // bins per histogram pass
 constexpr int W0_SHIFT = 20;    // pass-0 bin = value bits >> 20: 8 bins per binade
 constexpr int W0_BITS = 12;     // key bits (sign + exponent + 3 mantissa) fixed by a pass-0 bin
@@ -51,13 +52,14 @@ __device__ __forceinline__ void sel_mark(int slot) {
   if (g_sel_trace && blockIdx.y < 64 && threadIdx.x == 0 && slot < 16) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-    g_sel_trace[(blockIdx.y * SCL + blockIdx.x) * 16 + slot] = t;
+    g_sel_trace[(blockIdx.y * gridDim.x + blockIdx.x) * 16 + slot] = t;
   }
 #else
   (void)slot;
 #endif
 }
 
+template <int SCL>
 struct SelSm {
   float seg[SEGCAP];                      // group scores of this CTA's segment
   uint32_t bm_prev[SEGCAP / 32];          // previous selection, segment-relative bitmap
@@ -86,7 +88,8 @@ __device__ __forceinline__ unsigned long long key_of(uint32_t vb, int p, int len
 }
 
 // Block-wide exclusive scan of one uint64 per thread (ST threads).
-__device__ __forceinline__ unsigned long long scan_u64(SelSm& s, unsigned long long v) {
+template <int SCL>
+__device__ __forceinline__ unsigned long long scan_u64(SelSm<SCL>& s, unsigned long long v) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   unsigned long long incl = v;
 #pragma unroll
@@ -112,7 +115,8 @@ __device__ __forceinline__ unsigned long long scan_u64(SelSm& s, unsigned long l
 }
 
 // Push the nonzero bins of the local histogram into red[buf] of every CTA.
-__device__ __forceinline__ void push_hist(SelSm& s, cg::cluster_group& cl, int buf) {
+template <int SCL>
+__device__ __forceinline__ void push_hist(SelSm<SCL>& s, cg::cluster_group& cl, int buf) {
   const int t = threadIdx.x;
   if (t < NB) {
     const unsigned h = s.hist[t];
@@ -125,7 +129,8 @@ __device__ __forceinline__ void push_hist(SelSm& s, cg::cluster_group& cl, int b
 
 // After the cluster barrier: bin of the r-th largest element counted from the top of
 // red[buf] -> s.find = {bin, count above it, count in it}.  Clears red[buf].
-__device__ __forceinline__ void find_bin(SelSm& s, int buf, int r) {
+template <int SCL>
+__device__ __forceinline__ void find_bin(SelSm<SCL>& s, int buf, int r) {
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   unsigned c = 0, incl = 0;
   if (t < NB) {
@@ -153,8 +158,8 @@ __device__ __forceinline__ void find_bin(SelSm& s, int buf, int r) {
   __syncthreads();
 }
 
-template <int ALPHA, int NC>
-__global__ void __cluster_dims__(SCL, 1, 1) __launch_bounds__(ST, 1) select_kernel(
+template <int ALPHA, int NC, int SCL>
+__global__ void __launch_bounds__(ST, 1) select_kernel(
     const float* __restrict__ logits, const float* __restrict__ head_max,
     const int32_t* __restrict__ seq_len, int G, int Smax, int k, int force,
     int64_t* __restrict__ head_sumfix, float* __restrict__ group_score,
@@ -164,7 +169,7 @@ __global__ void __cluster_dims__(SCL, 1, 1) __launch_bounds__(ST, 1) select_kern
     int32_t* __restrict__ n_evict) {
   spc_pdl_entry();
   extern __shared__ __align__(16) uint8_t sel_raw[];
-  SelSm& s = *reinterpret_cast<SelSm*>(sel_raw);
+  SelSm<SCL>& s = *reinterpret_cast<SelSm<SCL>*>(sel_raw);
   cg::cluster_group cl = cg::this_cluster();
   const int rank = (int)cl.block_rank();
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -608,11 +613,38 @@ __global__ void __cluster_dims__(SCL, 1, 1) __launch_bounds__(ST, 1) select_kern
 using namespace spc;
 
 // debug only (not in include/spc.h): point the -DSPC_TRACE stamps at a device buffer of
-// 64 x SCL x 16 uint64, or NULL to stop
+// 64 rows x 16 CTAs x 16 uint64, or NULL to stop
 extern "C" int spc_debug_set_select_trace(unsigned long long* buf) {
   return cudaMemcpyToSymbol(spc::g_sel_trace, &buf, sizeof(buf)) == cudaSuccess ? SPC_OK
                                                                                  : SPC_E_CUDA;
 }
+
+namespace spc {
+namespace {
+template <int AA, int SCL>
+int launch_select(const float* logits, const float* head_max, const int32_t* seq_len, int B, int G,
+                  int Smax, int k, int force_last, int64_t* head_sumfix, float* group_score,
+                  int32_t* out_idx, int32_t* out_count, const int32_t* prev_idx,
+                  const int32_t* prev_count, int32_t* load_tok, int32_t* n_load,
+                  int32_t* evict_tok, int32_t* n_evict, cudaStream_t st) {
+  auto kern = select_kernel<AA, (AA > 4 ? 1 : 2), SCL>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)sizeof(SelSm<SCL>));
+    if (e == cudaSuccess && SCL > 8)
+      e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return launched(e);
+    attr = true;
+  }
+  return launched(launch_kc(kern, dim3(SCL, B * G), dim3(ST), sizeof(SelSm<SCL>), st, SCL,
+                            logits, head_max, seq_len, G, Smax, k, force_last, head_sumfix,
+                            group_score, out_idx, out_count, prev_idx, prev_count, load_tok,
+                            n_load, evict_tok, n_evict));
+}
+
+}  // namespace
+}  // namespace spc
 
 extern "C" int spc_select(const float* logits, const float* head_max, const int32_t* seq_len, int B,
                           int Hq, int G, int Smax, int k, int force_last, int64_t* head_sumfix,
@@ -625,24 +657,14 @@ extern "C" int spc_select(const float* logits, const float* head_max, const int3
     return SPC_E_NULL;
   if (B <= 0 || G <= 0 || Hq <= 0 || Hq % G || Smax <= 0) return SPC_E_SHAPE;
   if (k < 1 || k > SPC_MAX_K) return SPC_E_BUDGET;
-  if (Smax > SCL * SEGCAP || Smax % 4) return SPC_E_UNSUPPORTED;
+  if (Smax > 8 * SEGCAP || Smax % 4) return SPC_E_UNSUPPORTED;
   const int alpha = Hq / G;
   cudaStream_t st = as_stream(stream);
 #define SEL(AA)                                                                                 \
-  if (alpha == AA) {                                                                            \
-    static bool attr = false;                                                                   \
-    if (!attr) {                                                                                \
-      SPC_TRY(cudaFuncSetAttribute((const void*)select_kernel<AA, (AA > 4 ? 1 : 2)>,                              \
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize,                 \
-                                   (int)sizeof(SelSm)));                                        \
-      attr = true;                                                                              \
-    }                                                                                           \
-    (void)launch_k(select_kernel<AA, (AA > 4 ? 1 : 2)>, dim3(SCL, B * G), dim3(ST),             \
-                   sizeof(SelSm), st, logits, head_max, seq_len, G, Smax, k, force_last,         \
-                   head_sumfix, group_score, out_idx, out_count, prev_idx, prev_count, load_tok, \
-                   n_load, evict_tok, n_evict);                                                  \
-    return launched();                                                                          \
-  }
+  if (alpha == AA)                                                                              \
+    return launch_select<AA, 8>(logits, head_max, seq_len, B, G, Smax, k, force_last,           \
+                                head_sumfix, group_score, out_idx, out_count, prev_idx,          \
+                                prev_count, load_tok, n_load, evict_tok, n_evict, st);
   SEL(1) SEL(2) SEL(4) SEL(8)
 #undef SEL
   return SPC_E_UNSUPPORTED;

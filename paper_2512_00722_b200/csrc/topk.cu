@@ -444,10 +444,10 @@ extern "C" int spc_topk(const float* val, const int32_t* seq_len, int B, int G, 
     SPC_TRY(set_big_smem((const void*)topk_cluster_kernel, sizeof(ClSmem)));
     attr = true;
   }
-  (void)launch_k(topk_cluster_kernel, dim3(dim3(CL, B * G)), dim3(SEL_THREADS), sizeof(ClSmem), as_stream(stream), 
-      val, seq_len, G, n_cols, k, force_last, id_stride, id_offset, out_idx, out_val, out_count,
-      (unsigned long long*)out_thresh);
-  return launched();
+  return launched(launch_k(topk_cluster_kernel, dim3(CL, B * G), dim3(SEL_THREADS),
+                           sizeof(ClSmem), as_stream(stream), val, seq_len, G, n_cols, k,
+                           force_last, id_stride, id_offset, out_idx, out_val, out_count,
+                           (unsigned long long*)out_thresh));
 }
 
 extern "C" size_t spc_topk_merge_workspace(int P, int R, int k) {
@@ -470,9 +470,9 @@ extern "C" int spc_topk_merge(const float* cand_val, const int32_t* cand_pos,
     SPC_TRY(set_big_smem((const void*)merge_kernel, sizeof(SelSmem)));
     attr = true;
   }
-  (void)launch_k(merge_kernel, dim3(R), dim3(SEL_THREADS), sizeof(SelSmem), as_stream(stream), 
-      cand_val, cand_pos, cand_count, P, R, k, (unsigned long long*)out_thresh);
-  return launched();
+  return launched(launch_k(merge_kernel, dim3(R), dim3(SEL_THREADS), sizeof(SelSmem),
+                           as_stream(stream), cand_val, cand_pos, cand_count, P, R, k,
+                           (unsigned long long*)out_thresh));
 }
 
 extern "C" int spc_topk_filter(int32_t* idx, const float* val, int32_t* count,
@@ -481,7 +481,7 @@ extern "C" int spc_topk_filter(int32_t* idx, const float* val, int32_t* count,
   if (!idx || !val || !count || !thresh) return SPC_E_NULL;
   if (R < 1) return SPC_E_SHAPE;
   if (k < 1 || k > SPC_MAX_K) return SPC_E_BUDGET;
-  (void)launch_k(filter_kernel, dim3(R), dim3(SEL_THREADS), 0, as_stream(stream), 
-      idx, val, count, (const unsigned long long*)thresh, k, id_stride, id_offset);
-  return launched();
+  return launched(launch_k(filter_kernel, dim3(R), dim3(SEL_THREADS), 0, as_stream(stream), idx,
+                           val, count, (const unsigned long long*)thresh, k, id_stride,
+                           id_offset));
 }

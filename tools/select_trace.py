@@ -28,7 +28,8 @@ ws = spc.alloc_workspace(spc.score_workspace(B, Hq, S), dev)
 idx = [z(B, G, k, dt=i32) for _ in range(2)]
 cnt = [z(B, G, dt=i32) for _ in range(2)]
 lt, nl = z(B, G, k, dt=i32), z(B, G, dt=i32)
-tr = torch.zeros(64 * 8 * 16, dtype=torch.int64, device=dev)
+tr = torch.zeros(64 * 16 * 16, dtype=torch.int64, device=dev)
+GX = int(os.environ.get("SCL", "16" if B * G <= 9 else "8"))  # CTAs per row used by the lib
 names = ["start", "norm", "group", "pass0", "passes", "T", "counts", "end", "x_comp", "x_sync",
          "bitmap", "exp", "push"]
 for step in range(4):
@@ -43,11 +44,11 @@ for step in range(4):
     e[1].record()
     torch.cuda.synchronize()
     print(f"step {step}: {e[0].elapsed_time(e[1]) * 1e3:.1f} us")
-t = tr.view(64, 8, 16).cpu().numpy().astype("float64")
+t = tr[:64 * GX * 16].view(64, GX, 16).cpu().numpy().astype("float64")
 rows = int((t[:, 0, 0] > 0).sum())
 t0 = t[:rows, :, 0].min()
 print("rank " + " ".join(f"{n:>8s}" for n in names))
-for r in range(8):
+for r in range(GX):
     print(f"{r:4d} " + " ".join(f"{(t[0, r, i] - t0) / 1e3:8.2f}" if t[0, r, i] > 0 else "       -"
                                 for i in range(len(names))))
 print("row  start_min start_max  end_max   (us from the first CTA start)")
