@@ -24,7 +24,8 @@ from . import spc
 class DecodeStep:
     def __init__(self, kr: torch.Tensor, k_layers, v_layers, seq_len: torch.Tensor, L: int,
                  Hq: int, k: int, mode: str = "indexed", force_last: bool = True, scale=None,
-                 kv_rows=None, k_src_layers=None, v_src_layers=None, fused=None):
+                 kv_rows=None, k_src_layers=None, v_src_layers=None, fused=None,
+                 src_rows=None):
         """kr: retrieval keys [B][G][Smax][D] bf16.  k_layers/v_layers: L tensors [B][G][rows][D]
         (INDEXED: the full caches; SLOTS: the budget buffers [B][G][k][D], with
         k_src_layers/v_src_layers the full caches, device or mapped host)."""
@@ -52,7 +53,7 @@ class DecodeStep:
             # pinned host tensors are device-addressable under UVA (zero-copy PCIe reads)
             self.k_src_tab = spc.ptr_table(self.k_src, self.dev)
             self.v_src_tab = spc.ptr_table(self.v_src, self.dev)
-            self.src_rows = self.k_src[0].shape[2]
+            self.src_rows = src_rows if src_rows is not None else self.k_src[0].shape[2]
         B, G, Hq, D, dev = self.B, self.G, Hq, self.D, self.dev
         f32, i32 = torch.float32, torch.int32
         self.q_ret = torch.zeros((B, Hq, D), dtype=torch.bfloat16, device=dev)
