@@ -172,8 +172,24 @@ __device__ void narrow_by_row_scan(SelSmem& s, const KeyFn& key, int len, unsign
 struct DenseKey {
   const float* row;
   int len, force, stride, offset;
+  bool vec;  // row 16-byte aligned: quad() reads one float4 (p is a multiple of 4)
   __device__ unsigned long long operator()(int p) const {
     return row_key(row, p, len, force, stride, offset);
+  }
+  // keys of positions p .. p+3 (p a multiple of 4; positions >= len are never used)
+  __device__ __forceinline__ void quad(int p, unsigned long long (&x)[4]) const {
+    if (vec) {
+      const float4 v = __ldg(reinterpret_cast<const float4*>(row + p));
+      const float vs[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const uint32_t vb = (force && p + i == len - 1) ? 0x7F800000u : __float_as_uint(vs[i]);
+        x[i] = composite(vb, (p + i) * stride + offset);
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) x[i] = p + i < len ? row_key(row, p + i, len, force, stride, offset) : 0ull;
+    }
   }
 };
 
@@ -202,7 +218,13 @@ __device__ void cluster_select(ClSmem& s, cg::cluster_group& cl, const KeyFn& ke
     // ---- 1. top-11-bit histogram, reduced over the cluster
     for (int i = tid; i < NBIN0; i += SEL_THREADS) s.hist[i] = 0;
     __syncthreads();
-    for (int p = s0 + tid; p < s1; p += SEL_THREADS) atomicAdd(&s.hist[key(p) >> 53], 1u);
+    for (int p = s0 + 4 * tid; p < s1; p += 4 * SEL_THREADS) {
+      unsigned long long x[4];
+      key.quad(p, x);
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        if (p + i < s1) atomicAdd(&s.hist[x[i] >> 53], 1u);
+    }
     cl.sync();
     for (int i = tid; i < NBIN0; i += SEL_THREADS) {
       unsigned t = 0;
@@ -223,9 +245,13 @@ __device__ void cluster_select(ClSmem& s, cg::cluster_group& cl, const KeyFn& ke
       const unsigned mask = (1u << db) - 1;
       for (int i = tid; i < 256; i += SEL_THREADS) s.hist[i] = 0;
       __syncthreads();
-      for (int p = s0 + tid; p < s1; p += SEL_THREADS) {
-        const unsigned long long x = key(p);
-        if (prefix_match(x, prefix, bits)) atomicAdd(&s.hist[(unsigned)(x >> shift) & mask], 1u);
+      for (int p = s0 + 4 * tid; p < s1; p += 4 * SEL_THREADS) {
+        unsigned long long x[4];
+        key.quad(p, x);
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          if (p + i < s1 && prefix_match(x[i], prefix, bits))
+            atomicAdd(&s.hist[(unsigned)(x[i] >> shift) & mask], 1u);
       }
       cl.sync();
       for (int i = tid; i < 256; i += SEL_THREADS) {
@@ -248,17 +274,21 @@ __device__ void cluster_select(ClSmem& s, cg::cluster_group& cl, const KeyFn& ke
     cl.sync();
     int* n0 = cl.map_shared_rank(&s.sel.n[0], 0);
     unsigned long long* c0 = cl.map_shared_rank(&s.sel.cand[0][0], 0);
-    for (int p0 = s0; p0 < s1; p0 += SEL_THREADS) {
-      const int p = p0 + tid;
-      unsigned long long x = 0;
-      const bool hit = p < s1 && prefix_match(x = key(p), prefix, bits);
-      const unsigned m = __ballot_sync(0xffffffffu, hit);
-      if (!m) continue;
-      const int leader = __ffs(m) - 1;
-      int base = 0;
-      if (lane == leader) base = atomicAdd(n0, __popc(m));
-      base = __shfl_sync(0xffffffffu, base, leader);
-      if (hit) c0[base + __popc(m & ((1u << lane) - 1))] = x;
+    for (int p0 = s0; p0 < s1; p0 += 4 * SEL_THREADS) {
+      const int p = p0 + 4 * tid;
+      unsigned long long x[4] = {0, 0, 0, 0};
+      if (p < s1) key.quad(p, x);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const bool hit = p + i < s1 && prefix_match(x[i], prefix, bits);
+        const unsigned m = __ballot_sync(0xffffffffu, hit);
+        if (!m) continue;
+        const int leader = __ffs(m) - 1;
+        int base = 0;
+        if (lane == leader) base = atomicAdd(n0, __popc(m));
+        base = __shfl_sync(0xffffffffu, base, leader);
+        if (hit) c0[base + __popc(m & ((1u << lane) - 1))] = x[i];
+      }
     }
     cl.sync();
     if (rank == 0) {
@@ -270,10 +300,15 @@ __device__ void cluster_select(ClSmem& s, cg::cluster_group& cl, const KeyFn& ke
   }
   // ---- 4. ordered compaction over the cluster
   const int seg = s1 - s0;
-  const int pt = (seg + SEL_THREADS - 1) / SEL_THREADS;
-  const int q0 = s0 + tid * pt, q1 = min(s1, q0 + pt);
+  const int pt = ((seg + SEL_THREADS - 1) / SEL_THREADS + 3) & ~3;  // multiple of 4
+  const int q0 = min(s1, s0 + tid * pt), q1 = min(s1, q0 + pt);
   int cnt = 0;
-  for (int p = q0; p < q1; ++p) cnt += key(p) >= T;
+  for (int p = q0; p < q1; p += 4) {
+    unsigned long long x[4];
+    key.quad(p, x);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) cnt += (p + i < q1 && x[i] >= T);
+  }
   int pos = block_excl_scan(cnt, s.sel.wsum, &s.total);
   __syncthreads();
   if (tid < CL) cl.map_shared_rank(s.counts, tid)[rank] = s.total;
@@ -287,13 +322,16 @@ __device__ void cluster_select(ClSmem& s, cg::cluster_group& cl, const KeyFn& ke
   *my_base = base;
   *my_count = s.counts[rank];
   pos += base;
-  for (int p = q0; p < q1; ++p) {
-    const unsigned long long x = key(p);
-    if (x >= T) {
-      oi[pos] = p;
-      if (ov) ov[pos] = __uint_as_float((uint32_t)(x >> 32));
-      ++pos;
-    }
+  for (int p = q0; p < q1; p += 4) {
+    unsigned long long x[4];
+    key.quad(p, x);
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      if (p + i < q1 && x[i] >= T) {
+        oi[pos] = p + i;
+        if (ov) ov[pos] = __uint_as_float((uint32_t)(x[i] >> 32));
+        ++pos;
+      }
   }
   if (rank == CL - 1)
     for (int i = all + tid; i < k; i += SEL_THREADS) {
@@ -318,8 +356,10 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(SEL_THREADS, 1)
   const int rank = (int)cl.block_rank();
   const int row = blockIdx.y;
   const int len = row_len(seq_len, row, G, n_cols);
-  const DenseKey key{val + (size_t)row * n_cols, len, force, stride, offset};
-  const int per = (len + CL - 1) / CL;
+  const float* rowp = val + (size_t)row * n_cols;
+  const DenseKey key{rowp, len, force, stride, offset,
+                     (n_cols & 3) == 0 && ((uintptr_t)rowp & 15) == 0};
+  const int per = ((len + CL - 1) / CL + 3) & ~3;  // multiple of 4: quads never straddle
   const int s0 = min(len, rank * per), s1 = min(len, s0 + per);
   int my_base, my_count;
   cluster_select(s, cl, key, len, k, s0, s1, out_idx + (size_t)row * k,
