@@ -334,6 +334,7 @@ def bench_ours(args):
     for j in range(args.steps):
         st.use_set(j % NSETS)
         bi, bo = st.step_host(q_ret_h, q_llm_h, out_h, use_graph=True)
+    st.sync_host()  # the last step's read-back is inside the timed region
     e2[1].record(stream)
     torch.cuda.synchronize()
     e2e_ms = e2[0].elapsed_time(e2[1])

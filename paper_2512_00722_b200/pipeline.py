@@ -56,8 +56,11 @@ class DecodeStep:
             self.src_rows = src_rows if src_rows is not None else self.k_src[0].shape[2]
         B, G, Hq, D, dev = self.B, self.G, Hq, self.D, self.dev
         f32, i32 = torch.float32, torch.int32
-        self.q_ret = torch.zeros((B, Hq, D), dtype=torch.bfloat16, device=dev)
-        self.q_llm = torch.zeros((L, B, Hq, D), dtype=self.kv_dtype, device=dev)
+        # step inputs and outputs are double-buffered by step parity, so the host copies of
+        # one step (step_host) overlap the neighbouring steps' kernels
+        self.q_rets = [torch.zeros((B, Hq, D), dtype=torch.bfloat16, device=dev) for _ in range(2)]
+        self.q_llms = [torch.zeros((L, B, Hq, D), dtype=self.kv_dtype, device=dev)
+                       for _ in range(2)]
         self.logits = torch.zeros((B, Hq, self.Smax), dtype=f32, device=dev)
         self.head_max = torch.zeros((B, Hq), dtype=f32, device=dev)
         self.head_sumfix = torch.zeros((B, Hq), dtype=torch.int64, device=dev)
@@ -68,8 +71,11 @@ class DecodeStep:
         self.n_load = torch.zeros((B, G), dtype=i32, device=dev)
         self.slot_tok = torch.full((B, G, k), -1, dtype=i32, device=dev) if mode == "slots" else None
         self.load_slot = torch.full((B, G, k), -1, dtype=i32, device=dev) if mode == "slots" else None
-        self.out = torch.zeros((L, B, Hq, D), dtype=f32, device=dev)
-        self.lse = torch.zeros((L, B, Hq), dtype=f32, device=dev)
+        self.outs = [torch.zeros((L, B, Hq, D), dtype=f32, device=dev) for _ in range(2)]
+        self.lses = [torch.zeros((L, B, Hq), dtype=f32, device=dev) for _ in range(2)]
+        self.last = 0  # parity of the most recent step (out / lse / q_ret / q_llm views)
+        self._h2d = self._d2h = None  # copy streams of step_host, created on first use
+        self._ev = {}
         self.ws_score = spc.alloc_workspace(spc.score_workspace(B, Hq, self.Smax), dev)
         self.ws_topk = spc.alloc_workspace(spc.topk_workspace(B, G, self.Smax, k), dev)
         self.ws_attn = spc.alloc_workspace(spc.attn_workspace(L, B, Hq, D, k), dev)
@@ -79,6 +85,23 @@ class DecodeStep:
         self.sets = [(self.kr, self.k_tab, self.v_tab, [self.k_layers, self.v_layers])]
         self.cur_set = 0
         self.graphs = {}
+
+    # the input buffers of the next step and the outputs of the most recent one
+    @property
+    def q_ret(self):
+        return self.q_rets[self.parity]
+
+    @property
+    def q_llm(self):
+        return self.q_llms[self.parity]
+
+    @property
+    def out(self):
+        return self.outs[self.last]
+
+    @property
+    def lse(self):
+        return self.lses[self.last]
 
     def add_input_set(self, kr, k_layers, v_layers):
         """Register another (retrieval keys, K layers, V layers) copy; returns its index."""
@@ -96,8 +119,9 @@ class DecodeStep:
         q_ret / q_llm: read the step's queries in place from these tensors instead of the
         step's own input buffers."""
         cur, prev = parity, 1 - parity
-        q_ret = self.q_ret if q_ret is None else q_ret
-        q_llm = self.q_llm if q_llm is None else q_llm
+        q_ret = self.q_rets[parity] if q_ret is None else q_ret
+        q_llm = self.q_llms[parity] if q_llm is None else q_llm
+        out, lse = self.outs[parity], self.lses[parity]
         if self.fused:
             # LOGITS, then NORM + GROUP + top-k + diff in one cluster launch (spc_select)
             spc.score(q_ret, self.kr, self.seq_len, self.G, self.scale, self.logits,
@@ -122,20 +146,20 @@ class DecodeStep:
                           dtype=spc.BF16 if self.kv_dtype == torch.bfloat16 else spc.F32,
                           stream=stream)
             spc.sparse_decode_attn(q_llm, self.k_tab, self.v_tab, spc.KV_SLOTS, None,
-                                   self.cnt[cur], self.k, self.k, self.scale, self.out, self.lse,
+                                   self.cnt[cur], self.k, self.k, self.scale, out, lse,
                                    self.ws_attn, self.G, stream=stream)
         else:
             spc.sparse_decode_attn(q_llm, self.k_tab, self.v_tab, spc.KV_INDEXED,
                                    self.idx[cur], self.cnt[cur], self.rows, self.k, self.scale,
-                                   self.out, self.lse, self.ws_attn, self.G, stream=stream)
+                                   out, lse, self.ws_attn, self.G, stream=stream)
 
     def step(self, q_ret=None, q_llm=None, use_graph: bool = False):
         """Run one decode step on device tensors (copied into the step's input buffers)."""
-        if q_ret is not None:
-            self.q_ret.copy_(q_ret, non_blocking=True)
-        if q_llm is not None:
-            self.q_llm.copy_(q_llm, non_blocking=True)
         p = self.parity
+        if q_ret is not None:
+            self.q_rets[p].copy_(q_ret, non_blocking=True)
+        if q_llm is not None:
+            self.q_llms[p].copy_(q_llm, non_blocking=True)
         if use_graph:
             key = (self.cur_set, p)
             if key not in self.graphs:
@@ -143,6 +167,7 @@ class DecodeStep:
             self.graphs[key].replay()
         else:
             self.enqueue(p)
+        self.last = p
         self.parity ^= 1
         return self.idx[p], self.cnt[p]
 
@@ -194,12 +219,43 @@ class DecodeStep:
     # ------------------------------------------------------------------ end to end
     def step_host(self, q_ret_host: torch.Tensor, q_llm_host: torch.Tensor,
                   out_host: torch.Tensor, use_graph: bool = True):
-        """Public end-to-end call: pinned host inputs -> step -> host attention output.
+        """Public end-to-end call: pinned host inputs -> step -> host attention output, all
+        asynchronous.  The step's host->device copies run on one copy stream, its
+        device->host read on another, ordered with events against the step's kernels, so
+        consecutive calls overlap one step's copies with the neighbouring steps' kernels.
+        `out_host` is complete after `sync_host()` (or a device synchronisation).
         Returns (bytes host->device, bytes device->host)."""
-        self.q_ret.copy_(q_ret_host, non_blocking=True)
-        self.q_llm.copy_(q_llm_host, non_blocking=True)
+        main = torch.cuda.current_stream(self.dev)
+        if self._h2d is None:
+            self._h2d = torch.cuda.Stream(device=self.dev)
+            self._d2h = torch.cuda.Stream(device=self.dev)
+        p = self.parity
+        ev = self._ev
+        # inputs of parity p: the step two calls ago (same parity) must have consumed them
+        if ("done", p) in ev:
+            self._h2d.wait_event(ev[("done", p)])
+        with torch.cuda.stream(self._h2d):
+            self.q_rets[p].copy_(q_ret_host, non_blocking=True)
+            self.q_llms[p].copy_(q_llm_host, non_blocking=True)
+            ev[("in", p)] = torch.cuda.Event()
+            ev[("in", p)].record(self._h2d)
+        main.wait_event(ev[("in", p)])
+        if ("read", p) in ev:  # outs[p] of two calls ago has been read back
+            main.wait_event(ev[("read", p)])
         self.step(use_graph=use_graph)
-        out_host.copy_(self.out, non_blocking=True)
+        ev[("done", p)] = torch.cuda.Event()
+        ev[("done", p)].record(main)
+        self._d2h.wait_event(ev[("done", p)])
+        with torch.cuda.stream(self._d2h):
+            out_host.copy_(self.outs[p], non_blocking=True)
+            ev[("read", p)] = torch.cuda.Event()
+            ev[("read", p)].record(self._d2h)
         return (q_ret_host.numel() * q_ret_host.element_size() +
                 q_llm_host.numel() * q_llm_host.element_size(),
                 out_host.numel() * out_host.element_size())
+
+    def sync_host(self):
+        """Make every pending step_host copy part of the current stream's history."""
+        if self._d2h is not None:
+            torch.cuda.current_stream(self.dev).wait_stream(self._d2h)
+            torch.cuda.current_stream(self.dev).wait_stream(self._h2d)

@@ -98,3 +98,21 @@ def test_pipeline_config_b_sampled(oracle):
             overlap = 1 - nl.sum() / cnt.sum()
             assert 0.3 < overlap < 1.0  # synthetic AR(1) queries: high adjacent overlap
         prev = idx
+
+
+def test_step_host_matches_device_steps():
+    """step_host (pinned host inputs, double-buffered async copies) reproduces the device
+    path bit for bit, every step."""
+    c, st, kr, kc, vc, qr, ql = build("A", synth.BASE_SEED + 9, steps=4)
+    want = []
+    for s in range(qr.shape[0]):
+        st.step(qr[s], ql[s], use_graph=True)
+        torch.cuda.synchronize()
+        want.append(st.out.clone())
+    _, st2, *_ = build("A", synth.BASE_SEED + 9, steps=4)
+    out_h = torch.empty(st2.outs[0].shape, dtype=torch.float32).pin_memory()
+    for s in range(qr.shape[0]):
+        st2.step_host(qr[s].cpu().pin_memory(), ql[s].cpu().pin_memory(), out_h)
+        st2.sync_host()
+        torch.cuda.synchronize()
+        assert torch.equal(out_h, want[s].cpu()), s
