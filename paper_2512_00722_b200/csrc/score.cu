@@ -136,9 +136,9 @@ __global__ void __launch_bounds__(GRP_THREADS) group_kernel(
 
 template <int D, int ALPHA>
 int launch_logits(const uint16_t* kr, const uint16_t* q, const int32_t* seq_len, int B, int G,
-                  int Smax, float scale, float* logits, float* seg_max, int segstride,
-                  unsigned* counters, float* head_max, cudaStream_t st) {
-  const size_t smem = Lg4Smem<D, ALPHA>::BYTES;
+                  int Smax, float scale, float* logits, float* tile_max, unsigned* ctr,
+                  float* head_max, cudaStream_t st) {
+  const size_t smem = LgSmem<D, ALPHA>::BYTES;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(logits_kernel<D, ALPHA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -147,12 +147,14 @@ int launch_logits(const uint16_t* kr, const uint16_t* q, const int32_t* seq_len,
   }
   const int tpr = (Smax + LG_TR - 1) / LG_TR;
   const int ntiles = B * G * tpr;
-  int tpc = (ntiles + num_sms() - 1) / num_sms();
-  if (tpc > tpr) tpc = tpr;  // a CTA spans at most two groups
-  const int ncta = (ntiles + tpc - 1) / tpc;
-  return launched(launch_k(logits_kernel<D, ALPHA>, dim3(ncta), dim3(32 * lg_warps<ALPHA>()),
-                           smem, st, kr, q, seq_len, G, Smax, scale, tpc, tpr, ntiles, logits,
-                           seg_max, segstride, counters, head_max));
+  const int nw = (ntiles + 1) / 2;  // >= 2 tiles per warp
+  const int ncta = max(1, min(num_sms(), (nw + lg_warps<ALPHA>() - 1) / lg_warps<ALPHA>()));
+  SPC_TRY(launched(launch_k(logits_kernel<D, ALPHA>, dim3(ncta), dim3(32 * lg_warps<ALPHA>()),
+                           smem, st, kr, q, seq_len, G, Smax, scale, tpr, ntiles, logits,
+                           tile_max, ctr)));
+  const int nh = B * G * ALPHA;
+  return launched(launch_k(lg_finalize_kernel, dim3((nh + 3) / 4), dim3(128), 0, st,
+                           (const float*)tile_max, tpr, nh, head_max, ctr));
 }
 
 template <int ALPHA>
@@ -164,28 +166,25 @@ int launch_group(const float* logits, const float* head_max, const int64_t* sumf
 }
 
 struct ScoreWs {
-  float* tile_max;
+  float* tile_max;     // [B][Hq][tiles of LG_TR rows] LOGITS: per-tile head maxima
+  unsigned* lg_ctr;    // LOGITS: tile-claim counter
   long long* tile_sum;
-  unsigned* cnt1;
   unsigned* cnt2;
-  size_t nt1;  // segment stride of tile_max
   size_t bytes;
 };
 ScoreWs score_ws_layout(void* ws, int B, int Hq, int Smax) {
-  // nt1 bounds the CTA segments of one group in LOGITS (every CTA owns >= 1 tile)
-  const size_t nt1 = (Smax + LG_TR - 1) / LG_TR + 2, nt2 = (Smax + NORM_TILE - 1) / NORM_TILE;
+  const size_t nt2 = (Smax + NORM_TILE - 1) / NORM_TILE;
   uint8_t* p = (uint8_t*)ws;
   ScoreWs w;
   size_t off = 0;
   w.tile_max = (float*)(p + off);
-  off = align_up(off + sizeof(float) * B * Hq * nt1, 256);
+  off = align_up(off + sizeof(float) * B * Hq * ((Smax + LG_TR - 1) / LG_TR), 256);
+  w.lg_ctr = (unsigned*)(p + off);
+  off = align_up(off + sizeof(unsigned) * 2, 256);
   w.tile_sum = (long long*)(p + off);
   off = align_up(off + sizeof(long long) * B * Hq * nt2, 256);
-  w.cnt1 = (unsigned*)(p + off);
-  off = align_up(off + sizeof(unsigned) * B * Hq, 256);
   w.cnt2 = (unsigned*)(p + off);
   off = align_up(off + sizeof(unsigned) * B * Hq, 256);
-  w.nt1 = nt1;
   w.bytes = off;
   return w;
 }
@@ -222,8 +221,8 @@ extern "C" int spc_score(int dtype, const void* q, const void* kr, const int32_t
     const uint16_t* qq = (const uint16_t*)q;
 #define LG(DD, AA)                                                                            \
   if (D == DD && alpha == AA)                                                                 \
-    SPC_TRY((launch_logits<DD, AA>((const uint16_t*)kr, qq, seq_len, B, G, Smax, scale, logits, w.tile_max, \
-                                   (int)w.nt1, w.cnt1, head_max, st)));
+    SPC_TRY((launch_logits<DD, AA>((const uint16_t*)kr, qq, seq_len, B, G, Smax, scale, logits, \
+                                   w.tile_max, w.lg_ctr, head_max, st)));
     LG(64, 1) LG(64, 2) LG(64, 4) LG(64, 8) LG(128, 1) LG(128, 2) LG(128, 4) LG(128, 8)
 #undef LG
   }
