@@ -44,6 +44,9 @@ constexpr int WR = 16;      // rows per warp per chunk
 #ifndef SPC_ATTN_CTAS
 #define SPC_ATTN_CTAS 2
 #endif
+#ifndef SPC_ATTN_PF
+#define SPC_ATTN_PF 1  // chunks of L2 prefetch ahead of the cp.async issue point
+#endif
 constexpr int NSTAGE = SPC_ATTN_NSTAGE;  // per-warp ring depth (chunks in flight: NSTAGE - 1)
 // 8 warps/SM.  (3 CTAs x 2 stages measured slower: 70 vs 62 us for config B.)
 constexpr int AT2_CTAS_PER_SM = SPC_ATTN_CTAS;
@@ -51,6 +54,8 @@ constexpr int NWARP = 4;
 constexpr int AT2_THREADS = NWARP * 32;
 constexpr int TRING = 8;    // per-warp ring of prefetched chunk metadata
 constexpr int MAHEAD = 5;   // metadata fetched this many chunks before its rows are issued
+// the prefetch of chunk i + NSTAGE - 1 + PF at iteration i reads metadata that landed
+static_assert(SPC_ATTN_PF <= MAHEAD - NSTAGE, "prefetch needs landed metadata");
 
 template <int D, int ALPHA>
 struct PSmem {
@@ -259,6 +264,24 @@ __global__ void __launch_bounds__(AT2_THREADS, AT2_CTAS_PER_SM) attn_bf16_kernel
     }
   };
   // ---- rows of chunk j -> stage s_iss (requires meta of chunk j landed)
+  // ---- L2 prefetch of the rows of chunk j (SPC_ATTN_PF chunks ahead of their cp.async):
+  // the DRAM latency is paid by a prefetch that holds no shared memory or registers, so
+  // the cp.async ring waits only on L2 latency.  Lanes 0-15: K rows, 16-31: V rows.
+  ChunkIt it_pf = it0;
+  auto prefetch_rows = [&](int j) {
+    const ChunkIt c = it_pf;
+    it_pf.next(cpg, BG);
+    if (j >= n_chunks) return;
+    const uint8_t* m = meta + (j & (TRING - 1)) * SM::META;
+    const int rr = lane & 15;
+    const int r = c.rc * CH + warp * WR + rr;
+    if (r >= min(*(const int*)(m + 64), kbud)) return;
+    const int tok = ind ? *(const int*)(m + rr * 4) : r;
+    const uint16_t* base = *(const uint16_t* const*)(m + (lane < 16 ? 72 : 80));
+    const uint16_t* row = base + ((size_t)c.bg * rows + tok) * D;
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(row) : "memory");
+    if (D * 2 > 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(row + 64) : "memory");
+  };
   ChunkIt it_rows = it0;
   int s_iss = 0, cached_grp = -1, cnt_g = 0;
   const uint16_t *Kcol = nullptr, *Vcol = nullptr;
@@ -323,6 +346,10 @@ __global__ void __launch_bounds__(AT2_THREADS, AT2_CTAS_PER_SM) attn_bf16_kernel
   cp_async_commit();
   cp_async_wait<0>();
   __syncwarp();
+#if SPC_ATTN_PF > 0
+  for (int j = 0; j < NSTAGE - 1; ++j) it_pf.next(cpg, BG);  // rows issued below directly
+  for (int j = NSTAGE - 1; j < NSTAGE - 1 + SPC_ATTN_PF; ++j) prefetch_rows(j);
+#endif
 #pragma unroll
   for (int j = 0; j < NSTAGE - 1; ++j) {
     issue_rows(j);
@@ -362,6 +389,9 @@ __global__ void __launch_bounds__(AT2_THREADS, AT2_CTAS_PER_SM) attn_bf16_kernel
     cp_async_wait<NSTAGE - 1>();
     __syncwarp();
     issue_rows(i + NSTAGE - 1);
+#if SPC_ATTN_PF > 0
+    prefetch_rows(i + NSTAGE - 1 + SPC_ATTN_PF);
+#endif
     fetch_meta(i + NSTAGE - 1 + MAHEAD);
     cp_async_commit();
     trace(i, 0);

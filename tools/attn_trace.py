@@ -3,7 +3,7 @@ import ctypes, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 from paper_2512_00722_b200 import build, spc, synth
-_so = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libspc_trace.so")
+_so = os.environ.get("SPC_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libspc_trace.so")
 if not os.path.exists(_so):
     build.build(out=_so, defines=["SPC_TRACE"])
 spc._lib = spc.load_library(_so)
