@@ -41,6 +41,9 @@ def parse():
                          "D (KV in pinned host memory, B=4) or E (context-sharded); default B "
                          "at N=1, E at N>1")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--kv-layout", default="token", choices=["token", "layer"],
+                    help="config D host KV layout: token-major records (one contiguous record "
+                         "per token) or layer-major [L][B][G][rows][D]")
     return ap.parse_args()
 
 
@@ -646,18 +649,34 @@ def bench_offload(args):
     rows = S + (L // PHYS - 1) * OFF
     seed = synth.BASE_SEED + 4
     kr = synth.retrieval_keys(B, G, S, D, seed=seed, device=dev)
-    host = []
-    for p in range(PHYS):  # generated on the GPU layer by layer, copied into pinned host memory
-        pair = []
-        for t in range(2):
-            h = torch.empty((B, G, rows, D), dtype=torch.bfloat16, pin_memory=True)
-            for b in range(B):
-                h[b].copy_(synth.normal_bf16((G, rows, D), seed * 131 + p * 7 + t * 3 + b,
-                                             device=dev))
-            pair.append(h)
-        host.append(pair)
-    k_src = [host[l % PHYS][0].view(-1)[(l // PHYS) * OFF * D:] for l in range(L)]
-    v_src = [host[l % PHYS][1].view(-1)[(l // PHYS) * OFF * D:] for l in range(L)]
+    token_major = args.kv_layout == "token"
+    src_strides = None
+    if token_major:
+        # one record per token: [PHYS layers][K, V][D] (4 KiB); layer l reads physical layer
+        # l % PHYS of the record of token t + (l // PHYS) * OFF (a real deployment's record
+        # holds all L layers: 16 KiB contiguous per selected token -- this is conservative)
+        rec = torch.empty((B, G, rows, PHYS, 2, D), dtype=torch.bfloat16, pin_memory=True)
+        for b in range(B):
+            for g in range(G):
+                rec[b, g].copy_(synth.normal_bf16((rows, PHYS, 2, D), seed * 131 + b * G + g,
+                                                  device=dev))
+        host = [[rec]]
+        k_src = [rec[:, :, (l // PHYS) * OFF:, l % PHYS, 0] for l in range(L)]
+        v_src = [rec[:, :, (l // PHYS) * OFF:, l % PHYS, 1] for l in range(L)]
+        src_strides = (PHYS * 2 * D, rows * PHYS * 2 * D)
+    else:
+        host = []
+        for p in range(PHYS):  # generated on the GPU layer by layer, copied into pinned memory
+            pair = []
+            for t in range(2):
+                h = torch.empty((B, G, rows, D), dtype=torch.bfloat16, pin_memory=True)
+                for b in range(B):
+                    h[b].copy_(synth.normal_bf16((G, rows, D), seed * 131 + p * 7 + t * 3 + b,
+                                                 device=dev))
+                pair.append(h)
+            host.append(pair)
+        k_src = [host[l % PHYS][0].view(-1)[(l // PHYS) * OFF * D:] for l in range(L)]
+        v_src = [host[l % PHYS][1].view(-1)[(l // PHYS) * OFF * D:] for l in range(L)]
     kb = torch.zeros((L, B, G, k, D), dtype=torch.bfloat16, device=dev)
     vb = torch.zeros_like(kb)
     qr = synth.retrieval_queries(nsteps + 1, B, Hq, G, D, seed=seed, device=dev)
@@ -665,7 +684,7 @@ def bench_offload(args):
     seq = torch.full((B,), S, dtype=torch.int32, device=dev)
     st = DecodeStep(kr, [kb[l] for l in range(L)], [vb[l] for l in range(L)], seq, L, Hq, k,
                     mode="slots", k_src_layers=k_src, v_src_layers=v_src, kv_rows=k,
-                    src_rows=rows)
+                    src_rows=rows, src_strides=src_strides)
     st.step(qr[0], ql[0])
     n0 = spc.launch_count()
     seq_graphs = st.capture_sequence([(0, qr[i], ql[i % 2]) for i in range(nsteps)])
@@ -716,10 +735,16 @@ def bench_offload(args):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (seeded; DESIGN.md §5)",
         "config": {"workload": workload_name(dict(c, B=B), "D") + " (B reduced from 32: host RAM)",
-                   "kv": f"LLM KV in pinned host memory: {PHYS} physical layers aliased at row "
-                         f"offsets, {sum(t.numel() for p in host for t in p) * 2 / 2**30:.1f} GiB",
-                   "kv_mode": "SLOTS: spc_gather_kv of the new rows (host -> HBM budget "
-                              "buffers, zero-copy reads of pinned memory), then attention",
+                   "kv": (f"LLM KV in pinned host memory, token-major records [{PHYS} layers][K,V]"
+                          f"[D] (4 KiB) per token, layer l = physical l % {PHYS} of the record "
+                          f"of token t + (l // {PHYS}) * {OFF}" if token_major else
+                          f"LLM KV in pinned host memory, layer-major: {PHYS} physical layers "
+                          f"aliased at row offsets") +
+                         f", {sum(t.numel() for p in host for t in p) * 2 / 2**30:.1f} GiB",
+                   "kv_mode": ("SLOTS: spc_gather_kv_strided of the new tokens' records"
+                               if token_major else "SLOTS: spc_gather_kv of the new rows") +
+                              " (host -> HBM budget buffers, zero-copy reads of pinned memory),"
+                              " then attention",
                    "rows_loaded_per_step": rows_loaded,
                    "elastic_reuse": round(1 - rows_loaded / (B * G * k), 4),
                    "pcie_bytes_per_step": pcie_bytes,

@@ -215,6 +215,29 @@ int spc_gather_kv(int dtype, const void* const* k_src, const void* const* v_src,
                   void* const* v_buf, spc_stream_t stream);
 
 /* ------------------------------------------------------------------------
+ * spc_gather_kv_strided — spc_gather_kv (O9, same copy) for sources laid out
+ * with explicit strides, in particular TOKEN-MAJOR offloaded KV where one
+ * token's K and V rows of every layer form one contiguous record
+ * ([B][G][Smax][L][2][D]: k_src[l] = base + l*2*D, v_src[l] = k_src[l] + D,
+ * row_stride = L*2*D, bg_stride = Smax*L*2*D).  Paper: P:374 elastic copy_,
+ * P:180/P:197 KV in CPU DRAM, P:363-365 (loading I/O dominates): a selected
+ * token is then one contiguous PCIe read (config D).
+ * K row of token t of (b,g) in layer l (bf16 elements):
+ *   k_src[l] + (b*G+g)*bg_stride + t*row_stride        (same for v_src)
+ * For every l in [layer_begin, layer_end), (b,g), i < n_load[b][g]:
+ *   k_buf[l][b][g][load_slot[i]][:] = K row of token load_tok[i]  (same for V)
+ * k_src/v_src/k_buf/v_buf: DEVICE arrays of L pointers (sources may be mapped
+ * pinned host memory); row_stride >= D; strides in elements, 16-byte aligned.
+ * Supported: SPC_BF16, D in {64, 128}.  Errors: SPC_E_NULL, SPC_E_SHAPE,
+ * SPC_E_BUDGET, SPC_E_RANGE, SPC_E_UNSUPPORTED, SPC_E_CUDA.
+ * ---------------------------------------------------------------------- */
+int spc_gather_kv_strided(int dtype, const void* const* k_src, const void* const* v_src,
+                          long long row_stride, long long bg_stride, int L, int B, int G, int D,
+                          int k, int layer_begin, int layer_end, const int32_t* load_tok,
+                          const int32_t* load_slot, const int32_t* n_load, void* const* k_buf,
+                          void* const* v_buf, spc_stream_t stream);
+
+/* ------------------------------------------------------------------------
  * spc_sparse_decode_attn — GQA decode attention over the selected rows, O10.
  *
  * Paper: Eq.1 softmax(QK^T/sqrt(d)) V restricted to the selected tokens,

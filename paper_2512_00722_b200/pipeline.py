@@ -25,10 +25,12 @@ class DecodeStep:
     def __init__(self, kr: torch.Tensor, k_layers, v_layers, seq_len: torch.Tensor, L: int,
                  Hq: int, k: int, mode: str = "indexed", force_last: bool = True, scale=None,
                  kv_rows=None, k_src_layers=None, v_src_layers=None, fused=None,
-                 src_rows=None):
+                 src_rows=None, src_strides=None):
         """kr: retrieval keys [B][G][Smax][D] bf16.  k_layers/v_layers: L tensors [B][G][rows][D]
         (INDEXED: the full caches; SLOTS: the budget buffers [B][G][k][D], with
-        k_src_layers/v_src_layers the full caches, device or mapped host)."""
+        k_src_layers/v_src_layers the full caches, device or mapped host).  src_strides =
+        (row_stride, bg_stride) in elements: the sources are strided views (e.g. the layers of
+        token-major KV records) and the elastic load uses spc_gather_kv_strided."""
         self.dev = kr.device
         # fused spc_select (one launch for NORM..diff) where it applies: INDEXED mode and
         # Smax <= 135168, a multiple of 4; otherwise the separate ABI calls
@@ -54,6 +56,7 @@ class DecodeStep:
             self.k_src_tab = spc.ptr_table(self.k_src, self.dev)
             self.v_src_tab = spc.ptr_table(self.v_src, self.dev)
             self.src_rows = src_rows if src_rows is not None else self.k_src[0].shape[2]
+            self.src_strides = src_strides
         B, G, Hq, D, dev = self.B, self.G, Hq, self.D, self.dev
         f32, i32 = torch.float32, torch.int32
         # step inputs and outputs are double-buffered by step parity, so the host copies of
@@ -140,11 +143,17 @@ class DecodeStep:
                              self.load_tok, self.n_load, slot_tok=self.slot_tok,
                              load_slot=self.load_slot, stream=stream)
         if self.mode == "slots":
-            spc.gather_kv(self.k_src_tab, self.v_src_tab, self.L, self.B, self.G, self.D,
-                          self.src_rows, self.k, self.load_tok, self.load_slot, self.n_load,
-                          self.k_tab, self.v_tab,
-                          dtype=spc.BF16 if self.kv_dtype == torch.bfloat16 else spc.F32,
-                          stream=stream)
+            if self.src_strides is not None:
+                spc.gather_kv_strided(self.k_src_tab, self.v_src_tab, self.src_strides[0],
+                                      self.src_strides[1], self.L, self.B, self.G, self.D, self.k,
+                                      self.load_tok, self.load_slot, self.n_load, self.k_tab,
+                                      self.v_tab, stream=stream)
+            else:
+                spc.gather_kv(self.k_src_tab, self.v_src_tab, self.L, self.B, self.G, self.D,
+                              self.src_rows, self.k, self.load_tok, self.load_slot, self.n_load,
+                              self.k_tab, self.v_tab,
+                              dtype=spc.BF16 if self.kv_dtype == torch.bfloat16 else spc.F32,
+                              stream=stream)
             spc.sparse_decode_attn(q_llm, self.k_tab, self.v_tab, spc.KV_SLOTS, None,
                                    self.cnt[cur], self.k, self.k, self.scale, out, lse,
                                    self.ws_attn, self.G, stream=stream)

@@ -26,8 +26,8 @@ EXPORTS = [
     "spc_status_string", "spc_last_cuda_error", "spc_version", "spc_launch_count",
     "spc_score_workspace", "spc_score", "spc_topk_workspace", "spc_topk",
     "spc_topk_merge_workspace", "spc_topk_merge", "spc_topk_filter", "spc_elastic_diff",
-    "spc_gather_kv", "spc_attn_workspace", "spc_sparse_decode_attn", "spc_attn_merge",
-    "spc_select",
+    "spc_gather_kv", "spc_gather_kv_strided", "spc_attn_workspace", "spc_sparse_decode_attn",
+    "spc_attn_merge", "spc_select",
 ]
 
 
@@ -64,6 +64,8 @@ def load_library(path: str = LIB_PATH):
     L.spc_elastic_diff.argtypes = [P, P, P, P, i32, i32, i32, P, P, P, P, P, P, P]
     L.spc_gather_kv.argtypes = [i32, P, P, i32, i32, i32, i32, i32, i32, i32, i32, P, P, P, P, P,
                                 P]
+    L.spc_gather_kv_strided.argtypes = [i32, P, P, ctypes.c_longlong, ctypes.c_longlong, i32, i32,
+                                        i32, i32, i32, i32, i32, P, P, P, P, P, P]
     L.spc_attn_workspace.argtypes = [i32, i32, i32, i32, i32]
     L.spc_attn_workspace.restype = sz
     L.spc_sparse_decode_attn.argtypes = [i32, P, P, P, i32, P, P, i32, i32, i32, i32, i32, i32,
@@ -195,6 +197,18 @@ def gather_kv(k_src_tab, v_src_tab, L: int, B: int, G: int, D: int, Smax: int, k
     _check(lib().spc_gather_kv(dtype, _p(k_src_tab), _p(v_src_tab), L, B, G, D, Smax, k,
                                layer_begin, layer_end, _p(load_tok), _p(load_slot), _p(n_load),
                                _p(k_buf_tab), _p(v_buf_tab), _s(stream)), "spc_gather_kv")
+
+
+def gather_kv_strided(k_src_tab, v_src_tab, row_stride: int, bg_stride: int, L: int, B: int,
+                      G: int, D: int, k: int, load_tok, load_slot, n_load, k_buf_tab, v_buf_tab,
+                      layer_begin: int = 0, layer_end=None, dtype: int = BF16, stream=None):
+    """spc_gather_kv_strided: the O9 copy from sources with explicit (token, (b,g)) strides,
+    e.g. token-major offloaded KV records."""
+    layer_end = L if layer_end is None else layer_end
+    _check(lib().spc_gather_kv_strided(dtype, _p(k_src_tab), _p(v_src_tab), int(row_stride),
+                                       int(bg_stride), L, B, G, D, k, layer_begin, layer_end,
+                                       _p(load_tok), _p(load_slot), _p(n_load), _p(k_buf_tab),
+                                       _p(v_buf_tab), _s(stream)), "spc_gather_kv_strided")
 
 
 def sparse_decode_attn(q, k_tab, v_tab, kv_mode: int, idx, count, rows: int, k: int, scale: float,

@@ -61,6 +61,13 @@ def test_host_validation_without_gpu(libspc):
     assert libspc.spc_elastic_diff(P, P, P, P, 1, 1, 0, None, P, None, P, None, None, st) == 3
     # layer range
     assert libspc.spc_gather_kv(0, P, P, 4, 1, 1, 128, 100, 16, 3, 2, P, P, P, P, P, st) == 4
+    ll = ctypes.c_longlong
+    assert libspc.spc_gather_kv_strided(0, P, P, ll(1024), ll(0), 4, 1, 1, 128, 16, 3, 2, P, P,
+                                        P, P, P, st) == 4
+    assert libspc.spc_gather_kv_strided(0, P, P, ll(64), ll(0), 4, 1, 1, 128, 16, 0, 4, P, P,
+                                        P, P, P, st) == 2  # row_stride < D
+    assert libspc.spc_gather_kv_strided(0, None, P, ll(1024), ll(0), 4, 1, 1, 128, 16, 0, 4, P,
+                                        P, P, P, P, st) == 1
     assert libspc.spc_sparse_decode_attn(0, P, P, P, 0, P, P, 2, 0, 3, 1, 4, 1, 128, 100, 16,
                                          0.1, P, None, P, 1 << 30, st) == 4
     assert libspc.spc_score_workspace(1, 32, 32768) > 0

@@ -205,6 +205,49 @@ def test_gather_kv_bytes_exact(oracle):
                     assert torch.equal(vbc[l, b, g, ls[r, i]], vcc[l, b, g, lt[r, i]])
 
 
+@pytest.mark.parametrize("D", [128, 64])
+def test_gather_kv_strided_token_major_bytes_exact(D):
+    """O9 from a TOKEN-MAJOR source (one record [L][2][D] per token, the offloaded-KV layout
+    of config D): spc_gather_kv_strided copies the K and V rows of every layer in range
+    byte for byte, from device or pinned host memory, for empty, partial and full loads."""
+    L, B, G, Smax, k = 5, 2, 3, 300, 96
+    rec = synth.normal_bf16((B, G, Smax, L, 2, D), 31)
+    for host in (False, True):
+        src = rec.pin_memory() if host else rec.to(DEV)
+        base, esz = src.data_ptr(), 2
+        k_tab = torch.tensor([base + l * 2 * D * esz for l in range(L)], dtype=torch.int64,
+                             device=DEV)
+        v_tab = k_tab + D * esz
+        kb = torch.zeros((L, B, G, k, D), dtype=torch.bfloat16, device=DEV) - 1
+        vb = torch.zeros_like(kb) - 1
+        rng = np.random.default_rng(5)
+        lt = np.full((B * G, k), -1, np.int32)
+        ls = np.full((B * G, k), -1, np.int32)
+        nl = np.array([0, k, 1, 37, 64, 95][:B * G], np.int32)
+        for r in range(B * G):
+            n = int(nl[r])
+            lt[r, :n] = np.sort(rng.choice(Smax, n, replace=False))
+            ls[r, :n] = rng.permutation(k)[:n]
+        l0, l1 = (0, L) if host else (1, 4)
+        spc.gather_kv_strided(k_tab, v_tab, L * 2 * D, Smax * L * 2 * D, L, B, G, D, k,
+                              torch.from_numpy(lt).to(DEV), torch.from_numpy(ls).to(DEV),
+                              torch.from_numpy(nl).to(DEV), spc.ptr_table([kb[l] for l in range(L)], DEV),
+                              spc.ptr_table([vb[l] for l in range(L)], DEV), layer_begin=l0,
+                              layer_end=l1)
+        torch.cuda.synchronize()
+        kbc, vbc = kb.cpu(), vb.cpu()
+        expect_k = torch.zeros_like(kbc) - 1
+        expect_v = torch.zeros_like(vbc) - 1
+        for l in range(l0, l1):
+            for r in range(B * G):
+                b, g = divmod(r, G)
+                n = int(nl[r])
+                expect_k[l, b, g, ls[r, :n]] = rec[b, g, lt[r, :n], l, 0]
+                expect_v[l, b, g, ls[r, :n]] = rec[b, g, lt[r, :n], l, 1]
+        assert torch.equal(kbc.view(torch.int16), expect_k.view(torch.int16))
+        assert torch.equal(vbc.view(torch.int16), expect_v.view(torch.int16))
+
+
 @pytest.mark.parametrize("alpha,G,S,k", [(4, 8, 32768, 2048), (2, 3, 5000, 700), (8, 1, 300, 512),
                                          (1, 4, 20000, 64)])
 def test_fused_select_equals_separate_calls(oracle, alpha, G, S, k):
