@@ -272,6 +272,41 @@ int spc_sparse_decode_attn(int dtype, const void* q, const void* const* k_layers
 int spc_attn_merge(const float* o_parts, const float* lse_parts, int P, int n, int D, float* out,
                    float* lse_out, spc_stream_t stream);
 
+/* ------------------------------------------------------------------------
+ * spc_rethead_qk — the retrieval head's per-step front-end (SURVEY §8(f)
+ * NEXT-1): embedding lookup -> RMSNorm -> Q/K projection GEMV -> RoPE (YaRN
+ * scaled) -> K-cache append.  It precedes spc_score on the critical path.
+ *
+ * Paper §4.3: the retrieval head keeps the DLM's embedding module and
+ * QK projection weights, extends its context with YaRN, and maintains a full
+ * K cache; ~60 MB of weights.  SPEC run_retrieval_head: the
+ * new key is appended at position = cache length, then scored (reading R6).
+ * Per request b (readings R22-R24):
+ *   x  = emb[token[b]];  xn = bf16(w * bf16(x / sqrt(mean(x^2) + eps)))
+ *   pre = W_qk xn (fp32 accumulation);  RoPE on pairs (i, i + D/2) of every
+ *   head with a = fl32(pos[b] * inv_freq[i]), c = cos(a)*mscale,
+ *   s = sin(a)*mscale: (u, v) -> (u c - v s, v c + u s);  results rounded to bf16.
+ * token    [B] int32 DEVICE, 0 <= token < V (UB otherwise)
+ * emb      [V][H] bf16;  norm_w [H] bf16 or NULL (unit weight);  eps > 0
+ * w_qk     [(Hq+G)*D][H] bf16: rows h*D + d for query head h < Hq, then
+ *          (Hq + g)*D + d for key head g (W_q then W_k, nn.Linear layout)
+ * inv_freq [D/2] f32 (the caller's rotary table, e.g. YaRN-scaled); mscale
+ *          multiplies cos and sin (YaRN attention scaling; 1 = plain RoPE)
+ * pos      [B] int32 DEVICE: the new token's position = keys already cached,
+ *          0 <= pos < Smax
+ * q_out    [B][Hq][D] bf16 out (the query spc_score takes)
+ * kr       [B][G][Smax][D] bf16 in/out: row pos[b] of every group written
+ * seq_len_out [B] int32 out or NULL: pos + 1 (the seq_len spc_score takes)
+ * x_out    [B][H] bf16 out or NULL: xn (the normalised input)
+ * Supported: D in {64, 128}, H % 8 == 0, B <= 16, B*H*2 <= 200 KiB.
+ * Errors: SPC_E_NULL, SPC_E_SHAPE, SPC_E_RANGE (16-byte alignment of emb,
+ * w_qk), SPC_E_UNSUPPORTED, SPC_E_CUDA.
+ * ---------------------------------------------------------------------- */
+int spc_rethead_qk(const int32_t* token, const void* emb, int V, int H, const void* norm_w,
+                   float eps, const void* w_qk, const float* inv_freq, float mscale,
+                   const int32_t* pos, int B, int Hq, int G, int D, int Smax, void* q_out,
+                   void* kr, int32_t* seq_len_out, void* x_out, spc_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

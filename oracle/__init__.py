@@ -56,6 +56,8 @@ def lib():
         L.spcref_group_score_f64.argtypes = [P, P, P, i32, i32, i32, i32, i32, f64, P]
         L.spcref_topk_row.argtypes = [P, P, i32, i32, i32, i32, i32, P, P, P]
         L.spcref_topk_row.restype = i32
+        L.spcref_rmsnorm_bf16.argtypes = [P, P, i32, f64, P]
+        L.spcref_rethead_qk.argtypes = [P, i32, i32, P, P, i32, i32, f64, P, P]
         L.spcref_composite.argtypes = [f32, ctypes.c_int32]
         L.spcref_composite.restype = ctypes.c_uint64
         L.spcref_elastic_diff_row.argtypes = [P, i32, P, i32, i32, P, P, P, P, P, P]
@@ -259,3 +261,31 @@ def attn_merge(o_parts, lse_parts):
         lse[i] = lib().spcref_attn_merge_row(_p(o), _p(s), P, D, _p(r))
         out[i] = r
     return out, lse
+
+
+# ---------------------------------------------------------------- NEXT-1 front-end
+def rmsnorm_bf16(x, w, eps: float):
+    """x [B][H] bf16 bits (uint16); w [H] bits or None -> xn [B][H] bf16 bits (spcref_rmsnorm_bf16)."""
+    x = np.ascontiguousarray(_bf16_bits(x))
+    B, H = x.shape
+    wb = None if w is None else np.ascontiguousarray(_bf16_bits(w))
+    out = np.zeros((B, H), np.uint16)
+    for b in range(B):
+        lib().spcref_rmsnorm_bf16(_p(x[b]), None if wb is None else _p(wb), H, float(eps), _p(out[b]))
+    return out
+
+
+def rethead_qk(W, xn, inv_freq, pos, D: int, mscale: float = 1.0):
+    """W [N][H] bits, xn [B][H] bits, inv_freq [D/2] f32, pos [B] -> (out [B][N] f64 rotated
+    projections, bound [B][N] f64 = sum |W x|) (spcref_rethead_qk)."""
+    W = np.ascontiguousarray(_bf16_bits(W))
+    xn = np.ascontiguousarray(_bf16_bits(xn))
+    inv = np.ascontiguousarray(np.asarray(inv_freq, np.float32))
+    N, H = W.shape
+    B = xn.shape[0]
+    out = np.zeros((B, N), np.float64)
+    bound = np.zeros((B, N), np.float64)
+    for b in range(B):
+        lib().spcref_rethead_qk(_p(W), N, H, _p(xn[b]), _p(inv), D, int(pos[b]), float(mscale),
+                                _p(out[b]), _p(bound[b]))
+    return out, bound

@@ -336,3 +336,56 @@ double spcref_attn_merge_row(const double* o_parts, const double* lse_parts, int
   for (int d = 0; d < D; ++d) out[d] /= den;
   return M + log(den);
 }
+
+/* =====================================================================
+ * NEXT-1: the retrieval head's front-end.  Paper §4.3: the head keeps the
+ * DLM's embedding module and QK projection weights and a full K cache, with YaRN
+ * for long context; SPEC run_retrieval_head appends the new key at
+ * position = cache length.  The normalisation follows the HF Llama RMSNorm the
+ * EAGLE-3 DLM uses (reading R22); the rotation is rotate_half RoPE with the
+ * caller's (YaRN-scaled) frequency table and attention scale (R23, R24).
+ * ===================================================================== */
+static uint16_t f_to_bf16_rn(float f) { /* IEEE RN-even of a finite float to bf16 */
+  uint32_t u = bits_from_f(f);
+  u += 0x7FFFu + ((u >> 16) & 1u);
+  return (uint16_t)(u >> 16);
+}
+
+void spcref_rmsnorm_bf16(const uint16_t* x, const uint16_t* w, int H, double eps, uint16_t* out) {
+  double ss = 0.0;
+  for (int h = 0; h < H; ++h) {
+    const double v = (double)bf16_to_f(x[h]);
+    ss += v * v;
+  }
+  const double r = 1.0 / sqrt(ss / (double)H + eps);
+  for (int h = 0; h < H; ++h) {
+    const float t = bf16_to_f(f_to_bf16_rn((float)((double)bf16_to_f(x[h]) * r)));
+    const float wv = w ? bf16_to_f(w[h]) : 1.0f;
+    out[h] = f_to_bf16_rn(wv * t);
+  }
+}
+
+void spcref_rethead_qk(const uint16_t* W, int N, int H, const uint16_t* xn, const float* inv_freq, int D,
+                       int pos, double mscale, double* out, double* bound) {
+  double* pre = (double*)malloc(sizeof(double) * (size_t)N);
+  for (int n = 0; n < N; ++n) {
+    double acc = 0.0, ab = 0.0;
+    for (int h = 0; h < H; ++h) {
+      const double t = (double)bf16_to_f(W[(size_t)n * H + h]) * (double)bf16_to_f(xn[h]);
+      acc += t;
+      ab += fabs(t);
+    }
+    pre[n] = acc;
+    bound[n] = ab;
+  }
+  const int half = D / 2;
+  for (int hd = 0; hd < N / D; ++hd)
+    for (int i = 0; i < half; ++i) {
+      const float a = (float)pos * inv_freq[i]; /* fl32 angle, as the kernel */
+      const double c = cos((double)a) * mscale, s = sin((double)a) * mscale;
+      const double u = pre[hd * D + i], v = pre[hd * D + i + half];
+      out[hd * D + i] = u * c - v * s;
+      out[hd * D + i + half] = v * c + u * s;
+    }
+  free(pre);
+}

@@ -73,6 +73,16 @@ double spcref_attn_head(const void* q, const void* k, const void* v, int is_bf16
 double spcref_attn_merge_row(const double* o_parts, const double* lse_parts, int P, int D,
                              double* out);
 
+/* ---- NEXT-1: retrieval-head front-end (DESIGN R22-R24) ----
+ * RMSNorm of one bf16 row, HF Llama reading: r = 1/sqrt(mean(x^2) + eps) (fp64), t = bf16(fl32(x*r)),
+ * out = bf16(fl32(w*t)) (w = 1 when NULL). */
+void spcref_rmsnorm_bf16(const uint16_t* x, const uint16_t* w, int H, double eps, uint16_t* out);
+/* Projection + RoPE of one request in fp64: pre[n] = sum_h W[n][h]*xn[h], bound[n] = sum_h |W[n][h]*xn[h]|,
+ * pairs (i, i+D/2) of each of the N/D heads rotated by a = fl32(pos*inv_freq[i]),
+ * c = cos(a)*mscale, s = sin(a)*mscale: out[i] = pre[i]c - pre[i+D/2]s, out[i+D/2] = pre[i+D/2]c + pre[i]s. */
+void spcref_rethead_qk(const uint16_t* W, int N, int H, const uint16_t* xn, const float* inv_freq, int D,
+                       int pos, double mscale, double* out, double* bound);
+
 #ifdef __cplusplus
 }
 #endif

@@ -27,7 +27,7 @@ EXPORTS = [
     "spc_score_workspace", "spc_score", "spc_topk_workspace", "spc_topk",
     "spc_topk_merge_workspace", "spc_topk_merge", "spc_topk_filter", "spc_elastic_diff",
     "spc_gather_kv", "spc_gather_kv_strided", "spc_attn_workspace", "spc_sparse_decode_attn",
-    "spc_attn_merge", "spc_select",
+    "spc_attn_merge", "spc_select", "spc_rethead_qk",
 ]
 
 
@@ -66,6 +66,8 @@ def load_library(path: str = LIB_PATH):
                                 P]
     L.spc_gather_kv_strided.argtypes = [i32, P, P, ctypes.c_longlong, ctypes.c_longlong, i32, i32,
                                         i32, i32, i32, i32, i32, P, P, P, P, P, P]
+    L.spc_rethead_qk.argtypes = [P, P, i32, i32, P, f32, P, P, f32, P, i32, i32, i32, i32, i32,
+                                 P, P, P, P, P]
     L.spc_attn_workspace.argtypes = [i32, i32, i32, i32, i32]
     L.spc_attn_workspace.restype = sz
     L.spc_sparse_decode_attn.argtypes = [i32, P, P, P, i32, P, P, i32, i32, i32, i32, i32, i32,
@@ -209,6 +211,19 @@ def gather_kv_strided(k_src_tab, v_src_tab, row_stride: int, bg_stride: int, L: 
                                        int(bg_stride), L, B, G, D, k, layer_begin, layer_end,
                                        _p(load_tok), _p(load_slot), _p(n_load), _p(k_buf_tab),
                                        _p(v_buf_tab), _s(stream)), "spc_gather_kv_strided")
+
+
+def rethead_qk(token, emb, norm_w, eps: float, w_qk, inv_freq, mscale: float, pos, Hq: int,
+               G: int, q_out, kr, seq_len_out=None, x_out=None, stream=None):
+    """spc_rethead_qk: embedding -> RMSNorm -> Q/K projection -> RoPE -> K append."""
+    V, H = emb.shape
+    B = token.numel()
+    D = q_out.shape[-1]
+    Smax = kr.shape[2]
+    _check(lib().spc_rethead_qk(_p(token), _p(emb), V, H, _p(norm_w), float(eps), _p(w_qk),
+                                _p(inv_freq), float(mscale), _p(pos), B, Hq, G, D, Smax,
+                                _p(q_out), _p(kr), _p(seq_len_out), _p(x_out), _s(stream)),
+           "spc_rethead_qk")
 
 
 def sparse_decode_attn(q, k_tab, v_tab, kv_mode: int, idx, count, rows: int, k: int, scale: float,

@@ -135,3 +135,20 @@ def duplicate_rows(kr: torch.Tensor, n_dup: int, seed: int) -> torch.Tensor:
 def bf16_bits(t: torch.Tensor):
     """Raw bf16 bit patterns as a numpy uint16 array on the host."""
     return t.detach().contiguous().cpu().view(torch.int16).numpy().view("uint16")
+
+
+def retrieval_head_weights(V: int, H: int, Hq: int, G: int, D: int, seed: int, device="cpu"):
+    """Random-init weights of the retrieval head's front-end (NEXT-1; the trained EAGLE-3 DLM
+    weights are out of scope): embedding [V][H] ~ N(0, 1), RMSNorm weight [H] ~
+    1 + N(0, 0.05^2), W_qk [(Hq+G)*D][H] ~ N(0, 1/H) (unit-variance projections), all bf16."""
+    emb = normal_bf16((V, H), seed * 11 + 1, device)
+    norm_w = (1.0 + 0.05 * normal_bf16((H,), seed * 11 + 2, device, torch.float32)).to(torch.bfloat16)
+    w_qk = (normal_bf16(((Hq + G) * D, H), seed * 11 + 3, device, torch.float32)
+            * (1.0 / math.sqrt(H))).to(torch.bfloat16)
+    return emb, norm_w, w_qk
+
+
+def tokens(steps: int, B: int, V: int, seed: int, device="cpu") -> torch.Tensor:
+    """Token ids [steps][B] int32, uniform over the vocabulary."""
+    g = _gen(seed * 11 + 4, "cpu")
+    return torch.randint(0, V, (steps, B), generator=g, dtype=torch.int32).to(device)
