@@ -38,8 +38,9 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default=None,
                     help="A/B (single GPU, replicas for N>1), C (B=16, growing 128K context), "
-                         "D (KV in pinned host memory, B=4) or E (context-sharded); default B "
-                         "at N=1, E at N>1")
+                         "D (KV in pinned host memory, B=4), E (context-sharded) or R (the "
+                         "retrieval head's front-end, NEXT-1); default B at N=1, E at N>1")
+    ap.add_argument("--batch", type=int, default=1, help="config R: requests per step (<= 16)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--kv-layout", default="token", choices=["token", "layer"],
                     help="config D host KV layout: token-major records (one contiguous record "
@@ -758,6 +759,131 @@ def bench_offload(args):
     }), flush=True)
 
 
+def bench_frontend(args):
+    """Config R: the retrieval head's front-end spc_rethead_qk at the
+    config-B retrieval-head shape (Llama-3-8B: vocabulary 128,256, hidden 4,096, 32 query /
+    8 key heads of 128, YaRN x64 over a 2k original context), random-init weights.  Step =
+    one token per request: embedding -> RMSNorm -> Q/K projection (40 MiB of bf16 weights)
+    -> RoPE -> K append.  HBM-bound GEMV: roofline bytes = weights + embedding rows + writes.
+    Four address-distinct weight copies (160 MiB > L2) are rotated launch by launch, in a CUDA
+    graph of 4 launches."""
+    import torch
+
+    import oracle
+    from paper_2512_00722_b200 import build as spc_build
+    from paper_2512_00722_b200 import rope, spc, synth
+
+    if not os.path.exists(spc.LIB_PATH) or not spc_build.up_to_date():
+        spc_build.build()
+    dev = torch.device("cuda", 0)
+    B, V, H, Hq, G, D = args.batch, 128256, 4096, 32, 8, 128
+    Smax, NC = 32768 + 64, 4
+    seed = synth.BASE_SEED + 5
+    emb, norm_w, w0 = synth.retrieval_head_weights(V, H, Hq, G, D, seed, device=dev)
+    ws = [w0] + [w0.clone() for _ in range(NC - 1)]
+    inv, mscale = rope.yarn_inv_freq(D, factor=64.0, orig_ctx=2048)
+    inv_d = torch.from_numpy(inv).to(dev)
+    toks = synth.tokens(NC, B, V, seed, device=dev)
+    pos = torch.full((B,), 32768, dtype=torch.int32, device=dev)
+    q = torch.zeros((B, Hq, D), dtype=torch.bfloat16, device=dev)
+    kr = torch.zeros((B, G, Smax, D), dtype=torch.bfloat16, device=dev)
+    sl = torch.zeros(B, dtype=torch.int32, device=dev)
+    stream = torch.cuda.Stream()
+
+    def call(i, st=None):
+        spc.rethead_qk(toks[i % NC], emb, norm_w, 1e-5, ws[i % NC], inv_d, mscale, pos, Hq, G,
+                       q, kr, seq_len_out=sl, stream=st)
+
+    with torch.cuda.stream(stream):
+        for i in range(NC):
+            call(i, stream)
+        stream.synchronize()
+        g = torch.cuda.CUDAGraph()
+        n0 = spc.launch_count()
+        with torch.cuda.graph(g, stream=stream):
+            for i in range(NC):
+                call(i, stream)
+        per_replay = spc.launch_count() - n0
+        for _ in range(max(1, args.warmup)):
+            g.replay()
+        stream.synchronize()
+        reps = max(1, args.steps // NC)
+        sampler = ClockSampler(0)
+        sampler.start()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(reps):
+            g.replay()
+        e1.record(stream)
+        stream.synchronize()
+        clocks = sampler.stop()
+    n_launch = reps * NC
+    us = e0.elapsed_time(e1) * 1e3 / n_launch
+    wbytes = (Hq + G) * D * H * 2
+    alg = wbytes + B * H * 2 + B * (Hq + G) * D * 2
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    achieved = alg / (us * 1e-6) / 1e9
+    # e2e through the public call: token ids and positions from pinned host memory, the
+    # query read back, every step
+    tok_h = toks.cpu().pin_memory()
+    pos_h = pos.cpu().pin_memory()
+    q_h = torch.empty(q.shape, dtype=q.dtype).pin_memory()
+    tok_d = torch.empty_like(toks[0])
+    e2 = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    with torch.cuda.stream(stream):
+        e2[0].record(stream)
+        for i in range(args.steps):
+            tok_d.copy_(tok_h[i % NC], non_blocking=True)
+            pos.copy_(pos_h, non_blocking=True)
+            spc.rethead_qk(tok_d, emb, norm_w, 1e-5, ws[i % NC], inv_d, mscale, pos, Hq, G, q,
+                           kr, seq_len_out=sl, stream=stream)
+            q_h.copy_(q, non_blocking=True)
+        e2[1].record(stream)
+        stream.synchronize()
+    e2e_us = e2[0].elapsed_time(e2[1]) * 1e3 / args.steps
+    # CPU baseline: the oracle's front-end (C, fp64 projection) on one request
+    import time
+    oracle.build()
+    wh = synth.bf16_bits(w0)
+    xh = synth.bf16_bits(emb[toks[0, :1].long()])
+    nwh = synth.bf16_bits(norm_w)
+    t0 = time.perf_counter()
+    n_cpu = 0
+    while time.perf_counter() - t0 < 3.0:
+        xn = oracle.rmsnorm_bf16(xh, nwh, 1e-5)
+        oracle.rethead_qk(wh, xn, inv, [32768], D, mscale=mscale)
+        n_cpu += 1
+    cpu_s = (time.perf_counter() - t0) / n_cpu
+    print(json.dumps({
+        "metric": METRIC, "value": B / (us * 1e-6), "unit": "tokens/s", "n_gpus": 1,
+        "steps": n_launch, "warmup": args.warmup, "ms_per_step": us * 1e-3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (seeded random-init retrieval-head weights; DESIGN.md §5)",
+        "config": {"workload": f"R: retrieval-head front-end (NEXT-1), Llama-3-8B shape "
+                               f"(V={V}, H={H}, Hq={Hq}, G={G}, d={D}), YaRN x64, batch={B}",
+                   "l2": f"{NC} address-distinct weight copies ({NC * wbytes / 2**20:.0f} MiB > "
+                         f"L2) rotated launch by launch",
+                   "algorithmic_bytes_per_step": alg, "front_end_us": us},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": None,
+                     "kernel": "rethead_kernel (spc_rethead_qk)",
+                     "algorithmic_bytes_per_launch": alg,
+                     "peak_source": "measured (MEASURED_PEAKS.json hbm_gbs)"},
+        "cpu_baseline": {"value": 1.0 / cpu_s, "unit": "tokens/s", "cores": 1, "kind": "oracle",
+                         "sample": f"{n_cpu} single-request front-end calls of the C oracle "
+                                   f"(RMSNorm + fp64 projection + RoPE) in {n_cpu * cpu_s:.1f} s"},
+        "e2e": {"value": B / (e2e_us * 1e-6), "unit": "tokens/s", "h2d_bytes_per_step": B * 8,
+                "d2h_bytes_per_step": B * Hq * D * 2},
+        "gpu_launches": per_replay * reps,
+        "clocks": clocks,
+    }), flush=True)
+
+
 def main():
     args = parse()
     if args.warmup < 3:
@@ -774,6 +900,8 @@ def main():
             bench_grow(args)
         elif args.config == "D":
             bench_offload(args)
+        elif args.config == "R":
+            bench_frontend(args)
         else:
             bench_ours(args)
 
