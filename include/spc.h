@@ -307,6 +307,41 @@ int spc_rethead_qk(const int32_t* token, const void* emb, int V, int H, const vo
                    const int32_t* pos, int B, int Hq, int G, int D, int Smax, void* q_out,
                    void* kr, int32_t* seq_len_out, void* x_out, spc_stream_t stream);
 
+/* ------------------------------------------------------------------------
+ * Adaptive memory management — HOST functions (no GPU work).
+ * Paper §6: Eq. 6-8, Algorithm 1 (thresholds at compile time) and
+ * Algorithm 2 (progressive per-layer offload during decode).  Readings R25-R27.
+ *   M_part(S, l_gpu) = trunc(runtime_factor * model_bytes)
+ *       + 2*bytes_per_elem*R*[(l_gpu + extra_layers)*S + (L - l_gpu)*B]*H*D   (Eq. 7;
+ *   Eq. 6 is l_gpu = L).  extra_layers: the paper's 1 + alpha (retrieval-head cache +
+ *   repeat_kv buffer); this framework never materialises repeat_kv, so 1.
+ * ---------------------------------------------------------------------- */
+typedef struct {
+  int64_t mem_gpu;        /* Mem_GPU, bytes */
+  int64_t model_bytes;    /* M_O + M_D, bytes */
+  double runtime_factor;  /* 1.3: runtime memory = 30% of the model */
+  int L, H, D;            /* LLM layers, KV heads, head dim */
+  int extra_layers;       /* KV layers besides the L of the LLM (paper: 1 + alpha) */
+  int R;                  /* concurrent requests */
+  int64_t B;              /* retrieval budget, tokens */
+  int bytes_per_elem;     /* 2 (fp16 / bf16): the KV coefficient 4 = 2 * 2 */
+} spc_plan_cfg;
+/* Eq. 7 in bytes (-1 on invalid arguments). */
+int64_t spc_plan_mem_part(const spc_plan_cfg* cfg, int64_t S, int l_gpu);
+/* Algorithm 1: thresholds[0..L]; S^T_i = floor((C - c*i*B) / (c*(L + extra - i))) with
+ * C = mem_gpu - trunc(runtime_factor*model_bytes), c = 2*bytes_per_elem*R*H*D (Eq. 7's
+ * coefficient on the B term, reading R25); INT64_MAX where no KV layer stays on the GPU.
+ * Errors: SPC_E_NULL, SPC_E_SHAPE, SPC_E_BUDGET (C <= 0). */
+int spc_plan_thresholds(const spc_plan_cfg* cfg, int64_t* thresholds);
+/* Eq. 8: the largest l_gpu in [0, L] with M_part(S, l_gpu) <= mem_gpu.  SPC_E_BUDGET (and
+ * *l_gpu = -1, *shortfall = M_part(S, 0) - mem_gpu) when even l_gpu = 0 does not fit. */
+int spc_plan_max_resident(const spc_plan_cfg* cfg, int64_t S, int* l_gpu, int64_t* shortfall);
+/* Algorithm 2, one check at sequence length S: while S >= thresholds[*l_cpu] and
+ * *l_cpu < L, offload layer L - *l_cpu - 1 (listed in offload_layers, may be NULL) and
+ * increment *l_cpu; *n_offload = layers offloaded by this call (0 = no action). */
+int spc_plan_step(const int64_t* thresholds, int L, int64_t S, int* l_cpu, int32_t* offload_layers,
+                  int* n_offload);
+
 #ifdef __cplusplus
 }
 #endif

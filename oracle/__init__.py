@@ -58,6 +58,14 @@ def lib():
         L.spcref_topk_row.restype = i32
         L.spcref_rmsnorm_bf16.argtypes = [P, P, i32, f64, P]
         L.spcref_rethead_qk.argtypes = [P, i32, i32, P, P, i32, i32, f64, P, P]
+        L.spcref_plan_mem.argtypes = [i64, f64, i32, i32, i32, i32, i32, i64, i32, i64, i32]
+        L.spcref_plan_mem.restype = i64
+        L.spcref_plan_thresholds_search.argtypes = [i64, i64, f64, i32, i32, i32, i32, i32, i64, i32,
+                                                    i64, P]
+        L.spcref_plan_max_resident.argtypes = [i64, i64, f64, i32, i32, i32, i32, i32, i64, i32, i64]
+        L.spcref_plan_max_resident.restype = i32
+        L.spcref_plan_step.argtypes = [P, i32, i64, i32, P, P]
+        L.spcref_plan_step.restype = i32
         L.spcref_composite.argtypes = [f32, ctypes.c_int32]
         L.spcref_composite.restype = ctypes.c_uint64
         L.spcref_elastic_diff_row.argtypes = [P, i32, P, i32, i32, P, P, P, P, P, P]
@@ -289,3 +297,33 @@ def rethead_qk(W, xn, inv_freq, pos, D: int, mscale: float = 1.0):
         lib().spcref_rethead_qk(_p(W), N, H, _p(xn[b]), _p(inv), D, int(pos[b]), float(mscale),
                                 _p(out[b]), _p(bound[b]))
     return out, bound
+
+
+# ---------------------------------------------------------------- NEXT-2 planner
+def _plan_args(c):
+    return (int(c["model_bytes"]), float(c.get("runtime_factor", 1.3)), int(c["L"]), int(c["H"]),
+            int(c["D"]), int(c["extra_layers"]), int(c["R"]), int(c["B"]),
+            int(c.get("bytes_per_elem", 2)))
+
+
+def plan_mem(c, S: int, l_gpu: int) -> int:
+    """Eq. 7 (Eq. 6 at l_gpu = L) for a planner config dict c."""
+    return int(lib().spcref_plan_mem(*_plan_args(c), int(S), int(l_gpu)))
+
+
+def plan_thresholds_search(c, s_cap: int = 1 << 40):
+    th = np.zeros(int(c["L"]) + 1, np.int64)
+    lib().spcref_plan_thresholds_search(int(c["mem_gpu"]), *_plan_args(c), int(s_cap), _p(th))
+    return th
+
+
+def plan_max_resident(c, S: int) -> int:
+    return int(lib().spcref_plan_max_resident(int(c["mem_gpu"]), *_plan_args(c), int(S)))
+
+
+def plan_step(th, L: int, S: int, l_cpu: int):
+    th = np.ascontiguousarray(np.asarray(th, np.int64))
+    out = np.zeros(L, np.int32)
+    n = np.zeros(1, np.int32)
+    lc = int(lib().spcref_plan_step(_p(th), L, int(S), int(l_cpu), _p(out), _p(n)))
+    return lc, out[:int(n[0])].tolist()

@@ -389,3 +389,64 @@ void spcref_rethead_qk(const uint16_t* W, int N, int H, const uint16_t* xn, cons
     }
   free(pre);
 }
+
+/* =====================================================================
+ * NEXT-2: adaptive memory management, paper §6.  Eq. 6/7: the model
+ * with 30% runtime memory plus the KV cache, coefficient 2 bytes x (K, V) = 4
+ * at fp16, (L_GPU + 1 + alpha) resident layers (the retrieval head's layer and
+ * the repeat_kv buffer; `extra_layers` = 1 + alpha) and a B-row buffer for each
+ * offloaded layer.  Algorithm 1 is checked here by SEARCH over S, Eq. 8 by a linear scan.
+ * ===================================================================== */
+int64_t spcref_plan_mem(int64_t model_bytes, double runtime_factor, int L, int H, int D, int extra_layers,
+                        int R, int64_t B, int bytes_per_elem, int64_t S, int l_gpu) {
+  const int64_t m_model = (int64_t)(runtime_factor * (double)model_bytes);
+  const int64_t per_tok_layer = (int64_t)2 * bytes_per_elem * R * H * D; /* K and V */
+  const int64_t resident = (int64_t)(l_gpu + extra_layers) * S * per_tok_layer;
+  const int64_t buffers = (int64_t)(L - l_gpu) * B * per_tok_layer;
+  return m_model + resident + buffers;
+}
+
+void spcref_plan_thresholds_search(int64_t mem_gpu, int64_t model_bytes, double runtime_factor, int L, int H,
+                                   int D, int extra_layers, int R, int64_t B, int bytes_per_elem,
+                                   int64_t s_cap, int64_t* th) {
+  const int64_t per_tok_layer = (int64_t)2 * bytes_per_elem * R * H * D;
+  if (s_cap > mem_gpu / per_tok_layer + 1) s_cap = mem_gpu / per_tok_layer + 1; /* no overflow */
+  for (int i = 0; i <= L; ++i) { /* i layers offloaded: l_gpu = L - i */
+    int64_t lo = -1, hi = s_cap;     /* invariant: fits(lo) or lo = -1; largest fitting S in [lo, hi] */
+    if (spcref_plan_mem(model_bytes, runtime_factor, L, H, D, extra_layers, R, B, bytes_per_elem, 0, L - i) >
+        mem_gpu) {
+      th[i] = -1;
+      continue;
+    }
+    lo = 0;
+    while (lo < hi) { /* monotone in S: binary search for the last S that fits */
+      const int64_t mid = lo + (hi - lo + 1) / 2;
+      if (spcref_plan_mem(model_bytes, runtime_factor, L, H, D, extra_layers, R, B, bytes_per_elem, mid,
+                          L - i) <= mem_gpu)
+        lo = mid;
+      else
+        hi = mid - 1;
+    }
+    th[i] = lo;
+  }
+}
+
+int spcref_plan_max_resident(int64_t mem_gpu, int64_t model_bytes, double runtime_factor, int L, int H, int D,
+                             int extra_layers, int R, int64_t B, int bytes_per_elem, int64_t S) {
+  int best = -1;
+  for (int l = 0; l <= L; ++l)
+    if (spcref_plan_mem(model_bytes, runtime_factor, L, H, D, extra_layers, R, B, bytes_per_elem, S, l) <=
+        mem_gpu)
+      best = l;
+  return best;
+}
+
+int spcref_plan_step(const int64_t* th, int L, int64_t S, int l_cpu, int32_t* out, int* n_out) {
+  int n = 0;
+  while (S >= th[l_cpu] && l_cpu < L) { /* Alg. 2 line 4, in the paper's order */
+    out[n++] = L - l_cpu - 1;          /* line 5: offload Layer_{L - L_CPU - 1} */
+    l_cpu = l_cpu + 1;                 /* line 6 */
+  }
+  *n_out = n;
+  return l_cpu;
+}

@@ -83,6 +83,21 @@ void spcref_rmsnorm_bf16(const uint16_t* x, const uint16_t* w, int H, double eps
 void spcref_rethead_qk(const uint16_t* W, int N, int H, const uint16_t* xn, const float* inv_freq, int D,
                        int pos, double mscale, double* out, double* bound);
 
+/* ---- NEXT-2: adaptive memory management (Eq. 6-8, Alg. 1-2; SPEC memory-planner) ----
+ * Eq. 7 term by term (Eq. 6: l_gpu = L); model term trunc(runtime_factor * model_bytes). */
+int64_t spcref_plan_mem(int64_t model_bytes, double runtime_factor, int L, int H, int D, int extra_layers,
+                        int R, int64_t B, int bytes_per_elem, int64_t S, int l_gpu);
+/* Alg. 1 by SEARCH (not the closed form): th[i] = the largest S >= 0 with
+ * M_part(S, L - i) <= mem_gpu, or -1 if none (S searched in [0, s_cap]). */
+void spcref_plan_thresholds_search(int64_t mem_gpu, int64_t model_bytes, double runtime_factor, int L, int H,
+                                   int D, int extra_layers, int R, int64_t B, int bytes_per_elem,
+                                   int64_t s_cap, int64_t* th);
+/* Eq. 8 by linear scan from l_gpu = 0 upward: the largest feasible l_gpu, -1 if none. */
+int spcref_plan_max_resident(int64_t mem_gpu, int64_t model_bytes, double runtime_factor, int L, int H, int D,
+                             int extra_layers, int R, int64_t B, int bytes_per_elem, int64_t S);
+/* Alg. 2, lines 4-7, at sequence length S: returns the new L_CPU; offloaded layers in out. */
+int spcref_plan_step(const int64_t* th, int L, int64_t S, int l_cpu, int32_t* out, int* n_out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -27,12 +27,21 @@ EXPORTS = [
     "spc_score_workspace", "spc_score", "spc_topk_workspace", "spc_topk",
     "spc_topk_merge_workspace", "spc_topk_merge", "spc_topk_filter", "spc_elastic_diff",
     "spc_gather_kv", "spc_gather_kv_strided", "spc_attn_workspace", "spc_sparse_decode_attn",
-    "spc_attn_merge", "spc_select", "spc_rethead_qk",
+    "spc_attn_merge", "spc_select", "spc_rethead_qk", "spc_plan_mem_part",
+    "spc_plan_thresholds", "spc_plan_max_resident", "spc_plan_step",
 ]
 
 
 class SpcError(RuntimeError):
     pass
+
+
+class PlanCfg(ctypes.Structure):
+    """spc_plan_cfg (include/spc.h): inputs of the adaptive memory planner (Eq. 6-8)."""
+    _fields_ = [("mem_gpu", ctypes.c_int64), ("model_bytes", ctypes.c_int64),
+                ("runtime_factor", ctypes.c_double), ("L", ctypes.c_int), ("H", ctypes.c_int),
+                ("D", ctypes.c_int), ("extra_layers", ctypes.c_int), ("R", ctypes.c_int),
+                ("B", ctypes.c_int64), ("bytes_per_elem", ctypes.c_int)]
 
 
 _lib = None
@@ -68,6 +77,13 @@ def load_library(path: str = LIB_PATH):
                                         i32, i32, i32, i32, i32, P, P, P, P, P, P]
     L.spc_rethead_qk.argtypes = [P, P, i32, i32, P, f32, P, P, f32, P, i32, i32, i32, i32, i32,
                                  P, P, P, P, P]
+    i64 = ctypes.c_int64
+    L.spc_plan_mem_part.argtypes = [ctypes.POINTER(PlanCfg), i64, i32]
+    L.spc_plan_mem_part.restype = i64
+    L.spc_plan_thresholds.argtypes = [ctypes.POINTER(PlanCfg), P]
+    L.spc_plan_max_resident.argtypes = [ctypes.POINTER(PlanCfg), i64, ctypes.POINTER(i32),
+                                        ctypes.POINTER(i64)]
+    L.spc_plan_step.argtypes = [P, i32, i64, ctypes.POINTER(i32), P, ctypes.POINTER(i32)]
     L.spc_attn_workspace.argtypes = [i32, i32, i32, i32, i32]
     L.spc_attn_workspace.restype = sz
     L.spc_sparse_decode_attn.argtypes = [i32, P, P, P, i32, P, P, i32, i32, i32, i32, i32, i32,
@@ -251,3 +267,42 @@ def attn_merge(o_parts, lse_parts, out, lse_out=None, stream=None):
     P, n, D = o_parts.shape
     _check(lib().spc_attn_merge(_p(o_parts), _p(lse_parts), P, n, D, _p(out), _p(lse_out),
                                 _s(stream)), "spc_attn_merge")
+
+
+# ------------------------------------------------------------------ adaptive memory planner
+def plan_cfg(mem_gpu, model_bytes, L, H, D, R, B, extra_layers=1, runtime_factor=1.3,
+             bytes_per_elem=2) -> PlanCfg:
+    return PlanCfg(int(mem_gpu), int(model_bytes), float(runtime_factor), int(L), int(H), int(D),
+                   int(extra_layers), int(R), int(B), int(bytes_per_elem))
+
+
+def plan_mem_part(cfg: PlanCfg, S: int, l_gpu: int) -> int:
+    return int(lib().spc_plan_mem_part(ctypes.byref(cfg), int(S), int(l_gpu)))
+
+
+def plan_thresholds(cfg: PlanCfg):
+    import numpy as np
+    out = np.zeros(cfg.L + 1, np.int64)
+    _check(lib().spc_plan_thresholds(ctypes.byref(cfg), out.ctypes.data_as(ctypes.c_void_p)),
+           "spc_plan_thresholds")
+    return out
+
+
+def plan_max_resident(cfg: PlanCfg, S: int):
+    """(l_gpu, shortfall); l_gpu = -1 when even l_gpu = 0 does not fit."""
+    lg, sf = ctypes.c_int(0), ctypes.c_int64(0)
+    rc = lib().spc_plan_max_resident(ctypes.byref(cfg), int(S), ctypes.byref(lg), ctypes.byref(sf))
+    if rc not in (0, 3):
+        _check(rc, "spc_plan_max_resident")
+    return lg.value, sf.value
+
+
+def plan_step(thresholds, L: int, S: int, l_cpu: int):
+    """Algorithm 2 at sequence length S: (new l_cpu, [offloaded layers])."""
+    import numpy as np
+    th = np.ascontiguousarray(np.asarray(thresholds, np.int64))
+    lc, n = ctypes.c_int(int(l_cpu)), ctypes.c_int(0)
+    lay = np.zeros(L, np.int32)
+    _check(lib().spc_plan_step(th.ctypes.data_as(ctypes.c_void_p), L, int(S), ctypes.byref(lc),
+                               lay.ctypes.data_as(ctypes.c_void_p), ctypes.byref(n)), "spc_plan_step")
+    return lc.value, lay[:n.value].tolist()
