@@ -348,6 +348,48 @@ def bench_ours(args):
         e2e_ms = float(t.item())
     e2e_val = B * world * args.steps / (e2e_ms / 1e3)
 
+    # ---- the same step started from token ids: the retrieval head's front-end (NEXT-1,
+    # spc_rethead_qk at the Llama-3-8B retrieval-head shape, random-init weights) writes the
+    # query and the newest key first; device-resident and end to end (host token ids in,
+    # attention output back)
+    fe = None
+    if key == "B":
+        from paper_2512_00722_b200 import rope
+        V, H = 128256, 4096
+        emb, norm_w, w_qk = synth.retrieval_head_weights(V, H, Hq, G, D, seed, device=dev)
+        inv, msc = rope.yarn_inv_freq(D, factor=64.0, orig_ctx=2048)
+        st.set_frontend(emb, norm_w, w_qk, torch.from_numpy(inv).to(dev), msc)
+        toks = synth.tokens(args.steps, B, V, seed, device=dev)
+        st.step(use_graph=False)
+        st.capture()
+        for j in range(args.warmup):
+            st.use_set(j % NSETS)
+            st.step(use_graph=True)
+        torch.cuda.synchronize()
+        e3 = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        e3[0].record(stream)
+        for j in range(args.steps):
+            st.use_set(j % NSETS)
+            st.tokens[st.parity].copy_(toks[j], non_blocking=True)
+            st.step(use_graph=True)
+        e3[1].record(stream)
+        torch.cuda.synchronize()
+        fe_ms = e3[0].elapsed_time(e3[1]) / args.steps
+        tok_h = toks.cpu().pin_memory()
+        e3[0].record(stream)
+        for j in range(args.steps):
+            st.use_set(j % NSETS)
+            fbi, fbo = st.step_host(tok_h[j], q_llm_h, out_h, use_graph=True)
+        st.sync_host()
+        e3[1].record(stream)
+        torch.cuda.synchronize()
+        fe_e2e_ms = e3[0].elapsed_time(e3[1]) / args.steps
+        fe = {"what": "step incl. the retrieval head's front-end (spc_rethead_qk: token ids -> "
+                      "query + newest key; NEXT-1)",
+              "us_per_step": fe_ms * 1e3, "tokens_per_s": B / (fe_ms * 1e-3),
+              "e2e_tokens_per_s": B / (fe_e2e_ms * 1e-3), "e2e_h2d_bytes_per_step": fbi,
+              "e2e_d2h_bytes_per_step": fbo}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = run_cpu_baseline(c, key)
@@ -368,7 +410,7 @@ def bench_ours(args):
                        "hbm_roofline_frac_step": step_bytes / (ms_per_step * 1e-3) / 1e9 / peak,
                        "phase_us": {p: round(acc[p] * 1e3, 2) for p in phases},
                        "elastic_reuse": round(1 - n_load_tot / max(1, cnt_tot), 4),
-                       "n_load_last_step": n_load_tot},
+                       "n_load_last_step": n_load_tot, "with_frontend": fe},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "kernel": "attn_bf16_kernel (spc_sparse_decode_attn, all layers)",

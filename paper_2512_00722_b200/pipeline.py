@@ -88,6 +88,7 @@ class DecodeStep:
         self.sets = [(self.kr, self.k_tab, self.v_tab, [self.k_layers, self.v_layers])]
         self.cur_set = 0
         self.graphs = {}
+        self.fe = None  # retrieval-head front-end (set_frontend)
 
     # the input buffers of the next step and the outputs of the most recent one
     @property
@@ -116,6 +117,18 @@ class DecodeStep:
         self.cur_set = i
         self.kr, self.k_tab, self.v_tab, _ = self.sets[i]
 
+    def set_frontend(self, emb, norm_w, w_qk, inv_freq, mscale: float, eps: float = 1e-5):
+        """Start every step with the retrieval head's front-end (spc_rethead_qk, NEXT-1): the
+        step then takes token ids (tokens[parity], [B] int32) instead of retrieval queries;
+        the front-end writes the query into q_rets[parity] and the token's key into row
+        seq_len - 1 of the retrieval key cache (the newest position, Z6), then the step
+        scores it.  Graphs captured before this call are dropped."""
+        self.fe = dict(emb=emb, norm_w=norm_w, w_qk=w_qk, inv=inv_freq, mscale=float(mscale),
+                       eps=float(eps))
+        self.fe_pos = (self.seq_len - 1).to(torch.int32).contiguous()
+        self.tokens = [torch.zeros(self.B, dtype=torch.int32, device=self.dev) for _ in range(2)]
+        self.graphs = {}
+
     # ------------------------------------------------------------------ eager
     def enqueue(self, parity: int, stream=None, q_ret=None, q_llm=None):
         """Enqueue one step writing the selection into idx[parity] (prev = idx[1-parity]).
@@ -125,6 +138,11 @@ class DecodeStep:
         q_ret = self.q_rets[parity] if q_ret is None else q_ret
         q_llm = self.q_llms[parity] if q_llm is None else q_llm
         out, lse = self.outs[parity], self.lses[parity]
+        if self.fe is not None:  # token -> query + appended key (NEXT-1)
+            f = self.fe
+            spc.rethead_qk(self.tokens[parity], f["emb"], f["norm_w"], f["eps"], f["w_qk"], f["inv"],
+                           f["mscale"], self.fe_pos, self.Hq, self.G, q_ret, self.kr,
+                           stream=stream)
         if self.fused:
             # LOGITS, then NORM + GROUP + top-k + diff in one cluster launch (spc_select)
             spc.score(q_ret, self.kr, self.seq_len, self.G, self.scale, self.logits,
@@ -233,6 +251,7 @@ class DecodeStep:
         device->host read on another, ordered with events against the step's kernels, so
         consecutive calls overlap one step's copies with the neighbouring steps' kernels.
         `out_host` is complete after `sync_host()` (or a device synchronisation).
+        With a front-end (set_frontend) `q_ret_host` holds the step's token ids [B] int32.
         Returns (bytes host->device, bytes device->host)."""
         main = torch.cuda.current_stream(self.dev)
         if self._h2d is None:
@@ -244,7 +263,10 @@ class DecodeStep:
         if ("done", p) in ev:
             self._h2d.wait_event(ev[("done", p)])
         with torch.cuda.stream(self._h2d):
-            self.q_rets[p].copy_(q_ret_host, non_blocking=True)
+            if self.fe is not None:  # token ids instead of the retrieval query
+                self.tokens[p].copy_(q_ret_host, non_blocking=True)
+            else:
+                self.q_rets[p].copy_(q_ret_host, non_blocking=True)
             self.q_llms[p].copy_(q_llm_host, non_blocking=True)
             ev[("in", p)] = torch.cuda.Event()
             ev[("in", p)].record(self._h2d)

@@ -8,7 +8,7 @@ import numpy as np
 import pytest
 import torch
 
-from paper_2512_00722_b200 import synth
+from paper_2512_00722_b200 import spc, synth
 from paper_2512_00722_b200.pipeline import DecodeStep
 
 pytestmark = pytest.mark.gpu
@@ -116,3 +116,33 @@ def test_step_host_matches_device_steps():
         st2.sync_host()
         torch.cuda.synchronize()
         assert torch.equal(out_h, want[s].cpu()), s
+
+
+def test_step_with_frontend_equals_frontend_then_step():
+    """DecodeStep.set_frontend: the step from token ids (spc_rethead_qk writes the query and
+    the newest key row, then the usual step) is bit-identical to calling spc_rethead_qk by
+    hand into a copy of the key cache and stepping with that query."""
+    from paper_2512_00722_b200 import rope
+    B, G, Hq, D, S, L, k, V, H = 2, 2, 8, 64, 3000, 3, 256, 500, 512
+    dev = torch.device("cuda")
+    kr = synth.retrieval_keys(B, G, S, D, seed=5, device=dev)
+    kc, vc = synth.llm_kv(L, B, G, S, D, seed=5, device=dev)
+    ql = synth.llm_queries(1, L, B, Hq, D, seed=5, device=dev)[0]
+    seq = torch.tensor([S, S - 700], dtype=torch.int32, device=dev)
+    emb, nw, w = synth.retrieval_head_weights(V, H, Hq, G, D, 5, device=dev)
+    inv, m = rope.yarn_inv_freq(D, factor=8.0)
+    inv_d = torch.from_numpy(inv).to(dev)
+    toks = synth.tokens(3, B, V, 5, device=dev)
+    a = DecodeStep(kr.clone(), [kc[l] for l in range(L)], [vc[l] for l in range(L)], seq, L, Hq, k)
+    a.set_frontend(emb, nw, w, inv_d, m)
+    kr_b = kr.clone()
+    b = DecodeStep(kr_b, [kc[l] for l in range(L)], [vc[l] for l in range(L)], seq, L, Hq, k)
+    q = torch.zeros((B, Hq, D), dtype=torch.bfloat16, device=dev)
+    for i in range(3):
+        a.tokens[a.parity].copy_(toks[i])
+        ia, ca = a.step(q_llm=ql)
+        spc.rethead_qk(toks[i], emb, nw, 1e-5, w, inv_d, m, (seq - 1).contiguous(), Hq, G, q, kr_b)
+        ib, cb = b.step(q, ql)
+        torch.cuda.synchronize()
+        assert torch.equal(ia, ib) and torch.equal(ca, cb)
+        assert torch.equal(a.out, b.out) and torch.equal(a.kr, kr_b)
