@@ -95,10 +95,18 @@ uint64_t spc_launch_count(void);
  * head_sumfix [B][Hq]        int64     out (NORM)   / in (GROUP)
  * group_score [B][G][Smax]   f32       out (GROUP); may be NULL otherwise
  * ws          >= spc_score_workspace(B, Hq, Smax) bytes of device scratch
+ *   SPC_SCORE_BATCH (with GROUP): batch-level retrieval
+ *                     (Fig. 5(a)): one token set per
+ *                     request from the sum over ALL query heads of their weights,
+ *                     bs[b][t] = fl(...fl(p_0 + p_1) ... + p_{Hq-1}) (O5's p_h,
+ *                     ascending h, RN adds; O6b), written to every g of
+ *                     group_score[b][g][:] (so per-group top-k / diff / attention
+ *                     all select the same set).  Hq <= 128.
  * Supported: dtype SPC_BF16; D in {64, 128}; alpha in {1, 2, 4, 8};
  * Smax < SPC_MAX_SEQ.
  * ---------------------------------------------------------------------- */
-enum { SPC_SCORE_LOGITS = 1, SPC_SCORE_NORM = 2, SPC_SCORE_GROUP = 4, SPC_SCORE_ALL = 7 };
+enum { SPC_SCORE_LOGITS = 1, SPC_SCORE_NORM = 2, SPC_SCORE_GROUP = 4, SPC_SCORE_ALL = 7,
+       SPC_SCORE_BATCH = 16 /* with GROUP: batch-level retrieval, see below */ };
 size_t spc_score_workspace(int B, int Hq, int Smax);
 int spc_score(int dtype, const void* q, const void* kr, const int32_t* seq_len, int B, int Hq, int G,
               int D, int Smax, float scale, int phases, float* logits, float* head_max,

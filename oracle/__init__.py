@@ -66,6 +66,7 @@ def lib():
         L.spcref_plan_max_resident.restype = i32
         L.spcref_plan_step.argtypes = [P, i32, i64, i32, P, P]
         L.spcref_plan_step.restype = i32
+        L.spcref_batch_score.argtypes = [P, P, P, P, i32, i32, i32, P]
         L.spcref_composite.argtypes = [f32, ctypes.c_int32]
         L.spcref_composite.restype = ctypes.c_uint64
         L.spcref_elastic_diff_row.argtypes = [P, i32, P, i32, i32, P, P, P, P, P, P]
@@ -327,3 +328,16 @@ def plan_step(th, L: int, S: int, l_cpu: int):
     n = np.zeros(1, np.int32)
     lc = int(lib().spcref_plan_step(_p(th), L, int(S), int(l_cpu), _p(out), _p(n)))
     return lc, out[:int(n[0])].tolist()
+
+
+# ---------------------------------------------------------------- NEXT-3 batch-level
+def batch_score(lg, hm, F, seq_len):
+    """Batch-level score [B][Smax] (spcref_batch_score, O6b) from logits [B][Hq][Smax],
+    head_max [B][Hq], head_sumfix [B][Hq]."""
+    lg = np.ascontiguousarray(lg, np.float32)
+    B, Hq, Smax = lg.shape
+    out = np.zeros((B, Smax), np.float32)
+    lib().spcref_batch_score(_p(lg), _p(np.ascontiguousarray(hm, np.float32)),
+                             _p(np.ascontiguousarray(F, np.int64)),
+                             _p(np.ascontiguousarray(seq_len, np.int32)), B, Hq, Smax, _p(out))
+    return out

@@ -450,3 +450,28 @@ int spcref_plan_step(const int64_t* th, int L, int64_t S, int l_cpu, int32_t* ou
   *n_out = n;
   return l_cpu;
 }
+
+/* =====================================================================
+ * NEXT-3: batch-level retrieval.  Paper §4.2 (Fig. 5(a)): "the batch-level
+ * retrieval adopts a coarse-grained approach, retaining a single set of important tokens
+ * that apply to all attention heads"; sum the weights over all heads per
+ * position, then top-B.  The weights are O3-O5's; the sum runs over ascending h (O6b).
+ * ===================================================================== */
+void spcref_batch_score(const float* logits, const float* head_max, const int64_t* head_sumfix,
+                        const int32_t* seq_len, int B, int Hq, int Smax, float* out) {
+  for (int b = 0; b < B; ++b) {
+    const int S = seq_len[b];
+    for (int t = 0; t < Smax; ++t) {
+      float acc = 0.0f;
+      if (t < S)
+        for (int h = 0; h < Hq; ++h) {
+          const float m = head_max[(size_t)b * Hq + h];
+          const float l = (float)head_sumfix[(size_t)b * Hq + h] * 0x1p-40f;
+          const float r = 1.0f / l;
+          const float p = spcref_exp(logits[((size_t)b * Hq + h) * Smax + t] - m) * r;
+          acc = h == 0 ? p : acc + p;
+        }
+      out[(size_t)b * Smax + t] = acc;
+    }
+  }
+}

@@ -98,6 +98,11 @@ int spcref_plan_max_resident(int64_t mem_gpu, int64_t model_bytes, double runtim
 /* Alg. 2, lines 4-7, at sequence length S: returns the new L_CPU; offloaded layers in out. */
 int spcref_plan_step(const int64_t* th, int L, int64_t S, int l_cpu, int32_t* out, int* n_out);
 
+/* ---- NEXT-3: batch-level retrieval (Fig. 5(a); SPEC retrieve_batch_level S:125-132) ----
+ * out[b][t] = sum over h = 0..Hq-1 (ascending, fp32 RN adds) of O5's weight p_h(t); 0 for t >= S (O6b). */
+void spcref_batch_score(const float* logits, const float* head_max, const int64_t* head_sumfix,
+                        const int32_t* seq_len, int B, int Hq, int Smax, float* out);
+
 #ifdef __cplusplus
 }
 #endif

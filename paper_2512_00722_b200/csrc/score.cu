@@ -134,6 +134,48 @@ __global__ void __launch_bounds__(GRP_THREADS) group_kernel(
   }
 }
 
+// ---------------------------------------------------------- BATCH (O6b, NEXT-3)
+// Batch-level retrieval (Fig. 5(a); SPEC retrieve_batch_level S:125-132): one
+// token set per request from the SUM of every query head's weight, bs[t] = fl(...fl(p_0(t)
+// + p_1(t)) ... + p_{Hq-1}(t)) (O5's weights, ascending head order, RN adds), written to
+// all G rows of group_score so the per-group top-k / diff / attention select the same set.
+constexpr int BT_THREADS = 256;
+constexpr int BT_MAXH = 128;
+__global__ void __launch_bounds__(BT_THREADS) batch_kernel(
+    const float* __restrict__ logits, const float* __restrict__ head_max,
+    const int64_t* __restrict__ head_sumfix, const int32_t* __restrict__ seq_len, int Hq, int G,
+    int Smax, float* __restrict__ group_score) {
+  spc_pdl_entry();
+  __shared__ float sm_m[BT_MAXH], sm_r[BT_MAXH];
+  const int b = blockIdx.y;
+  for (int h = threadIdx.x; h < Hq; h += BT_THREADS) {
+    sm_m[h] = head_max[(size_t)b * Hq + h];
+    const float l = __fmul_rn(__ll2float_rn(head_sumfix[(size_t)b * Hq + h]),
+                              9.094947017729282379150390625e-13f);
+    sm_r[h] = __fdiv_rn(1.0f, l);
+  }
+  __syncthreads();
+  const int S = seq_len[b];
+  const int ta = blockIdx.x * (2 * BT_THREADS) + threadIdx.x, tb = ta + BT_THREADS;
+  if (ta >= Smax) return;
+  const float* lg = logits + (size_t)b * Hq * Smax;
+  float sa = 0.0f, sb = 0.0f;
+  for (int h = 0; h < Hq; ++h) {
+    const float m = sm_m[h];
+    const float xa = ta < S ? __ldcg(lg + (size_t)h * Smax + ta) : m;
+    const float xb = tb < S ? __ldcg(lg + (size_t)h * Smax + tb) : m;
+    const float2 e = spc_exp2_dev(__fsub_rn(xa, m), __fsub_rn(xb, m));
+    const float pa = __fmul_rn(e.x, sm_r[h]), pb = __fmul_rn(e.y, sm_r[h]);
+    sa = h ? __fadd_rn(sa, pa) : pa;
+    sb = h ? __fadd_rn(sb, pb) : pb;
+  }
+  for (int g = 0; g < G; ++g) {
+    float* out = group_score + ((size_t)b * G + g) * Smax;
+    out[ta] = ta < S ? sa : 0.0f;
+    if (tb < Smax) out[tb] = tb < S ? sb : 0.0f;
+  }
+}
+
 template <int D, int ALPHA>
 int launch_logits(const uint16_t* kr, const uint16_t* q, const int32_t* seq_len, int B, int G,
                   int Smax, float scale, float* logits, float* tile_max, unsigned* ctr,
@@ -207,7 +249,9 @@ extern "C" int spc_score(int dtype, const void* q, const void* kr, const int32_t
   if ((phases & SPC_SCORE_GROUP) && !group_score) return SPC_E_NULL;
   if (B <= 0 || Hq <= 0 || G <= 0 || Smax <= 0 || Hq % G) return SPC_E_SHAPE;
   if (Smax >= SPC_MAX_SEQ) return SPC_E_RANGE;
-  if (phases <= 0 || phases > SPC_SCORE_ALL) return SPC_E_RANGE;
+  if (phases <= 0 || phases > (SPC_SCORE_ALL | SPC_SCORE_BATCH)) return SPC_E_RANGE;
+  if ((phases & SPC_SCORE_BATCH) && (!(phases & SPC_SCORE_GROUP) || Hq > BT_MAXH))
+    return (phases & SPC_SCORE_GROUP) ? SPC_E_UNSUPPORTED : SPC_E_RANGE;
   if (dtype != SPC_BF16) return SPC_E_UNSUPPORTED;
   const int alpha = Hq / G;
   if (!(D == 64 || D == 128) || !(alpha == 1 || alpha == 2 || alpha == 4 || alpha == 8))
@@ -239,7 +283,11 @@ extern "C" int spc_score(int dtype, const void* q, const void* kr, const int32_t
                      seq_len, Hq, Smax, (unsigned long long*)w.tile_sum, w.cnt2, head_sumfix);
     SPC_TRY(launched());
   }
-  if (phases & SPC_SCORE_GROUP) {
+  if ((phases & SPC_SCORE_GROUP) && (phases & SPC_SCORE_BATCH)) {
+    dim3 grid((Smax + 2 * BT_THREADS - 1) / (2 * BT_THREADS), B);
+    SPC_TRY(launched(launch_k(batch_kernel, grid, dim3(BT_THREADS), 0, st, logits, head_max,
+                              head_sumfix, seq_len, Hq, G, Smax, group_score)));
+  } else if (phases & SPC_SCORE_GROUP) {
     switch (alpha) {
       case 1:
         SPC_TRY(launch_group<1>(logits, head_max, head_sumfix, seq_len, B, G, Smax,

@@ -25,17 +25,21 @@ class DecodeStep:
     def __init__(self, kr: torch.Tensor, k_layers, v_layers, seq_len: torch.Tensor, L: int,
                  Hq: int, k: int, mode: str = "indexed", force_last: bool = True, scale=None,
                  kv_rows=None, k_src_layers=None, v_src_layers=None, fused=None,
-                 src_rows=None, src_strides=None):
+                 src_rows=None, src_strides=None, retrieval: str = "head"):
         """kr: retrieval keys [B][G][Smax][D] bf16.  k_layers/v_layers: L tensors [B][G][rows][D]
         (INDEXED: the full caches; SLOTS: the budget buffers [B][G][k][D], with
         k_src_layers/v_src_layers the full caches, device or mapped host).  src_strides =
         (row_stride, bg_stride) in elements: the sources are strided views (e.g. the layers of
-        token-major KV records) and the elastic load uses spc_gather_kv_strided."""
+        token-major KV records) and the elastic load uses spc_gather_kv_strided.
+        retrieval: "head" (head-level, the paper's choice: group max) or "batch"
+        (batch-level: one set per request from the sum over all heads; NEXT-3)."""
+        assert retrieval in ("head", "batch")
+        self.retrieval = retrieval
         self.dev = kr.device
         # fused spc_select (one launch for NORM..diff) where it applies: INDEXED mode and
         # Smax <= 135168, a multiple of 4; otherwise the separate ABI calls
-        self.fused = (mode == "indexed" and kr.shape[2] <= 135168 and kr.shape[2] % 4 == 0) \
-            if fused is None else fused
+        self.fused = (mode == "indexed" and kr.shape[2] <= 135168 and kr.shape[2] % 4 == 0
+                      and retrieval == "head") if fused is None else fused
         self.B, self.G, self.Smax, self.D = kr.shape
         self.L, self.Hq, self.k = L, Hq, k
         self.alpha = Hq // self.G
@@ -154,7 +158,9 @@ class DecodeStep:
                        stream=stream)
         else:
             spc.score(q_ret, self.kr, self.seq_len, self.G, self.scale, self.logits,
-                      self.head_max, self.head_sumfix, self.gs, self.ws_score, stream=stream)
+                      self.head_max, self.head_sumfix, self.gs, self.ws_score,
+                      phases=spc.SCORE_ALL | (spc.SCORE_BATCH if self.retrieval == "batch" else 0),
+                      stream=stream)
             spc.topk(self.gs, self.seq_len, self.k, self.idx[cur], self.cnt[cur], self.ws_topk,
                      force_last=self.force_last, stream=stream)
             spc.elastic_diff(self.idx[prev], self.cnt[prev], self.idx[cur], self.cnt[cur],

@@ -18,7 +18,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libspc.so")
 
 BF16, F32 = 0, 1
-SCORE_LOGITS, SCORE_NORM, SCORE_GROUP, SCORE_ALL = 1, 2, 4, 7
+SCORE_LOGITS, SCORE_NORM, SCORE_GROUP, SCORE_ALL, SCORE_BATCH = 1, 2, 4, 7, 16
 KV_INDEXED, KV_SLOTS = 0, 1
 MAX_K = 4096
 

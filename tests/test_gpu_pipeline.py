@@ -146,3 +146,29 @@ def test_step_with_frontend_equals_frontend_then_step():
         torch.cuda.synchronize()
         assert torch.equal(ia, ib) and torch.equal(ca, cb)
         assert torch.equal(a.out, b.out) and torch.equal(a.kr, kr_b)
+
+
+def test_batch_level_step_selects_one_set_per_request(oracle):
+    """retrieval='batch' (NEXT-3): every KV group of a request attends to the same token set,
+    the oracle's top-k of the summed head weights; the attention matches the oracle."""
+    B, G, Hq, D, S, L, k = 2, 4, 16, 64, 2000, 2, 128
+    dev = torch.device("cuda")
+    kr = synth.retrieval_keys(B, G, S, D, seed=8, device=dev)
+    kc, vc = synth.llm_kv(L, B, G, S, D, seed=8, device=dev)
+    qr = synth.retrieval_queries(1, B, Hq, G, D, seed=8, device=dev)[0]
+    ql = synth.llm_queries(1, L, B, Hq, D, seed=8, device=dev)[0]
+    seq = torch.tensor([S, 1200], dtype=torch.int32, device=dev)
+    st = DecodeStep(kr, [kc[l] for l in range(L)], [vc[l] for l in range(L)], seq, L, Hq, k,
+                    retrieval="batch")
+    idx, cnt = st.step(qr, ql)
+    torch.cuda.synchronize()
+    olg, ohm, oF, _ = oracle.score(synth.bf16_bits(qr), synth.bf16_bits(kr), [S, 1200], G, st.scale)
+    obs = oracle.batch_score(olg, ohm, oF, [S, 1200])
+    oidx, _, ocnt, _ = oracle.topk(obs[:, None, :], [S, 1200], k, force_last=True)
+    oidx_g = np.repeat(oidx, G, axis=1)
+    ocnt_g = np.repeat(ocnt, G, axis=1)
+    assert np.array_equal(idx.cpu().numpy(), oidx_g) and np.array_equal(cnt.cpu().numpy(), ocnt_g)
+    kh, vh = synth.bf16_bits(kc), synth.bf16_bits(vc)
+    oo, _ = oracle.sparse_attn(synth.bf16_bits(ql), [kh[l] for l in range(L)],
+                               [vh[l] for l in range(L)], oidx_g, ocnt_g, st.scale)
+    assert float(np.abs(st.out.cpu().numpy() - oo).max()) <= 2e-3

@@ -143,3 +143,38 @@ def test_score_smax_not_multiple_of_4(oracle, Smax, lens):
     kr = synth.retrieval_keys(B, G, Smax, D, seed=Smax)
     q = synth.retrieval_queries(1, B, alpha * G, G, D, seed=Smax)[0]
     check(oracle, q, kr, lens, G, f32(1 / math.sqrt(D)))
+
+
+@pytest.mark.parametrize("Hq,G,Smax,seq_list", [(32, 8, 32768, [32768]), (8, 2, 1000, [1000, 513, 1]),
+                                                (4, 4, 3001, [3001, 17]), (64, 8, 2000, [2000])])
+def test_batch_level_score_and_topk(oracle, Hq, G, Smax, seq_list):
+    """SPC_SCORE_BATCH (NEXT-3): the batch-level score (sum of all heads' weights, O6b) is
+    bit-identical to the oracle on every group row, and the per-row top-k selects the
+    oracle's set in every group."""
+    dev = torch.device("cuda")
+    B, D, k = len(seq_list), 128, 256
+    kr = synth.retrieval_keys(B, G, Smax, D, seed=Hq + Smax)
+    q = synth.retrieval_queries(1, B, Hq, G, D, seed=Hq + Smax)[0]
+    scale = f32(1 / math.sqrt(D))
+    seq = torch.tensor(seq_list, dtype=torch.int32, device=dev)
+    lg = torch.zeros((B, Hq, Smax), dtype=torch.float32, device=dev)
+    hm = torch.zeros((B, Hq), dtype=torch.float32, device=dev)
+    F = torch.zeros((B, Hq), dtype=torch.int64, device=dev)
+    gs = torch.full((B, G, Smax), -1.0, dtype=torch.float32, device=dev)
+    ws = spc.alloc_workspace(spc.score_workspace(B, Hq, Smax), dev)
+    spc.score(q.to(dev), kr.to(dev), seq, G, scale, lg, hm, F, gs, ws,
+              phases=spc.SCORE_ALL | spc.SCORE_BATCH)
+    idx = torch.zeros((B, G, k), dtype=torch.int32, device=dev)
+    cnt = torch.zeros((B, G), dtype=torch.int32, device=dev)
+    wt = spc.alloc_workspace(spc.topk_workspace(B, G, Smax, k), dev)
+    spc.topk(gs, seq, k, idx, cnt, wt, force_last=True)
+    torch.cuda.synchronize()
+    olg, ohm, oF, _ = oracle.score(synth.bf16_bits(q), synth.bf16_bits(kr), seq_list, G, scale)
+    obs = oracle.batch_score(olg, ohm, oF, seq_list)
+    g = gs.cpu().numpy()
+    for gg in range(G):
+        assert np.array_equal(g[:, gg].view(np.uint32), obs.view(np.uint32)), gg
+    oidx, _, ocnt, _ = oracle.topk(obs[:, None, :], seq_list, k, force_last=True)
+    for gg in range(G):
+        assert np.array_equal(idx[:, gg].cpu().numpy(), oidx[:, 0])
+        assert np.array_equal(cnt[:, gg].cpu().numpy(), ocnt[:, 0])
