@@ -602,7 +602,8 @@ def bench_grow(args):
     qr = synth.retrieval_queries(nsteps + 1, B, Hq, G, D, seed=seed, device=dev)
     ql = synth.llm_queries(2, L, B, Hq, D, seed=seed, device=dev)
     seq = torch.full((B,), S0, dtype=torch.int32, device=dev)
-    st = DecodeStep(kr, k_layers, v_layers, seq, L, Hq, k, kv_rows=rows)
+    st = DecodeStep(kr, k_layers, v_layers, seq, L, Hq, k, kv_rows=rows,
+                    fused=None if os.environ.get("SPC_FUSED") is None else os.environ["SPC_FUSED"] == "1")
     st.step(qr[0], ql[0])
     n0 = spc.launch_count()
     seq_graphs = st.capture_sequence([(0, qr[i], ql[i % 2]) for i in range(nsteps)])

@@ -36,10 +36,15 @@ class DecodeStep:
         assert retrieval in ("head", "batch")
         self.retrieval = retrieval
         self.dev = kr.device
-        # fused spc_select (one launch for NORM..diff) where it applies: INDEXED mode and
-        # Smax <= 135168, a multiple of 4; otherwise the separate ABI calls
+        # fused spc_select (one launch for NORM..diff) where it applies: INDEXED mode, Smax <=
+        # 135168 and a multiple of 4, and every row's 8-CTA cluster resident in one wave
+        # (B*G*8 <= SMs); otherwise the separate ABI calls.  Measured: config B (8 rows)
+        # fused is faster; config C (128 rows: 7 waves of clusters) 2.03 ms fused vs 1.84 ms
+        # with the grid-wide NORM / GROUP kernels + cluster top-k + diff.
+        n_sm = torch.cuda.get_device_properties(kr.device).multi_processor_count
         self.fused = (mode == "indexed" and kr.shape[2] <= 135168 and kr.shape[2] % 4 == 0
-                      and retrieval == "head") if fused is None else fused
+                      and kr.shape[0] * kr.shape[1] * 8 <= n_sm and retrieval == "head") \
+            if fused is None else fused
         self.B, self.G, self.Smax, self.D = kr.shape
         self.L, self.Hq, self.k = L, Hq, k
         self.alpha = Hq // self.G
