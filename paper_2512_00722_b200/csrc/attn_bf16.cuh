@@ -52,8 +52,15 @@ constexpr int NSTAGE = SPC_ATTN_NSTAGE;  // per-warp ring depth (chunks in fligh
 constexpr int AT2_CTAS_PER_SM = SPC_ATTN_CTAS;
 constexpr int NWARP = 4;
 constexpr int AT2_THREADS = NWARP * 32;
-constexpr int TRING = 8;    // per-warp ring of prefetched chunk metadata
-constexpr int MAHEAD = 5;   // metadata fetched this many chunks before its rows are issued
+#ifndef SPC_ATTN_TRING
+#define SPC_ATTN_TRING 8
+#endif
+#ifndef SPC_ATTN_MAHEAD
+#define SPC_ATTN_MAHEAD 5
+#endif
+constexpr int TRING = SPC_ATTN_TRING;    // per-warp ring of prefetched chunk metadata
+constexpr int MAHEAD = SPC_ATTN_MAHEAD;  // metadata fetched this many chunks before its rows are issued
+static_assert(TRING >= MAHEAD + NSTAGE, "metadata ring too small");
 // the prefetch of chunk i + NSTAGE - 1 + PF at iteration i reads metadata that landed
 static_assert(SPC_ATTN_PF <= MAHEAD - NSTAGE, "prefetch needs landed metadata");
 

@@ -138,3 +138,20 @@ def test_attn_merge_parity(oracle):
     fin = np.isfinite(ol)
     assert np.array_equal(np.isfinite(lse.cpu().numpy()), fin)
     assert np.abs(lse.cpu().numpy()[fin] - ol[fin]).max() <= 1e-5
+
+
+def test_attn_maximum_budget(oracle):
+    """k = SPC_MAX_K (4096) selected rows per (layer, b, g) out of 50,000, ragged counts
+    (full / partial / one row), within the bf16 tolerance of the fp64 oracle."""
+    rng = np.random.default_rng(4096)
+    L, B, G, Hq, D, rows, k = 2, 1, 3, 12, 128, 50000, spc.MAX_K
+    kc, vc = synth.llm_kv(L, B, G, rows, D, seed=40)
+    q = synth.llm_queries(1, L, B, Hq, D, seed=40)[0]
+    idx = np.full((B, G, k), -1, np.int32)
+    cnt = np.array([[k, 2345, 1]], np.int32)
+    for g in range(G):
+        idx[0, g, :cnt[0, g]] = np.sort(rng.choice(rows, cnt[0, g], replace=False))
+    out, lse = run_attn(q, kc, vc, idx, cnt, k, 1.0 / math.sqrt(D))
+    oo, ol = oracle_attn(oracle, q, kc, vc, idx, cnt, 1.0 / math.sqrt(D))
+    assert np.abs(out - oo).max() <= TOL[torch.bfloat16]
+    assert np.abs(lse - ol).max() <= 1e-4

@@ -374,3 +374,20 @@ def test_fused_select_rejects_unsupported():
             spc.select(lg, z(B, Hq, dt=torch.float32), torch.tensor([S], dtype=torch.int32,
                        device=DEV), G, k, z(B, Hq, dt=torch.int64), z(B, G, S, dt=torch.float32),
                        z(B, G, k), z(B, G), z(B, G, k), z(B, G), z(B, G, k), z(B, G))
+
+
+def test_maximum_sizes(oracle):
+    """Upper limits of the ABI: k = SPC_MAX_K (4096) for the top-k, and the fused select at its
+    largest supported row (Smax = 135168) with k = 4096 -- bit-identical to the oracle / the
+    separate calls, with a ragged second request."""
+    rng = np.random.default_rng(11)
+    gs = rng.random((1, 2, 60000)).astype(np.float32) ** 4
+    check_topk(oracle, gs, [60000], spc.MAX_K, force=True)
+    B, G, Hq, S, k = 2, 1, 4, 135168, spc.MAX_K
+    g = torch.Generator(device="cpu").manual_seed(3)
+    lg = (torch.randn((B, Hq, S), generator=g) * 2).to(DEV)
+    seq = torch.tensor([S, 70001], dtype=torch.int32, device=DEV)
+    hm = torch.stack([lg[b, :, :int(seq[b])].amax(dim=1) for b in range(B)]).contiguous()
+    gsa, ia, ca = _select_both(lg, hm, seq, G, k)
+    oidx, _, ocnt, _ = oracle.topk(gsa.cpu().numpy(), seq.cpu().tolist(), k, force_last=True)
+    assert np.array_equal(ia.cpu().numpy(), oidx) and np.array_equal(ca.cpu().numpy(), ocnt)
