@@ -2,9 +2,9 @@
 //
 // Persistent, one CTA of LG_W warps per SM, every warp an autonomous cp.async
 // pipeline.  The retrieval-key cache [B*G][Smax][D] is cut into tiles of 128 rows;
-// warps claim tiles from ONE grid-wide counter (claims are prefetched one tile
-// ahead, so the atomic's latency hides behind the math), which balances the grid
-// to within one tile.  A tile is streamed in steps of 64 d (128 rows x 128 B =
+// warps claim tiles from ONE grid-wide counter (a warp's first tile is its grid-wide
+// warp index; later claims are prefetched one tile ahead, so the atomic's latency hides
+// behind the math), which balances the grid to within one tile.  A tile is streamed in steps of 64 d (128 rows x 128 B =
 // 16 KiB, 16-byte cp.async copies) through a per-warp 2-stage ring; rows are
 // stored unpadded with the 16-byte granule index XOR-swizzled by (row & 7), so the
 // lane-per-row LDS.128 reads are conflict-free.  A tile's first step also carries
@@ -74,9 +74,10 @@ __global__ void __launch_bounds__(32 * lg_warps<ALPHA>(), 1) logits_kernel(
 
   // ---- per-warp pipeline over steps (tile, chunk); tiles claimed from the grid counter
   int cur = 0, chunk = NCH;  // producer cursor
-  int nxt = 0;
-  if (lane == 0) nxt = atomicAdd(ctr, 1);
-  nxt = __shfl_sync(0xffffffffu, nxt, 0);
+  // the first tile of every warp is static (its grid-wide warp index: no atomic round trip
+  // before the first loads); later claims come from the counter, offset past those
+  const int nwarps = gridDim.x * LG_W;
+  int nxt = blockIdx.x * LG_W + warp;
   const int r_lane = lane / GPR, gr = lane % GPR;
   // swizzled destination granule for the two row parities of the copy pattern
   const uint32_t sw0 = (uint32_t)((gr ^ (r_lane & 7)) << 4), sw1 = (uint32_t)((gr ^ ((r_lane + 4) & 7)) << 4);
@@ -86,7 +87,7 @@ __global__ void __launch_bounds__(32 * lg_warps<ALPHA>(), 1) logits_kernel(
         cur = nxt;
         if (cur >= ntiles) break;
         int t = 0;
-        if (lane == 0) t = atomicAdd(ctr, 1);
+        if (lane == 0) t = (int)atomicAdd(ctr, 1u) + nwarps;
         nxt = __shfl_sync(0xffffffffu, t, 0);
         const int bg = cur / tpr;
         if ((cur - bg * tpr) * LG_TR < __ldg(seq_len + bg / G)) break;
