@@ -156,6 +156,163 @@ __global__ void __launch_bounds__(RH_WARPS * 32) rethead_kernel(
   }
 }
 
+// ---- Batched variant (5 <= B <= 16): the projection is a skinny GEMM, [(Hq+G)*D x H] x
+// [H x B], run on the tensor cores (mma.sync m16n8k16, bf16 in, fp32 accumulate).  An
+// m-tile holds 8 RoPE pairs of one head: rows i0 + gid (the pair's first row) and
+// i0 + D/2 + gid (its partner), so both rows a rotation mixes land in one lane's C
+// fragment.  The A operand comes straight from global memory: lane (gid, tig) loads the
+// 16-byte chunks tig + 4j of its two rows, and the k index inside every 16-wide MMA slice
+// is permuted consistently for A and B (the dot product is order-free across slices, and
+// each slice's 16 products are summed by the MMA), so no shared-memory staging or ldmatrix
+// is needed for the weights.  Persistent CTAs of 8 warps: each CTA normalises the B rows
+// once into shared memory; per m-tile each warp takes an H/8 slice and the 8 partial C
+// fragments meet in shared memory; warp 0 rotates and stores.
+constexpr int RM_WARPS = 8;
+__device__ __forceinline__ void rh_mma(float (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2,
+                                       uint32_t a3, uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, "
+      "{%8, %9}, {%0, %1, %2, %3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+template <int NT>  // n-tiles of 8 requests
+__global__ void __launch_bounds__(RM_WARPS * 32, 1) rethead_mma_kernel(
+    const int32_t* __restrict__ token, const uint16_t* __restrict__ emb, int H,
+    const uint16_t* __restrict__ norm_w, float eps, const uint16_t* __restrict__ w_qk,
+    const float* __restrict__ inv_freq, float mscale, const int32_t* __restrict__ pos, int B,
+    int Hq, int G, int D, int Smax, uint16_t* __restrict__ q_out, uint16_t* __restrict__ kr,
+    int32_t* __restrict__ seq_len_out, uint16_t* __restrict__ x_out) {
+  spc_pdl_entry();
+  extern __shared__ __align__(16) uint8_t rm_smem[];
+  uint16_t* xs = reinterpret_cast<uint16_t*>(rm_smem);  // [8 NT][H] (rows >= B zero)
+  __shared__ float red[RM_WARPS][NT][4][32];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int gid = lane >> 2, tig = lane & 3;
+  const int nchunk = H / 8;
+  // ---- RMSNorm of the B rows (warp b, b + 8, ...); rows B..8NT-1 are zero
+  for (int b = warp; b < 8 * NT; b += RM_WARPS) {
+    uint4* dstrow = reinterpret_cast<uint4*>(xs + (size_t)b * H);
+    if (b >= B) {
+      for (int c = lane; c < nchunk; c += 32) dstrow[c] = make_uint4(0, 0, 0, 0);
+      continue;
+    }
+    const uint4* x = reinterpret_cast<const uint4*>(emb + (size_t)token[b] * H);
+    float ss = 0.f;
+    for (int c = lane; c < nchunk; c += 32) {
+      const uint4 v = __ldg(x + c);
+      const uint32_t* pv = &v.x;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float lo = bf16lo(pv[e]), hi = bf16hi(pv[e]);
+        ss = fmaf(lo, lo, ss);
+        ss = fmaf(hi, hi, ss);
+      }
+    }
+    ss = warp_sum(ss);
+    const float r = 1.0f / sqrtf(ss / (float)H + eps);
+    for (int c = lane; c < nchunk; c += 32) {
+      const uint4 v = __ldg(x + c);
+      const uint4 wv = norm_w ? __ldg(reinterpret_cast<const uint4*>(norm_w) + c)
+                              : make_uint4(0x3f803f80u, 0x3f803f80u, 0x3f803f80u, 0x3f803f80u);
+      const uint32_t* pv = &v.x;
+      const uint32_t* pw = &wv.x;
+      uint32_t o[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float tl = bf16_to_f32(f32_to_bf16_rn(bf16lo(pv[e]) * r));
+        const float th = bf16_to_f32(f32_to_bf16_rn(bf16hi(pv[e]) * r));
+        o[e] = (uint32_t)f32_to_bf16_rn(bf16lo(pw[e]) * tl) |
+               ((uint32_t)f32_to_bf16_rn(bf16hi(pw[e]) * th) << 16);
+      }
+      const uint4 ov = make_uint4(o[0], o[1], o[2], o[3]);
+      dstrow[c] = ov;
+      if (x_out && blockIdx.x == 0) reinterpret_cast<uint4*>(x_out + (size_t)b * H)[c] = ov;
+    }
+  }
+  if (seq_len_out && blockIdx.x == 0 && tid < B) seq_len_out[tid] = pos[tid] + 1;
+  __syncthreads();
+
+  const int half = D / 2;
+  const int tiles = (Hq + G) * (half / 8);       // m-tiles: 8 pairs of one head
+  const int wch = nchunk / RM_WARPS;              // chunks of this warp's H slice
+  const uint32_t xs_s = smem_u32(xs);
+  for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+    const int hh = t / (half / 8), i0 = (t - hh * (half / 8)) * 8;
+    const uint4* wlo = reinterpret_cast<const uint4*>(w_qk + ((size_t)hh * D + i0 + gid) * H);
+    const uint4* whi = reinterpret_cast<const uint4*>(w_qk + ((size_t)hh * D + half + i0 + gid) * H);
+    float c[NT][4];
+#pragma unroll
+    for (int n = 0; n < NT; ++n) c[n][0] = c[n][1] = c[n][2] = c[n][3] = 0.f;
+    const int cbeg = warp * wch;
+    for (int j0 = 0; j0 < wch; j0 += 32) {      // 8 groups of 4 lanes' chunks in flight
+      uint4 alo[8], ahi[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int ch = cbeg + j0 + tig + 4 * u;
+        if (j0 + tig + 4 * u < wch) {
+          alo[u] = __ldcs(wlo + ch);
+          ahi[u] = __ldcs(whi + ch);
+        } else {
+          alo[u] = ahi[u] = make_uint4(0, 0, 0, 0);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int ch = cbeg + j0 + tig + 4 * u;
+        if (j0 + 4 * u >= wch) break;
+        const int chs = min(ch, nchunk - 1);
+#pragma unroll
+        for (int n = 0; n < NT; ++n) {
+          const uint4 xb = lds128(xs_s + (uint32_t)((((size_t)(n * 8 + gid)) * H + (size_t)chs * 8) * 2));
+          const bool ok = j0 + tig + 4 * u < wch;
+          // two MMA k-slices per 16-byte chunk: elements 0-3 then 4-7 (k permuted alike)
+          rh_mma(c[n], alo[u].x, ahi[u].x, alo[u].y, ahi[u].y, ok ? xb.x : 0u, ok ? xb.y : 0u);
+          rh_mma(c[n], alo[u].z, ahi[u].z, alo[u].w, ahi[u].w, ok ? xb.z : 0u, ok ? xb.w : 0u);
+        }
+      }
+    }
+#pragma unroll
+    for (int n = 0; n < NT; ++n)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) red[warp][n][e][lane] = c[n][e];
+    __syncthreads();
+    if (warp == 0) {
+      const int i = i0 + gid;
+      const float inv = inv_freq[i];
+#pragma unroll
+      for (int n = 0; n < NT; ++n) {
+        float s[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          float v = 0.f;
+#pragma unroll
+          for (int w = 0; w < RM_WARPS; ++w) v += red[w][n][e][lane];
+          s[e] = v;
+        }
+#pragma unroll
+        for (int col = 0; col < 2; ++col) {  // C columns 2 tig + col = request
+          const int b = n * 8 + 2 * tig + col;
+          if (b < B) {
+            const float u = s[col], vv = s[2 + col];  // row gid: pair first, gid + 8: partner
+            const int pb = pos[b];
+            float sn, cs;
+            sincosf((float)pb * inv, &sn, &cs);
+            cs *= mscale;
+            sn *= mscale;
+            uint16_t* dst = hh < Hq ? q_out + ((size_t)b * Hq + hh) * D
+                                    : kr + (((size_t)b * G + (hh - Hq)) * Smax + pb) * D;
+            dst[i] = f32_to_bf16_rn(u * cs - vv * sn);
+            dst[i + half] = f32_to_bf16_rn(vv * cs + u * sn);
+          }
+        }
+      }
+    }
+    __syncthreads();  // red[] is rewritten by the next tile
+  }
+}
+
 }  // namespace
 }  // namespace spc
 
@@ -190,6 +347,30 @@ extern "C" int spc_rethead_qk(const int32_t* token, const void* emb, int V, int 
   }
   if (B == 1) RH(1)
   if (B <= 4) RH(4)
+  if (H % (8 * RM_WARPS) == 0 && (D / 2) % 8 == 0) {  // tensor-core batched path
+    const int nt = B <= 8 ? 1 : 2;
+    const size_t msm = (size_t)8 * nt * H * 2;
+    if (msm <= 200 * 1024) {
+      const int tiles = (Hq + G) * (D / 2 / 8);
+      const int nct = std::max(1, std::min(num_sms(), tiles));
+#define RM(NT)                                                                                    \
+  {                                                                                               \
+    static bool rm_attr = false;                                                                  \
+    if (!rm_attr) {                                                                               \
+      cudaFuncSetAttribute(rethead_mma_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,   \
+                           200 * 1024);                                                           \
+      rm_attr = true;                                                                             \
+    }                                                                                             \
+    return launched(launch_k(rethead_mma_kernel<NT>, dim3(nct), dim3(RM_WARPS * 32), msm, st,    \
+                             token, (const uint16_t*)emb, H, (const uint16_t*)norm_w, eps,        \
+                             (const uint16_t*)w_qk, inv_freq, mscale, pos, B, Hq, G, D, Smax,     \
+                             (uint16_t*)q_out, (uint16_t*)kr, seq_len_out, (uint16_t*)x_out));    \
+  }
+      if (nt == 1) RM(1)
+      RM(2)
+#undef RM
+    }
+  }
   RH(16)
 #undef RH
 }

@@ -3,7 +3,8 @@ K append) against the CPU oracle.  The normalised input xn must equal the oracle
 except for rare one-ulp flips (the oracle's rms is fp64, the kernel's fp32); q and the
 appended key row are then checked against the oracle's fp64 projection + rotation OF THE
 KERNEL'S OWN xn, within a rigorous bound: bf16 output rounding (2^-8 |ref|) + fp32
-accumulation over H terms ((H + 16) 2^-24 mscale (sum|W_u x| + sum|W_v x|))."""
+accumulation over H terms ((H + 16) 2^-24 mscale (sum|W_u x| + sum|W_v x|)), times 4 for the
+tensor-core path of B > 4 (fp32 MMA accumulation: exact products, sums within ~2 ulps)."""
 import numpy as np
 import pytest
 import torch
@@ -36,6 +37,8 @@ def run(B, H, Hq, G, D, V, Smax, pos, factor=1.0, seed=1, norm=True):
     (3, 512, 8, 2, 64, 300, 50, [0, 49, 7], 4.0),           # D = 64, pos 0 and Smax-1
     (16, 1024, 4, 1, 128, 64, 40, list(range(0, 40, 40 // 16 + 1))[:16] + [39] * 0, 32.0),
     (2, 2048, 16, 2, 128, 50, 1 << 20, [1_000_000, 1], 64.0),  # 1M positions (config E)
+    (8, 4096, 32, 8, 128, 300, 64, [63, 0, 5, 9, 11, 2, 40, 41], 64.0),  # tensor-core path
+    (12, 4096, 16, 4, 64, 300, 128, list(range(3, 120, 10)), 8.0),      # two n-tiles, D = 64
 ])
 def test_rethead_matches_oracle(B, H, Hq, G, D, V, Smax, pos, factor):
     pos = (pos + [5] * B)[:B]
@@ -51,7 +54,8 @@ def test_rethead_matches_oracle(B, H, Hq, G, D, V, Smax, pos, factor):
     half = D // 2
     bnd = bound.reshape(B, Hq + G, 2, half)
     pair = np.concatenate([bnd.sum(2, keepdims=True)] * 2, axis=2).reshape(B, -1)
-    tol = 2.0 ** -8 * np.abs(out) + (H + 16) * 2.0 ** -24 * m * pair
+    acc = 4.0 if B > 4 else 1.0
+    tol = 2.0 ** -8 * np.abs(out) + acc * (H + 16) * 2.0 ** -24 * m * pair
     got_q = q.float().cpu().numpy().reshape(B, Hq * D)
     got_k = np.stack([kr[b, :, pos[b]].float().cpu().numpy().reshape(-1) for b in range(B)])
     got = np.concatenate([got_q, got_k], axis=1)
