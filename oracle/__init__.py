@@ -67,6 +67,8 @@ def lib():
         L.spcref_plan_step.argtypes = [P, i32, i64, i32, P, P]
         L.spcref_plan_step.restype = i32
         L.spcref_batch_score.argtypes = [P, P, P, P, i32, i32, i32, P]
+        L.spcref_mla_head.argtypes = [P, P, P, P, P, i32, i32, i32, i32, i32, f64, P]
+        L.spcref_mla_head.restype = f64
         L.spcref_composite.argtypes = [f32, ctypes.c_int32]
         L.spcref_composite.restype = ctypes.c_uint64
         L.spcref_elastic_diff_row.argtypes = [P, i32, P, i32, i32, P, P, P, P, P, P]
@@ -341,3 +343,18 @@ def batch_score(lg, hm, F, seq_len):
                              _p(np.ascontiguousarray(F, np.int64)),
                              _p(np.ascontiguousarray(seq_len, np.int32)), B, Hq, Smax, _p(out))
     return out
+
+
+# ---------------------------------------------------------------- NEXT-3 MLA
+def mla_head(q, cache, w_uk, w_uv, rows, DC: int, DR: int, scale: float):
+    """One head: select-then-expand MLA attention (spcref_mla_head) -> (o [DV] f64, lse)."""
+    q = np.ascontiguousarray(_bf16_bits(q))
+    cache = np.ascontiguousarray(_bf16_bits(cache))
+    w_uk = np.ascontiguousarray(_bf16_bits(w_uk))
+    w_uv = np.ascontiguousarray(_bf16_bits(w_uv))
+    rows = np.ascontiguousarray(np.asarray(rows, np.int32))
+    DN, DV = w_uk.shape[0], w_uv.shape[0]
+    out = np.zeros(DV, np.float64)
+    lse = lib().spcref_mla_head(_p(q), _p(cache), _p(w_uk), _p(w_uv), _p(rows), len(rows), DC, DR,
+                                DN, DV, float(scale), _p(out))
+    return out, lse

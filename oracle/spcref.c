@@ -475,3 +475,46 @@ void spcref_batch_score(const float* logits, const float* head_max, const int64_
     }
   }
 }
+
+/* =====================================================================
+ * NEXT-3: MLA select-then-expand.  Paper §4.3: "MLA caches a lower-dimensional
+ * latent representation c ... only the selected c cache is subjected to the increase in
+ * dimension" (Fig. 5(e)); the retrieval stays head-level as for MHA.  Written in the paper's
+ * order: expand the selected rows, then the attention of O10 over them (fp64).
+ * ===================================================================== */
+double spcref_mla_head(const uint16_t* q, const uint16_t* cache, const uint16_t* w_uk,
+                       const uint16_t* w_uv, const int32_t* rows, int n, int DC, int DR, int DN,
+                       int DV, double scale, double* out) {
+  const int W = DC + DR;
+  for (int d = 0; d < DV; ++d) out[d] = 0.0;
+  if (n <= 0) return -INFINITY;
+  double* z = (double*)malloc(sizeof(double) * (size_t)n);
+  double* vexp = (double*)malloc(sizeof(double) * (size_t)n * DV);
+  double m = -INFINITY;
+  for (int j = 0; j < n; ++j) {
+    const uint16_t* c = cache + (size_t)rows[j] * W;
+    double acc = 0.0;
+    for (int a = 0; a < DN; ++a) { /* K_j[a] = W_UK[a] . c_j (the expansion) */
+      double kj = 0.0;
+      for (int e = 0; e < DC; ++e) kj += (double)bf16_to_f(w_uk[(size_t)a * DC + e]) * (double)bf16_to_f(c[e]);
+      acc += (double)bf16_to_f(q[a]) * kj;
+    }
+    for (int r = 0; r < DR; ++r) acc += (double)bf16_to_f(q[DN + r]) * (double)bf16_to_f(c[DC + r]);
+    z[j] = acc * scale;
+    if (z[j] > m) m = z[j];
+    for (int a = 0; a < DV; ++a) { /* V_j[a] = W_UV[a] . c_j */
+      double vj = 0.0;
+      for (int e = 0; e < DC; ++e) vj += (double)bf16_to_f(w_uv[(size_t)a * DC + e]) * (double)bf16_to_f(c[e]);
+      vexp[(size_t)j * DV + a] = vj;
+    }
+  }
+  double l = 0.0;
+  for (int j = 0; j < n; ++j) l += exp(z[j] - m);
+  for (int j = 0; j < n; ++j) {
+    const double w = exp(z[j] - m) / l;
+    for (int a = 0; a < DV; ++a) out[a] += w * vexp[(size_t)j * DV + a];
+  }
+  free(z);
+  free(vexp);
+  return m + log(l);
+}

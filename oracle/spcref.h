@@ -103,6 +103,16 @@ int spcref_plan_step(const int64_t* th, int L, int64_t S, int l_cpu, int32_t* ou
 void spcref_batch_score(const float* logits, const float* head_max, const int64_t* head_sumfix,
                         const int32_t* seq_len, int B, int Hq, int Smax, float* out);
 
+/* ---- NEXT-3: MLA select-then-expand (Fig. 5(e)) ----
+ * One head of one request, fp64, in the paper's order: only the selected latent rows are
+ * up-projected -- K_j = [W_UK c_j | kpe_j] (DN + DR), V_j = W_UV c_j (DV) -- then softmax
+ * attention of q = [q_nope | q_pe] over them (scale given), o = sum_j w_j V_j.
+ * cache [rows][DC + DR] bf16 (latent c then the shared rope key), W_UK [DN][DC], W_UV [DV][DC]
+ * bf16, q [DN + DR] bf16.  Returns lse (natural log); -inf and o = 0 when n = 0. */
+double spcref_mla_head(const uint16_t* q, const uint16_t* cache, const uint16_t* w_uk,
+                       const uint16_t* w_uv, const int32_t* rows, int n, int DC, int DR, int DN,
+                       int DV, double scale, double* out);
+
 #ifdef __cplusplus
 }
 #endif

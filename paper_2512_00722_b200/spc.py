@@ -28,7 +28,8 @@ EXPORTS = [
     "spc_topk_merge_workspace", "spc_topk_merge", "spc_topk_filter", "spc_elastic_diff",
     "spc_gather_kv", "spc_gather_kv_strided", "spc_attn_workspace", "spc_sparse_decode_attn",
     "spc_attn_merge", "spc_select", "spc_rethead_qk", "spc_plan_mem_part",
-    "spc_plan_thresholds", "spc_plan_max_resident", "spc_plan_step",
+    "spc_plan_thresholds", "spc_plan_max_resident", "spc_plan_step", "spc_mla_workspace",
+    "spc_mla_sparse_attn",
 ]
 
 
@@ -84,6 +85,10 @@ def load_library(path: str = LIB_PATH):
     L.spc_plan_max_resident.argtypes = [ctypes.POINTER(PlanCfg), i64, ctypes.POINTER(i32),
                                         ctypes.POINTER(i64)]
     L.spc_plan_step.argtypes = [P, i32, i64, ctypes.POINTER(i32), P, ctypes.POINTER(i32)]
+    L.spc_mla_workspace.argtypes = [i32, i32, i32]
+    L.spc_mla_workspace.restype = sz
+    L.spc_mla_sparse_attn.argtypes = [P, P, P, P, P, P, i32, i32, i32, i32, i32, i32, i32, i32, f32,
+                                      P, P, P, sz, P]
     L.spc_attn_workspace.argtypes = [i32, i32, i32, i32, i32]
     L.spc_attn_workspace.restype = sz
     L.spc_sparse_decode_attn.argtypes = [i32, P, P, P, i32, P, P, i32, i32, i32, i32, i32, i32,
@@ -240,6 +245,22 @@ def rethead_qk(token, emb, norm_w, eps: float, w_qk, inv_freq, mscale: float, po
                                 _p(inv_freq), float(mscale), _p(pos), B, Hq, G, D, Smax,
                                 _p(q_out), _p(kr), _p(seq_len_out), _p(x_out), _s(stream)),
            "spc_rethead_qk")
+
+
+def mla_workspace(B: int, H: int, k: int) -> int:
+    return int(lib().spc_mla_workspace(B, H, k))
+
+
+def mla_sparse_attn(q, cache, w_uk, w_uv, idx, count, scale: float, out, lse, ws, stream=None):
+    """spc_mla_sparse_attn: MLA attention over each head's selected latent rows (NEXT-3)."""
+    B, H, _ = q.shape
+    Smax, W = cache.shape[1], cache.shape[2]
+    DN, DC = w_uk.shape[1], w_uk.shape[2]
+    DV = w_uv.shape[1]
+    k = idx.shape[2]
+    _check(lib().spc_mla_sparse_attn(_p(q), _p(cache), _p(w_uk), _p(w_uv), _p(idx), _p(count), B,
+                                     H, Smax, k, DC, W - DC, DN, DV, float(scale), _p(out), _p(lse),
+                                     _p(ws), ws.numel(), _s(stream)), "spc_mla_sparse_attn")
 
 
 def sparse_decode_attn(q, k_tab, v_tab, kv_mode: int, idx, count, rows: int, k: int, scale: float,
