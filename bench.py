@@ -39,7 +39,8 @@ def parse():
     ap.add_argument("--config", default=None,
                     help="A/B (single GPU, replicas for N>1), C (B=16, growing 128K context), "
                          "D (KV in pinned host memory, B=4), E (context-sharded) or R (the "
-                         "retrieval head's front-end, NEXT-1); default B at N=1, E at N>1")
+                         "retrieval head's front-end, NEXT-1) or M (MLA sparse attention, NEXT-3); default B at "
+                         "N=1, E at N>1")
     ap.add_argument("--batch", type=int, default=1, help="config R: requests per step (<= 16)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--kv-layout", default="token", choices=["token", "layer"],
@@ -927,6 +928,97 @@ def bench_frontend(args):
     }), flush=True)
 
 
+def bench_mla(args):
+    """Config M: MLA sparse decode attention over each head's selected
+    latent rows (spc_mla_sparse_attn) at the DeepSeek-V2-Lite attention shape: 27 layers, 16
+    heads, latent 512 + rope 64, no-rope / value head dims 128, 32K context, budget 2048
+    per head, B = 1.  Selections are synthetic (sorted random rows per head: the retrieval
+    that produces them is the head-level path measured by config B).  Step = one call for
+    all 27 layers (2 launches); 3 address-distinct latent caches rotated (3.1 GB > L2)."""
+    import torch
+
+    from paper_2512_00722_b200 import build as spc_build
+    from paper_2512_00722_b200 import spc, synth
+
+    if not os.path.exists(spc.LIB_PATH) or not spc_build.up_to_date():
+        spc_build.build()
+    dev = torch.device("cuda", 0)
+    L, B, H, DN, DV, DC, DR, S, k, NS = 27, 1, 16, 128, 128, 512, 64, 32768, 2048, 3
+    seed = synth.BASE_SEED + 6
+    caches = [[synth.normal_bf16((B, S, DC + DR), seed + 97 * c + l, device=dev) for l in range(L)]
+              for c in range(NS)]
+    w_uk = [(synth.normal_bf16((H, DN, DC), seed + 1000 + l, device=dev, dtype=torch.float32)
+             * DC ** -0.5).to(torch.bfloat16) for l in range(L)]
+    w_uv = [(synth.normal_bf16((H, DV, DC), seed + 2000 + l, device=dev, dtype=torch.float32)
+             * DC ** -0.5).to(torch.bfloat16) for l in range(L)]
+    q = synth.normal_bf16((L, B, H, DN + DR), seed + 3000, device=dev)
+    g = torch.Generator(device="cpu").manual_seed(seed)
+    idx = torch.stack([torch.sort(torch.randperm(S, generator=g)[:k])[0] for _ in range(B * H)])
+    idx = idx.view(B, H, k).to(torch.int32).to(dev)
+    cnt = torch.full((B, H), k, dtype=torch.int32, device=dev)
+    out = torch.zeros((L, B, H, DV), dtype=torch.float32, device=dev)
+    ws = spc.alloc_workspace(spc.mla_workspace(L, B, H, k), dev)
+    scale = (DN + DR) ** -0.5
+    stream = torch.cuda.Stream()
+    ctabs = [spc.ptr_table(caches[c], dev) for c in range(NS)]
+    uktab, uvtab = spc.ptr_table(w_uk, dev), spc.ptr_table(w_uv, dev)
+
+    def step(c, st):  # all 27 layers in one call
+        spc.mla_sparse_attn(q, ctabs[c], uktab, uvtab, idx, cnt, S, DN, DV, scale, out, None, ws,
+                            stream=st)
+
+    graphs = []
+    with torch.cuda.stream(stream):
+        for c in range(NS):
+            step(c, stream)
+        stream.synchronize()
+        n0 = spc.launch_count()
+        for c in range(NS):
+            gr = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gr, stream=stream):
+                step(c, stream)
+            graphs.append(gr)
+        per_step = (spc.launch_count() - n0) // NS
+        for i in range(args.warmup):
+            graphs[i % NS].replay()
+        stream.synchronize()
+        sampler = ClockSampler(0)
+        sampler.start()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for i in range(args.steps):
+            graphs[i % NS].replay()
+        e1.record(stream)
+        stream.synchronize()
+        clocks = sampler.stop()
+    ms = e0.elapsed_time(e1) / args.steps
+    alg = L * (B * H * k * (DC + DR) * 2 + H * (DN + DV) * DC * 2)
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    achieved = alg / (ms * 1e-3) / 1e9
+    print(json.dumps({
+        "metric": METRIC, "value": B / (ms * 1e-3), "unit": "tokens/s", "n_gpus": 1,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (seeded latent caches, weights and per-head selections)",
+        "config": {"workload": f"M: MLA sparse attention (NEXT-3), DeepSeek-V2-Lite attention "
+                               f"shape (L={L}, H={H}, latent {DC}+{DR}, d_nope={DN}, d_v={DV}, "
+                               f"ctx={S}, k={k} per head, batch={B})",
+                   "l2": f"{NS} address-distinct latent caches rotated step by step",
+                   "algorithmic_bytes_per_step": alg},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": None,
+                     "kernel": "mla_absorb_kernel + mla_attn_kernel, all layers",
+                     "peak_source": "measured (MEASURED_PEAKS.json hbm_gbs)"},
+        "gpu_launches": per_step * args.steps,
+        "clocks": clocks,
+    }), flush=True)
+
+
 def main():
     args = parse()
     if args.warmup < 3:
@@ -945,6 +1037,8 @@ def main():
             bench_offload(args)
         elif args.config == "R":
             bench_frontend(args)
+        elif args.config == "M":
+            bench_mla(args)
         else:
             bench_ours(args)
 

@@ -360,21 +360,23 @@ int spc_plan_step(const int64_t* thresholds, int L, int64_t S, int* l_cpu, int32
  *   o[b][h] = sum_j softmax_j(scale * [q_nope.W_UK c_j + q_pe.kpe_j]) W_UV c_j
  * over j in idx[b][h][0 .. count[b][h]); lse[b][h] natural-log log-sum-exp (-inf, o = 0
  * when the count is 0).
- * q      [B][H][DN + DR] bf16 (no-rope part, then the rope part)
- * cache  [B][Smax][DC + DR] bf16: latent c (DC) then the shared rope key kpe (DR)
- * w_uk   [H][DN][DC] bf16, w_uv [H][DV][DC] bf16 (the up-projections)
+ * All L layers in one call (the selection is layer-independent):
+ * q      [L][B][H][DN + DR] bf16 (no-rope part, then the rope part)
+ * cache  DEVICE array of L pointers, each [B][Smax][DC + DR] bf16: latent c (DC) then
+ *        the shared rope key kpe (DR), 16-byte aligned
+ * w_uk   DEVICE array of L pointers to [H][DN][DC] bf16; w_uv likewise to [H][DV][DC]
  * idx    [B][H][k] int32 rows (< Smax), count [B][H] int32 DEVICE
- * out    [B][H][DV] f32;  lse [B][H] f32 or NULL
- * ws     >= spc_mla_workspace(B, H, k) bytes, zero-filled on first use (left so)
+ * out    [L][B][H][DV] f32;  lse [L][B][H] f32 or NULL
+ * ws     >= spc_mla_workspace(L, B, H, k) bytes, zero-filled on first use (left so)
  * Supported: DC = 512, DR = 64 (DeepSeek-V2/V3 MLA), DN <= 512, DV <= 1024.
  * Errors: SPC_E_NULL, SPC_E_SHAPE, SPC_E_BUDGET, SPC_E_UNSUPPORTED, SPC_E_WORKSPACE,
- * SPC_E_RANGE (cache not 16-byte aligned), SPC_E_CUDA.
+ * SPC_E_CUDA.
  * ---------------------------------------------------------------------- */
-size_t spc_mla_workspace(int B, int H, int k);
-int spc_mla_sparse_attn(const void* q, const void* cache, const void* w_uk, const void* w_uv,
-                        const int32_t* idx, const int32_t* count, int B, int H, int Smax, int k,
-                        int DC, int DR, int DN, int DV, float scale, float* out, float* lse,
-                        void* ws, size_t ws_bytes, spc_stream_t stream);
+size_t spc_mla_workspace(int L, int B, int H, int k);
+int spc_mla_sparse_attn(const void* q, const void* const* cache, const void* const* w_uk,
+                        const void* const* w_uv, const int32_t* idx, const int32_t* count, int L,
+                        int B, int H, int Smax, int k, int DC, int DR, int DN, int DV, float scale,
+                        float* out, float* lse, void* ws, size_t ws_bytes, spc_stream_t stream);
 
 #ifdef __cplusplus
 }

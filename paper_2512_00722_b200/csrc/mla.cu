@@ -13,6 +13,8 @@
 //   o     = W_UV o_c,   lse = logsumexp(s)
 // so each selected latent row (576 bf16 = 1152 B) is read once per head and nothing of
 // size k x H x (DN + DV) is materialised.  HBM-bound: the selected latent rows dominate.
+// All L layers run in one launch of each kernel (grid.z = layer; the selection is
+// layer-independent), per-layer caches and weights through pointer tables.
 #include <algorithm>
 
 #include "common.cuh"
@@ -23,19 +25,19 @@ namespace {
 constexpr int ML_DC = 512, ML_DR = 64, ML_W = ML_DC + ML_DR;
 constexpr int ML_ROWS = 128;      // selected rows per CTA (split-K)
 constexpr int ML_WARPS = 8;
-constexpr int ML_UNR = 4;         // rows in flight per warp
+constexpr int ML_UNR = 8;         // rows in flight per warp
 
 struct MlaWs {
-  float* qabs;      // [B*H][576]
-  float* part_o;    // [B*H][nsplit][512]
-  float* part_ml;   // [B*H][nsplit][2]
-  unsigned* cnt;    // [B*H]
+  float* qabs;      // [L][B*H][576]
+  float* part_o;    // [L][B*H][nsplit][512]
+  float* part_ml;   // [L][B*H][nsplit][2]
+  unsigned* cnt;    // [L][B*H]
   int nsplit;
   size_t bytes;
 };
-MlaWs mla_ws_layout(void* ws, int B, int H, int k) {
+MlaWs mla_ws_layout(void* ws, int L, int B, int H, int k) {
   MlaWs w;
-  const size_t bh = (size_t)B * H;
+  const size_t bh = (size_t)L * B * H;
   w.nsplit = (k + ML_ROWS - 1) / ML_ROWS;
   uint8_t* p = (uint8_t*)ws;
   size_t off = 0;
@@ -53,38 +55,51 @@ MlaWs mla_ws_layout(void* ws, int B, int H, int k) {
 }
 
 // q_abs[e] = sum_n q_nope[n] W_UK[h][n][e] (e < 512), q_abs[512 + r] = q_pe[r]
-__global__ void __launch_bounds__(256) mla_absorb_kernel(const uint16_t* __restrict__ q,
-                                                         const uint16_t* __restrict__ w_uk, int H,
-                                                         int DN, float* __restrict__ qabs) {
+// grid (8 slices of 64 dims, B*H, L), 64 threads: one output per thread, 16 loads in flight
+__global__ void __launch_bounds__(64) mla_absorb_kernel(const uint16_t* __restrict__ q,
+                                                        const void* const* __restrict__ w_uk_l,
+                                                        int BH, int H, int DN,
+                                                        float* __restrict__ qabs) {
   spc_pdl_entry();
-  const int bh = blockIdx.x, h = bh % H, tid = threadIdx.x;
-  const uint16_t* qq = q + (size_t)bh * (DN + ML_DR);
-  const uint16_t* W = w_uk + (size_t)h * DN * ML_DC;
-  for (int e = tid; e < ML_DC; e += 256) {
-    float acc = 0.f;
-    for (int n = 0; n < DN; ++n)
-      acc = fmaf(__uint_as_float((uint32_t)qq[n] << 16),
-                 __uint_as_float((uint32_t)W[(size_t)n * ML_DC + e] << 16), acc);
-    qabs[(size_t)bh * ML_W + e] = acc;
+  const int bh = blockIdx.y, h = bh % H, l = blockIdx.z, tid = threadIdx.x;
+  const uint16_t* qq = q + ((size_t)l * BH + bh) * (DN + ML_DR);
+  const uint16_t* W = (const uint16_t*)w_uk_l[l] + (size_t)h * DN * ML_DC;
+  float* qa = qabs + ((size_t)l * BH + bh) * ML_W;
+  const int e = blockIdx.x * 64 + tid;
+  float acc = 0.f;
+  for (int n0 = 0; n0 < DN; n0 += 16) {
+    uint16_t wv[16], qv[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      const int n = min(n0 + u, DN - 1);
+      wv[u] = W[(size_t)n * ML_DC + e];
+      qv[u] = qq[n];
+    }
+#pragma unroll
+    for (int u = 0; u < 16; ++u)
+      if (n0 + u < DN)
+        acc = fmaf(__uint_as_float((uint32_t)qv[u] << 16), __uint_as_float((uint32_t)wv[u] << 16), acc);
   }
-  if (tid < ML_DR) qabs[(size_t)bh * ML_W + ML_DC + tid] = __uint_as_float((uint32_t)qq[DN + tid] << 16);
+  qa[e] = acc;
+  if (blockIdx.x == 0) qa[ML_DC + tid] = __uint_as_float((uint32_t)qq[DN + tid] << 16);
 }
 
 __global__ void __launch_bounds__(ML_WARPS * 32) mla_attn_kernel(
-    const uint16_t* __restrict__ cache, const uint16_t* __restrict__ w_uv,
-    const int32_t* __restrict__ idx, const int32_t* __restrict__ count, int H, int Smax, int k,
-    int DV, float scale_log2, MlaWs ws, float* __restrict__ out, float* __restrict__ lse) {
+    const void* const* __restrict__ cache_l, const void* const* __restrict__ w_uv_l,
+    const int32_t* __restrict__ idx, const int32_t* __restrict__ count, int BH, int H, int Smax,
+    int k, int DV, float scale_log2, MlaWs ws, float* __restrict__ out, float* __restrict__ lse) {
   spc_pdl_entry();
   __shared__ float s_o[ML_WARPS][ML_DC];
   __shared__ float s_ml[ML_WARPS][2];
   __shared__ float s_fin[ML_DC];
   __shared__ int flag;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int bh = blockIdx.y, b = bh / H, h = bh % H, split = blockIdx.x;
-  const int n = min(max(count[bh], 0), k);
+  const int bhs = blockIdx.y, b = bhs / H, h = bhs % H, split = blockIdx.x, lyr = blockIdx.z;
+  const int bh = lyr * BH + bhs;  // (layer, b, h) slot of the workspace and the outputs
+  const int n = min(max(count[bhs], 0), k);
   const int r0 = split * ML_ROWS, r1 = min(n, r0 + ML_ROWS);
-  const uint16_t* cb = cache + (size_t)b * Smax * ML_W;
-  const int32_t* rows = idx + (size_t)bh * k;
+  const uint16_t* cb = (const uint16_t*)cache_l[lyr] + (size_t)b * Smax * ML_W;
+  const int32_t* rows = idx + (size_t)bhs * k;
   // this lane's slice of q_abs: c dims [16 lane, +16), rope dims [2 lane, +2)
   float qa[16], qp[2];
   const float* qs = ws.qabs + (size_t)bh * ML_W;
@@ -180,15 +195,31 @@ __global__ void __launch_bounds__(ML_WARPS * 32) mla_attn_kernel(
     s_fin[d] = v * inv;
   }
   __syncthreads();
-  const uint16_t* Wv = w_uv + (size_t)h * DV * ML_DC;
-  for (int a = warp; a < DV; a += ML_WARPS) {  // o[a] = W_UV[h][a] . o_c
-    float acc = 0.f;
+  const uint16_t* Wv = (const uint16_t*)w_uv_l[lyr] + (size_t)h * DV * ML_DC;
+  for (int a0 = warp * 4; a0 < DV; a0 += ML_WARPS * 4) {  // o[a] = W_UV[h][a] . o_c
+    uint4 wr[4][2];  // 4 output rows in flight: 16 bf16 per lane each
 #pragma unroll
-    for (int i = 0; i < 16; ++i)
-      acc = fmaf(__uint_as_float((uint32_t)Wv[(size_t)a * ML_DC + lane + 32 * i] << 16),
-                 s_fin[lane + 32 * i], acc);
-    acc = warp_sum(acc);
-    if (lane == 0) out[(size_t)bh * DV + a] = acc;
+    for (int t = 0; t < 4; ++t) {
+      const int a = min(a0 + t, DV - 1);
+      const uint4* rowp = reinterpret_cast<const uint4*>(Wv + (size_t)a * ML_DC) + 2 * lane;
+      wr[t][0] = __ldg(rowp);
+      wr[t][1] = __ldg(rowp + 1);
+    }
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const uint32_t* p0 = &wr[t][0].x;
+      const uint32_t* p1 = &wr[t][1].x;
+      float acc = 0.f;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        acc = fmaf(bf16lo(p0[e]), s_fin[16 * lane + 2 * e], acc);
+        acc = fmaf(bf16hi(p0[e]), s_fin[16 * lane + 2 * e + 1], acc);
+        acc = fmaf(bf16lo(p1[e]), s_fin[16 * lane + 8 + 2 * e], acc);
+        acc = fmaf(bf16hi(p1[e]), s_fin[16 * lane + 8 + 2 * e + 1], acc);
+      }
+      acc = warp_sum(acc);
+      if (lane == 0 && a0 + t < DV) out[(size_t)bh * DV + a0 + t] = acc;
+    }
   }
   if (lse && tid == 0) lse[bh] = GL > 0.f ? (GM + log2f(GL)) * 0.6931471805599453f : -INFINITY;
 }
@@ -198,27 +229,26 @@ __global__ void __launch_bounds__(ML_WARPS * 32) mla_attn_kernel(
 
 using namespace spc;
 
-extern "C" size_t spc_mla_workspace(int B, int H, int k) {
-  if (B <= 0 || H <= 0 || k <= 0) return 0;
-  return mla_ws_layout(nullptr, B, H, k).bytes;
+extern "C" size_t spc_mla_workspace(int L, int B, int H, int k) {
+  if (L <= 0 || B <= 0 || H <= 0 || k <= 0) return 0;
+  return mla_ws_layout(nullptr, L, B, H, k).bytes;
 }
 
-extern "C" int spc_mla_sparse_attn(const void* q, const void* cache, const void* w_uk,
-                                   const void* w_uv, const int32_t* idx, const int32_t* count,
-                                   int B, int H, int Smax, int k, int DC, int DR, int DN, int DV,
-                                   float scale, float* out, float* lse, void* ws, size_t ws_bytes,
-                                   spc_stream_t stream) {
+extern "C" int spc_mla_sparse_attn(const void* q, const void* const* cache, const void* const* w_uk,
+                                   const void* const* w_uv, const int32_t* idx,
+                                   const int32_t* count, int L, int B, int H, int Smax, int k,
+                                   int DC, int DR, int DN, int DV, float scale, float* out,
+                                   float* lse, void* ws, size_t ws_bytes, spc_stream_t stream) {
   if (!q || !cache || !w_uk || !w_uv || !idx || !count || !out || !ws) return SPC_E_NULL;
-  if (B <= 0 || H <= 0 || Smax <= 0 || DN <= 0 || DV <= 0) return SPC_E_SHAPE;
+  if (L <= 0 || B <= 0 || H <= 0 || Smax <= 0 || DN <= 0 || DV <= 0) return SPC_E_SHAPE;
   if (k < 1 || k > SPC_MAX_K) return SPC_E_BUDGET;
   if (DC != ML_DC || DR != ML_DR || DN > 512 || DV > 1024) return SPC_E_UNSUPPORTED;
-  if (ws_bytes < spc_mla_workspace(B, H, k)) return SPC_E_WORKSPACE;
-  if (((uintptr_t)cache & 15)) return SPC_E_RANGE;
-  MlaWs w = mla_ws_layout(ws, B, H, k);
+  if (ws_bytes < spc_mla_workspace(L, B, H, k)) return SPC_E_WORKSPACE;
+  MlaWs w = mla_ws_layout(ws, L, B, H, k);
   cudaStream_t st = as_stream(stream);
-  SPC_TRY(launched(launch_k(mla_absorb_kernel, dim3(B * H), dim3(256), 0, st, (const uint16_t*)q,
-                            (const uint16_t*)w_uk, H, DN, w.qabs)));
-  return launched(launch_k(mla_attn_kernel, dim3(w.nsplit, B * H), dim3(ML_WARPS * 32), 0, st,
-                           (const uint16_t*)cache, (const uint16_t*)w_uv, idx, count, H, Smax, k,
-                           DV, scale * 1.4426950408889634f, w, out, lse));
+  SPC_TRY(launched(launch_k(mla_absorb_kernel, dim3(ML_DC / 64, B * H, L), dim3(64), 0, st,
+                            (const uint16_t*)q, w_uk, B * H, H, DN, w.qabs)));
+  return launched(launch_k(mla_attn_kernel, dim3(w.nsplit, B * H, L), dim3(ML_WARPS * 32), 0, st,
+                           cache, w_uv, idx, count, B * H, H, Smax, k, DV,
+                           scale * 1.4426950408889634f, w, out, lse));
 }

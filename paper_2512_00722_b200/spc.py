@@ -85,10 +85,10 @@ def load_library(path: str = LIB_PATH):
     L.spc_plan_max_resident.argtypes = [ctypes.POINTER(PlanCfg), i64, ctypes.POINTER(i32),
                                         ctypes.POINTER(i64)]
     L.spc_plan_step.argtypes = [P, i32, i64, ctypes.POINTER(i32), P, ctypes.POINTER(i32)]
-    L.spc_mla_workspace.argtypes = [i32, i32, i32]
+    L.spc_mla_workspace.argtypes = [i32, i32, i32, i32]
     L.spc_mla_workspace.restype = sz
-    L.spc_mla_sparse_attn.argtypes = [P, P, P, P, P, P, i32, i32, i32, i32, i32, i32, i32, i32, f32,
-                                      P, P, P, sz, P]
+    L.spc_mla_sparse_attn.argtypes = [P, P, P, P, P, P, i32, i32, i32, i32, i32, i32, i32, i32, i32,
+                                      f32, P, P, P, sz, P]
     L.spc_attn_workspace.argtypes = [i32, i32, i32, i32, i32]
     L.spc_attn_workspace.restype = sz
     L.spc_sparse_decode_attn.argtypes = [i32, P, P, P, i32, P, P, i32, i32, i32, i32, i32, i32,
@@ -247,20 +247,20 @@ def rethead_qk(token, emb, norm_w, eps: float, w_qk, inv_freq, mscale: float, po
            "spc_rethead_qk")
 
 
-def mla_workspace(B: int, H: int, k: int) -> int:
-    return int(lib().spc_mla_workspace(B, H, k))
+def mla_workspace(L: int, B: int, H: int, k: int) -> int:
+    return int(lib().spc_mla_workspace(L, B, H, k))
 
 
-def mla_sparse_attn(q, cache, w_uk, w_uv, idx, count, scale: float, out, lse, ws, stream=None):
-    """spc_mla_sparse_attn: MLA attention over each head's selected latent rows (NEXT-3)."""
-    B, H, _ = q.shape
-    Smax, W = cache.shape[1], cache.shape[2]
-    DN, DC = w_uk.shape[1], w_uk.shape[2]
-    DV = w_uv.shape[1]
+def mla_sparse_attn(q, cache_tab, w_uk_tab, w_uv_tab, idx, count, Smax: int, DN: int, DV: int,
+                    scale: float, out, lse, ws, DC: int = 512, DR: int = 64, stream=None):
+    """spc_mla_sparse_attn: MLA attention over each head's selected latent rows, all layers
+    (NEXT-3).  q [L][B][H][DN+DR]; *_tab: device pointer tables (ptr_table) per layer."""
+    L, B, H, _ = q.shape
     k = idx.shape[2]
-    _check(lib().spc_mla_sparse_attn(_p(q), _p(cache), _p(w_uk), _p(w_uv), _p(idx), _p(count), B,
-                                     H, Smax, k, DC, W - DC, DN, DV, float(scale), _p(out), _p(lse),
-                                     _p(ws), ws.numel(), _s(stream)), "spc_mla_sparse_attn")
+    _check(lib().spc_mla_sparse_attn(_p(q), _p(cache_tab), _p(w_uk_tab), _p(w_uv_tab), _p(idx),
+                                     _p(count), L, B, H, Smax, k, DC, DR, DN, DV, float(scale),
+                                     _p(out), _p(lse), _p(ws), ws.numel(), _s(stream)),
+           "spc_mla_sparse_attn")
 
 
 def sparse_decode_attn(q, k_tab, v_tab, kv_mode: int, idx, count, rows: int, k: int, scale: float,
