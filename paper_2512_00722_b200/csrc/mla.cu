@@ -23,7 +23,10 @@ namespace spc {
 namespace {
 
 constexpr int ML_DC = 512, ML_DR = 64, ML_W = ML_DC + ML_DR;
-constexpr int ML_ROWS = 128;      // selected rows per CTA (split-K)
+#ifndef SPC_ML_ROWS
+#define SPC_ML_ROWS 512
+#endif
+constexpr int ML_ROWS = SPC_ML_ROWS;  // selected rows per CTA (split-K)
 constexpr int ML_WARPS = 8;
 constexpr int ML_UNR = 8;         // rows in flight per warp
 
