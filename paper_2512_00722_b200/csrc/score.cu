@@ -61,17 +61,18 @@ __global__ void __launch_bounds__(NM_T) norm_kernel(
     const int nch = S >> 2;  // whole float4 chunks; the tail is done below
     const float4* r4 = reinterpret_cast<const float4*>(row);
     const int stride = gridDim.x * NM_T;
-    for (int c = blockIdx.x * NM_T + threadIdx.x; c < nch; c += 2 * stride) {
-      const float4 x0 = __ldcg(r4 + c);
-      const float4 x1 = c + stride < nch
-                            ? __ldcg(r4 + c + stride)
-                            : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
-      const float2 a0 = spc_exp2_dev(__fsub_rn(x0.x, m), __fsub_rn(x0.y, m));
-      const float2 a1 = spc_exp2_dev(__fsub_rn(x0.z, m), __fsub_rn(x0.w, m));
-      const float2 b0 = spc_exp2_dev(__fsub_rn(x1.x, m), __fsub_rn(x1.y, m));
-      const float2 b1 = spc_exp2_dev(__fsub_rn(x1.z, m), __fsub_rn(x1.w, m));
-      acc += fixpoint40(a0.x) + fixpoint40(a0.y) + fixpoint40(a1.x) + fixpoint40(a1.y) +
-             fixpoint40(b0.x) + fixpoint40(b0.y) + fixpoint40(b1.x) + fixpoint40(b1.y);
+    for (int c = blockIdx.x * NM_T + threadIdx.x; c < nch; c += 4 * stride) {  // 4 in flight
+      float4 x[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        x[u] = c + u * stride < nch ? __ldcg(r4 + c + u * stride)
+                                    : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const float2 a0 = spc_exp2_dev(__fsub_rn(x[u].x, m), __fsub_rn(x[u].y, m));
+        const float2 a1 = spc_exp2_dev(__fsub_rn(x[u].z, m), __fsub_rn(x[u].w, m));
+        acc += fixpoint40(a0.x) + fixpoint40(a0.y) + fixpoint40(a1.x) + fixpoint40(a1.y);
+      }
     }
     if (blockIdx.x == 0)
       for (int t = (nch << 2) + threadIdx.x; t < S; t += NM_T)
@@ -271,8 +272,10 @@ extern "C" int spc_score(int dtype, const void* q, const void* kr, const int32_t
 #undef LG
   }
   if (phases & SPC_SCORE_NORM) {
-    // enough CTAs per head to fill the GPU twice, each with >= 8 float4 chunks per thread
-    const int want = (2 * num_sms() + B * Hq - 1) / (B * Hq);
+    // enough CTAs per head for 8 CTAs (full occupancy) per SM, each with >= 8 float4 chunks
+    // per thread (4 in flight): long rows are latency-bound otherwise (1M tokens: 64 us at
+    // 2 CTAs per SM with 2 chunks in flight)
+    const int want = (8 * num_sms() + B * Hq - 1) / (B * Hq);
     const int cap = (Smax + 8 * 4 * NM_T - 1) / (8 * 4 * NM_T);
     const int nb = max(1, min(want, cap));
     if (Smax % 4 == 0)
