@@ -383,6 +383,10 @@ def test_maximum_sizes(oracle):
     rng = np.random.default_rng(11)
     gs = rng.random((1, 2, 60000)).astype(np.float32) ** 4
     check_topk(oracle, gs, [60000], spc.MAX_K, force=True)
+    # long rows, few of them: the 16-CTA cluster path (B*G*16 <= SMs, n >= 65536)
+    gl = (rng.random((2, 3, 300000)).astype(np.float32) ** 6)
+    gl[0, 1, 1000:1200] = gl[0, 1, 5]  # exact ties around the threshold
+    check_topk(oracle, gl, [300000, 123457], 2048, force=True, stride=3, offset=1)
     B, G, Hq, S, k = 2, 1, 4, 135168, spc.MAX_K
     g = torch.Generator(device="cpu").manual_seed(3)
     lg = (torch.randn((B, Hq, S), generator=g) * 2).to(DEV)
