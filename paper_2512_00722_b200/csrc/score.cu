@@ -200,9 +200,56 @@ int launch_logits(const uint16_t* kr, const uint16_t* q, const int32_t* seq_len,
                            (const float*)tile_max, tpr, nh, head_max, ctr));
 }
 
+// GROUP with float4 accesses (Smax % 4 == 0): a thread takes 4 consecutive tokens, one
+// float4 load per head (alpha in flight), the same O4..O6 arithmetic per element, one
+// float4 store.
+template <int ALPHA>
+__global__ void __launch_bounds__(GRP_THREADS) group4_kernel(
+    const float* __restrict__ logits, const float* __restrict__ head_max,
+    const int64_t* __restrict__ head_sumfix, const int32_t* __restrict__ seq_len, int G, int Smax,
+    float* __restrict__ group_score) {
+  spc_pdl_entry();
+  const int bg = blockIdx.y, b = bg / G, g = bg % G;
+  const int Hq = G * ALPHA;
+  const int S = seq_len[b];
+  float m[ALPHA], r[ALPHA];
+#pragma unroll
+  for (int j = 0; j < ALPHA; ++j) {
+    const int h = b * Hq + g * ALPHA + j;
+    m[j] = head_max[h];
+    const float l = __fmul_rn(__ll2float_rn(head_sumfix[h]), 9.094947017729282379150390625e-13f);
+    r[j] = __fdiv_rn(1.0f, l);
+  }
+  const float4* lg = reinterpret_cast<const float4*>(logits + ((size_t)b * Hq + g * ALPHA) * Smax);
+  float4* out = reinterpret_cast<float4*>(group_score + (size_t)bg * Smax);
+  const int c = blockIdx.x * GRP_THREADS + threadIdx.x;  // float4 chunk
+  if (c * 4 >= Smax) return;
+  float4 x[ALPHA];
+#pragma unroll
+  for (int j = 0; j < ALPHA; ++j) x[j] = __ldcg(lg + (size_t)j * (Smax / 4) + c);
+  float gsv[4];
+#pragma unroll
+  for (int j = 0; j < ALPHA; ++j) {
+    const float2 e0 = spc_exp2_dev(__fsub_rn(x[j].x, m[j]), __fsub_rn(x[j].y, m[j]));
+    const float2 e1 = spc_exp2_dev(__fsub_rn(x[j].z, m[j]), __fsub_rn(x[j].w, m[j]));
+    const float p[4] = {__fmul_rn(e0.x, r[j]), __fmul_rn(e0.y, r[j]), __fmul_rn(e1.x, r[j]),
+                        __fmul_rn(e1.y, r[j])};
+#pragma unroll
+    for (int u = 0; u < 4; ++u) gsv[u] = j ? fmaxf(gsv[u], p[u]) : p[u];
+  }
+  const int t = c * 4;
+  out[c] = make_float4(t < S ? gsv[0] : 0.f, t + 1 < S ? gsv[1] : 0.f, t + 2 < S ? gsv[2] : 0.f,
+                       t + 3 < S ? gsv[3] : 0.f);
+}
+
 template <int ALPHA>
 int launch_group(const float* logits, const float* head_max, const int64_t* sumfix,
                  const int32_t* seq_len, int B, int G, int Smax, float* gs, cudaStream_t st) {
+  if (Smax % 4 == 0) {
+    dim3 grid4((Smax / 4 + GRP_THREADS - 1) / GRP_THREADS, B * G);
+    return launched(launch_k(group4_kernel<ALPHA>, grid4, dim3(GRP_THREADS), 0, st, logits,
+                             head_max, sumfix, seq_len, G, Smax, gs));
+  }
   dim3 grid((Smax + GRP_TILE - 1) / GRP_TILE, B * G);
   return launched(launch_k(group_kernel<ALPHA>, grid, dim3(GRP_THREADS), 0, st, logits,
                            head_max, sumfix, seq_len, G, Smax, gs));
