@@ -9,6 +9,7 @@ python bench.py --config C --steps 30 > gpurun_out/${TAG}_bench_c.json 2> gpurun
 python bench.py --config D --steps 10 > gpurun_out/${TAG}_bench_d.json 2> gpurun_out/${TAG}_bench_d.err
 python bench.py --config E --steps 10 > gpurun_out/${TAG}_bench_e.json 2> gpurun_out/${TAG}_bench_e.err
 python bench.py --config R --steps 200 > gpurun_out/${TAG}_bench_r.json 2> gpurun_out/${TAG}_bench_r.err
+python bench.py --config M --steps 20 > gpurun_out/${TAG}_bench_m.json 2> gpurun_out/${TAG}_bench_m.err
 python bench.py --impl reference --steps 2 --warmup 3 > gpurun_out/${TAG}_bench_ref.json 2> gpurun_out/${TAG}_bench_ref.err
 K='regex:logits|lg_final|select_k|attn_bf16|norm_k|group_k|topk|diff_k|gather|merge|rethead'
 ncu --metrics gpu__time_duration.sum --clock-control none -k "$K" -c 40 --csv --log-file gpurun_out/${TAG}_launches.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
