@@ -378,6 +378,46 @@ int spc_mla_sparse_attn(const void* q, const void* const* cache, const void* con
                         int B, int H, int Smax, int k, int DC, int DR, int DN, int DV, float scale,
                         float* out, float* lse, void* ws, size_t ws_bytes, spc_stream_t stream);
 
+/* ------------------------------------------------------------------------
+ * spc_decode_step — the whole single-device §8(a) step in ONE call (native executor):
+ * spc_score(LOGITS) -> spc_select (NORM, GROUP, top-k, INDEXED elastic diff) ->
+ * spc_sparse_decode_attn over all L layers (INDEXED), enqueued on `stream`; when
+ * spc_select does not apply (Smax > 135168, Smax % 4, or B*G*8 > SMs) the separate
+ * spc_score(ALL) + spc_topk + spc_elastic_diff calls are used.  Same definitions and
+ * results as those calls in sequence.  The caller owns all buffers and the rolling
+ * state: prev_idx / prev_count (previous selection, count 0 on the first step) in,
+ * cur_idx / cur_count out -- swap them between steps.  scale is both the retrieval
+ * head's and the LLM's softmax scale (fl(1/sqrt(D)) in the paper's setting).
+ * ws >= spc_decode_step_workspace(L, B, Hq, G, D, Smax, k) bytes, zero-filled once.
+ * Errors: those of the calls it makes, and SPC_E_NULL / SPC_E_WORKSPACE.
+ * ---------------------------------------------------------------------- */
+typedef struct {
+  int L, B, Hq, G, D, Smax, rows, k, force_last;
+  float scale;
+  const void* q_ret;              /* [B][Hq][D] bf16 retrieval query */
+  const void* kr;                 /* [B][G][Smax][D] bf16 retrieval keys */
+  const int32_t* seq_len;         /* [B] */
+  const void* q_llm;              /* [L][B][Hq][D] bf16 */
+  const void* const* k_layers;    /* [L] -> [B][G][rows][D] bf16 */
+  const void* const* v_layers;
+  float* logits;                  /* [B][Hq][Smax] scratch */
+  float* head_max;                /* [B][Hq] */
+  int64_t* head_sumfix;           /* [B][Hq] */
+  float* group_score;             /* [B][G][Smax] */
+  const int32_t* prev_idx;        /* [B][G][k] */
+  const int32_t* prev_count;      /* [B][G] */
+  int32_t* cur_idx;               /* [B][G][k] out */
+  int32_t* cur_count;             /* [B][G] out */
+  int32_t* load_tok;              /* [B][G][k] out: cur \ prev */
+  int32_t* n_load;                /* [B][G] out */
+  float* out;                     /* [L][B][Hq][D] f32 */
+  float* lse;                     /* [L][B][Hq] or NULL */
+  void* ws;
+  size_t ws_bytes;
+} spc_step_args;
+size_t spc_decode_step_workspace(int L, int B, int Hq, int G, int D, int Smax, int k);
+int spc_decode_step(const spc_step_args* args, spc_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

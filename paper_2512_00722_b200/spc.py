@@ -29,12 +29,24 @@ EXPORTS = [
     "spc_gather_kv", "spc_gather_kv_strided", "spc_attn_workspace", "spc_sparse_decode_attn",
     "spc_attn_merge", "spc_select", "spc_rethead_qk", "spc_plan_mem_part",
     "spc_plan_thresholds", "spc_plan_max_resident", "spc_plan_step", "spc_mla_workspace",
-    "spc_mla_sparse_attn",
+    "spc_mla_sparse_attn", "spc_decode_step_workspace", "spc_decode_step",
 ]
 
 
 class SpcError(RuntimeError):
     pass
+
+
+class StepArgs(ctypes.Structure):
+    """spc_step_args (include/spc.h): every buffer of one spc_decode_step call."""
+    _fields_ = [(n, ctypes.c_int) for n in ("L", "B", "Hq", "G", "D", "Smax", "rows", "k",
+                                            "force_last")] + \
+        [("scale", ctypes.c_float)] + \
+        [(n, ctypes.c_void_p) for n in ("q_ret", "kr", "seq_len", "q_llm", "k_layers", "v_layers",
+                                        "logits", "head_max", "head_sumfix", "group_score",
+                                        "prev_idx", "prev_count", "cur_idx", "cur_count",
+                                        "load_tok", "n_load", "out", "lse", "ws")] + \
+        [("ws_bytes", ctypes.c_size_t)]
 
 
 class PlanCfg(ctypes.Structure):
@@ -89,6 +101,9 @@ def load_library(path: str = LIB_PATH):
     L.spc_mla_workspace.restype = sz
     L.spc_mla_sparse_attn.argtypes = [P, P, P, P, P, P, i32, i32, i32, i32, i32, i32, i32, i32, i32,
                                       f32, P, P, P, sz, P]
+    L.spc_decode_step_workspace.argtypes = [i32, i32, i32, i32, i32, i32, i32]
+    L.spc_decode_step_workspace.restype = sz
+    L.spc_decode_step.argtypes = [ctypes.POINTER(StepArgs), P]
     L.spc_attn_workspace.argtypes = [i32, i32, i32, i32, i32]
     L.spc_attn_workspace.restype = sz
     L.spc_sparse_decode_attn.argtypes = [i32, P, P, P, i32, P, P, i32, i32, i32, i32, i32, i32,
@@ -261,6 +276,29 @@ def mla_sparse_attn(q, cache_tab, w_uk_tab, w_uv_tab, idx, count, Smax: int, DN:
                                      _p(count), L, B, H, Smax, k, DC, DR, DN, DV, float(scale),
                                      _p(out), _p(lse), _p(ws), ws.numel(), _s(stream)),
            "spc_mla_sparse_attn")
+
+
+def decode_step_workspace(L: int, B: int, Hq: int, G: int, D: int, Smax: int, k: int) -> int:
+    return int(lib().spc_decode_step_workspace(L, B, Hq, G, D, Smax, k))
+
+
+def decode_step(args: "StepArgs", stream=None):
+    """spc_decode_step: the whole single-device step (score -> select -> attention) in one
+    C call; `args` is a StepArgs filled with data pointers (see make_step_args)."""
+    _check(lib().spc_decode_step(ctypes.byref(args), _s(stream)), "spc_decode_step")
+
+
+def make_step_args(q_ret, kr, seq_len, q_llm, k_tab, v_tab, rows: int, k: int, scale: float,
+                   logits, head_max, head_sumfix, group_score, prev_idx, prev_count, cur_idx,
+                   cur_count, load_tok, n_load, out, lse, ws, force_last: bool = True) -> StepArgs:
+    L, B, Hq, D = q_llm.shape
+    G = kr.shape[1]
+    ptr = lambda t: None if t is None else int(t.data_ptr())  # noqa: E731
+    return StepArgs(L, B, Hq, G, D, kr.shape[2], rows, k, int(force_last), float(scale),
+                    ptr(q_ret), ptr(kr), ptr(seq_len), ptr(q_llm), ptr(k_tab), ptr(v_tab),
+                    ptr(logits), ptr(head_max), ptr(head_sumfix), ptr(group_score), ptr(prev_idx),
+                    ptr(prev_count), ptr(cur_idx), ptr(cur_count), ptr(load_tok), ptr(n_load),
+                    ptr(out), ptr(lse), ptr(ws), ws.numel())
 
 
 def sparse_decode_attn(q, k_tab, v_tab, kv_mode: int, idx, count, rows: int, k: int, scale: float,

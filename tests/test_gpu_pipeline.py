@@ -172,3 +172,38 @@ def test_batch_level_step_selects_one_set_per_request(oracle):
     oo, _ = oracle.sparse_attn(synth.bf16_bits(ql), [kh[l] for l in range(L)],
                                [vh[l] for l in range(L)], oidx_g, ocnt_g, st.scale)
     assert float(np.abs(st.out.cpu().numpy() - oo).max()) <= 2e-3
+
+
+@pytest.mark.parametrize("S,B,G", [(4096, 1, 2), (150000, 1, 1), (3000, 2, 8)])
+def test_native_decode_step_equals_pipeline(S, B, G):
+    """spc_decode_step (one C call: score -> select -> attention, or the separate calls when
+    the fused select does not apply) is bit-identical to DecodeStep over three steps with
+    the previous selection rolled by the caller."""
+    Hq, D, L, k = 4 * G, 64, 2, 256
+    dev = torch.device("cuda")
+    kr = synth.retrieval_keys(B, G, S, D, seed=12, device=dev)
+    kc, vc = synth.llm_kv(L, B, G, S, D, seed=12, device=dev)
+    qr = synth.retrieval_queries(3, B, Hq, G, D, seed=12, device=dev)
+    ql = synth.llm_queries(1, L, B, Hq, D, seed=12, device=dev)[0]
+    seq = torch.full((B,), S, dtype=torch.int32, device=dev)
+    st = DecodeStep(kr, [kc[l] for l in range(L)], [vc[l] for l in range(L)], seq, L, Hq, k)
+    f32, i32 = torch.float32, torch.int32
+    z = lambda *s, dt=f32: torch.zeros(s, dtype=dt, device=dev)  # noqa: E731
+    lg, hm, F, gs = z(B, Hq, S), z(B, Hq), z(B, Hq, dt=torch.int64), z(B, G, S)
+    idx = [torch.full((B, G, k), -1, dtype=i32, device=dev) for _ in range(2)]
+    cnt = [z(B, G, dt=i32), z(B, G, dt=i32)]
+    lt, nl = z(B, G, k, dt=i32), z(B, G, dt=i32)
+    out, lse = z(L, B, Hq, D), z(L, B, Hq)
+    ws = spc.alloc_workspace(spc.decode_step_workspace(L, B, Hq, G, D, S, k), dev)
+    ktab = spc.ptr_table([kc[l] for l in range(L)], dev)
+    vtab = spc.ptr_table([vc[l] for l in range(L)], dev)
+    for s in range(3):
+        cur, prev = s % 2, 1 - s % 2
+        a = spc.make_step_args(qr[s], kr, seq, ql, ktab, vtab, S, k, st.scale, lg, hm, F, gs,
+                               idx[prev], cnt[prev], idx[cur], cnt[cur], lt, nl, out, lse, ws)
+        spc.decode_step(a)
+        ia, ca = st.step(qr[s], ql)
+        torch.cuda.synchronize()
+        assert torch.equal(ia, idx[cur]) and torch.equal(ca, cnt[cur])
+        assert torch.equal(st.n_load, nl)
+        assert torch.equal(st.out, out)
