@@ -24,11 +24,14 @@ namespace {
 
 constexpr int ML_DC = 512, ML_DR = 64, ML_W = ML_DC + ML_DR;
 #ifndef SPC_ML_ROWS
-#define SPC_ML_ROWS 512
+#define SPC_ML_ROWS 1024
 #endif
 constexpr int ML_ROWS = SPC_ML_ROWS;  // selected rows per CTA (split-K)
 constexpr int ML_WARPS = 8;
-constexpr int ML_UNR = 8;         // rows in flight per warp
+#ifndef SPC_ML_UNR
+#define SPC_ML_UNR 4
+#endif
+constexpr int ML_UNR = SPC_ML_UNR;  // rows in flight per warp
 
 struct MlaWs {
   float* qabs;      // [L][B*H][576]
