@@ -71,3 +71,21 @@ def test_host_validation_without_gpu(libspc):
     assert libspc.spc_sparse_decode_attn(0, P, P, P, 0, P, P, 2, 0, 3, 1, 4, 1, 128, 100, 16,
                                          0.1, P, None, P, 1 << 30, st) == 4
     assert libspc.spc_score_workspace(1, 32, 32768) > 0
+    # one-call step: NULL args / missing workspace are host-side errors
+    from paper_2512_00722_b200 import spc
+    assert libspc.spc_decode_step(None, st) == 1
+    a = spc.StepArgs()
+    a.L, a.B, a.Hq, a.G, a.D, a.Smax, a.rows, a.k = 32, 1, 32, 8, 128, 32768, 32768, 2048
+    assert libspc.spc_decode_step(ctypes.byref(a), st) == 1  # ws NULL
+    a.ws, a.ws_bytes = 16, 8
+    assert libspc.spc_decode_step(ctypes.byref(a), st) == 6  # workspace too small
+    assert libspc.spc_decode_step_workspace(32, 1, 32, 8, 128, 32768, 2048) > 0
+    # MLA: unsupported latent width, budget, workspace
+    assert libspc.spc_mla_sparse_attn(P, P, P, P, P, P, 1, 1, 16, 100, 64, 256, 64, 128, 128, 0.1,
+                                      P, None, P, 1 << 30, st) == 7
+    assert libspc.spc_mla_sparse_attn(P, P, P, P, P, P, 1, 1, 16, 100, 0, 512, 64, 128, 128, 0.1,
+                                      P, None, P, 1 << 30, st) == 3
+    assert libspc.spc_mla_workspace(27, 1, 16, 2048) > 0
+    # planner: C <= 0 is a capacity error
+    c = spc.plan_cfg(10, 100, 2, 1, 1, 1, 2)
+    assert libspc.spc_plan_thresholds(ctypes.byref(c), P) == 3
