@@ -32,7 +32,14 @@ namespace spc {
 namespace {
 
 constexpr int RH_WARPS = 8;
-constexpr int RH_UNR = 8;  // 16-byte weight chunks per row in flight per lane
+#ifndef SPC_RH_UNR
+#define SPC_RH_UNR 4
+#endif
+#ifndef SPC_RH_CPS
+#define SPC_RH_CPS 3
+#endif
+constexpr int RH_UNR = SPC_RH_UNR;  // 16-byte weight chunks per row in flight per lane
+constexpr int RH_CPS = SPC_RH_CPS;  // CTAs per SM of the B <= 4 kernel
 
 __device__ __forceinline__ uint16_t f32_to_bf16_rn(float f) {
   const __nv_bfloat16 h = __float2bfloat16_rn(f);
@@ -43,7 +50,7 @@ __device__ __forceinline__ float bf16_to_f32(uint16_t h) {
 }
 
 template <int BT>
-__global__ void __launch_bounds__(RH_WARPS * 32) rethead_kernel(
+__global__ void __launch_bounds__(RH_WARPS * 32, RH_CPS) rethead_kernel(
     const int32_t* __restrict__ token, const uint16_t* __restrict__ emb, int H,
     const uint16_t* __restrict__ norm_w, float eps, const uint16_t* __restrict__ w_qk,
     const float* __restrict__ inv_freq, float mscale, const int32_t* __restrict__ pos, int B,
@@ -330,7 +337,7 @@ extern "C" int spc_rethead_qk(const int32_t* token, const void* emb, int V, int 
   const size_t smem = (size_t)B * H * 2;
   if (smem > 200 * 1024) return SPC_E_UNSUPPORTED;
   const int npairs = (Hq + G) * (D / 2);
-  const int ncta = std::max(1, std::min(2 * num_sms(), (npairs + RH_WARPS - 1) / RH_WARPS));
+  const int ncta = std::max(1, std::min(RH_CPS * num_sms(), (npairs + RH_WARPS - 1) / RH_WARPS));
   cudaStream_t st = as_stream(stream);
 #define RH(BT)                                                                                    \
   {                                                                                               \
