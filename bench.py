@@ -54,6 +54,14 @@ def dist_env():
             int(os.environ.get("WORLD_SIZE", "1")))
 
 
+def traffic_of(key):
+    """ncu DRAM bytes per launch recorded in profiles/traffic.json (None if absent)."""
+    try:
+        return json.load(open(os.path.join(ROOT, "profiles", "traffic.json"))).get(key)
+    except Exception:
+        return None
+
+
 def workload_name(c, key):
     return (f"{key}: {c['name']} (L={c['L']}, Hq={c['Hq']}, G={c['G']}, d={c['D']}, "
             f"ctx={c['S']}, batch={c['B']}, k={c['k']})")
@@ -914,7 +922,7 @@ def bench_frontend(args):
                          f"L2) rotated launch by launch",
                    "algorithmic_bytes_per_step": alg, "front_end_us": us},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": None,
+                     "frac": achieved / peak, "traffic": traffic_of("rethead_b1") if B == 1 else None,
                      "kernel": "rethead_kernel (spc_rethead_qk)",
                      "algorithmic_bytes_per_launch": alg,
                      "peak_source": "measured (MEASURED_PEAKS.json hbm_gbs)"},
@@ -1011,7 +1019,10 @@ def bench_mla(args):
                    "l2": f"{NS} address-distinct latent caches rotated step by step",
                    "algorithmic_bytes_per_step": alg},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": None,
+                     "frac": achieved / peak, "traffic": traffic_of("mla_attn_27_layers"),
+                     "traffic_note": "ncu DRAM bytes of mla_attn_kernel per step: below the "
+                                     "per-head algorithmic bytes (heads sharing a selected "
+                                     "latent row hit L2)",
                      "kernel": "mla_absorb_kernel + mla_attn_kernel, all layers",
                      "peak_source": "measured (MEASURED_PEAKS.json hbm_gbs)"},
         "gpu_launches": per_step * args.steps,
