@@ -61,7 +61,8 @@ MlaWs mla_ws_layout(void* ws, int L, int B, int H, int k) {
 }
 
 // q_abs[e] = sum_n q_nope[n] W_UK[h][n][e] (e < 512), q_abs[512 + r] = q_pe[r]
-// grid (8 slices of 64 dims, B*H, L), 64 threads: one output per thread, 16 loads in flight
+// grid (4 slices of 128 dims, B*H, L), 64 threads: two adjacent outputs per thread
+// (bf16x2 loads of W_UK rows), 16 rows of W_UK in flight
 __global__ void __launch_bounds__(64) mla_absorb_kernel(const uint16_t* __restrict__ q,
                                                         const void* const* __restrict__ w_uk_l,
                                                         int BH, int H, int DN,
@@ -69,24 +70,29 @@ __global__ void __launch_bounds__(64) mla_absorb_kernel(const uint16_t* __restri
   spc_pdl_entry();
   const int bh = blockIdx.y, h = bh % H, l = blockIdx.z, tid = threadIdx.x;
   const uint16_t* qq = q + ((size_t)l * BH + bh) * (DN + ML_DR);
-  const uint16_t* W = (const uint16_t*)w_uk_l[l] + (size_t)h * DN * ML_DC;
+  const uint32_t* W = (const uint32_t*)((const uint16_t*)w_uk_l[l] + (size_t)h * DN * ML_DC);
   float* qa = qabs + ((size_t)l * BH + bh) * ML_W;
-  const int e = blockIdx.x * 64 + tid;
-  float acc = 0.f;
+  const int e2 = blockIdx.x * 64 + tid;  // pair of outputs 2 e2, 2 e2 + 1
+  float a0 = 0.f, a1 = 0.f;
   for (int n0 = 0; n0 < DN; n0 += 16) {
-    uint16_t wv[16], qv[16];
+    uint32_t wv[16];
+    uint16_t qv[16];
 #pragma unroll
     for (int u = 0; u < 16; ++u) {
       const int n = min(n0 + u, DN - 1);
-      wv[u] = W[(size_t)n * ML_DC + e];
+      wv[u] = __ldg(W + (size_t)n * (ML_DC / 2) + e2);
       qv[u] = qq[n];
     }
 #pragma unroll
     for (int u = 0; u < 16; ++u)
-      if (n0 + u < DN)
-        acc = fmaf(__uint_as_float((uint32_t)qv[u] << 16), __uint_as_float((uint32_t)wv[u] << 16), acc);
+      if (n0 + u < DN) {
+        const float qn = __uint_as_float((uint32_t)qv[u] << 16);
+        a0 = fmaf(qn, bf16lo(wv[u]), a0);
+        a1 = fmaf(qn, bf16hi(wv[u]), a1);
+      }
   }
-  qa[e] = acc;
+  qa[2 * e2] = a0;
+  qa[2 * e2 + 1] = a1;
   if (blockIdx.x == 0) qa[ML_DC + tid] = __uint_as_float((uint32_t)qq[DN + tid] << 16);
 }
 
@@ -252,7 +258,7 @@ extern "C" int spc_mla_sparse_attn(const void* q, const void* const* cache, cons
   if (ws_bytes < spc_mla_workspace(L, B, H, k)) return SPC_E_WORKSPACE;
   MlaWs w = mla_ws_layout(ws, L, B, H, k);
   cudaStream_t st = as_stream(stream);
-  SPC_TRY(launched(launch_k(mla_absorb_kernel, dim3(ML_DC / 64, B * H, L), dim3(64), 0, st,
+  SPC_TRY(launched(launch_k(mla_absorb_kernel, dim3(ML_DC / 128, B * H, L), dim3(64), 0, st,
                             (const uint16_t*)q, w_uk, B * H, H, DN, w.qabs)));
   return launched(launch_k(mla_attn_kernel, dim3(w.nsplit, B * H, L), dim3(ML_WARPS * 32), 0, st,
                            cache, w_uv, idx, count, B * H, H, Smax, k, DV,
