@@ -207,3 +207,44 @@ def test_native_decode_step_equals_pipeline(S, B, G):
         assert torch.equal(ia, idx[cur]) and torch.equal(ca, cnt[cur])
         assert torch.equal(st.n_load, nl)
         assert torch.equal(st.out, out)
+
+
+def test_offload_step_token_major_records(oracle):
+    """The config-D path at small size: LLM KV as token-major records in pinned host memory
+    ([B][G][S][L][2][D]), SLOTS mode with spc_gather_kv_strided over PCIe: over three steps
+    the selection is bit-exact, the budget slots hold exactly the selected tokens' rows, and
+    the attention matches the oracle."""
+    B, G, Hq, D, S, L, k = 1, 2, 8, 64, 3000, 3, 256
+    dev = torch.device("cuda")
+    kr = synth.retrieval_keys(B, G, S, D, seed=21, device=dev)
+    qr = synth.retrieval_queries(3, B, Hq, G, D, seed=21, device=dev)
+    ql = synth.llm_queries(1, L, B, Hq, D, seed=21, device=dev)[0]
+    rec = synth.normal_bf16((B, G, S, L, 2, D), 22).pin_memory()
+    k_src = [rec[:, :, :, l, 0] for l in range(L)]
+    v_src = [rec[:, :, :, l, 1] for l in range(L)]
+    kb = torch.zeros((L, B, G, k, D), dtype=torch.bfloat16, device=dev)
+    vb = torch.zeros_like(kb)
+    seq = torch.full((B,), S, dtype=torch.int32, device=dev)
+    st = DecodeStep(kr, [kb[l] for l in range(L)], [vb[l] for l in range(L)], seq, L, Hq, k,
+                    mode="slots", k_src_layers=k_src, v_src_layers=v_src, kv_rows=k, src_rows=S,
+                    src_strides=(L * 2 * D, S * L * 2 * D))
+    kr_h = synth.bf16_bits(kr)
+    kc = rec[..., 0, :].permute(3, 0, 1, 2, 4).contiguous()  # [L][B][G][S][D]
+    vc = rec[..., 1, :].permute(3, 0, 1, 2, 4).contiguous()
+    kh, vh = synth.bf16_bits(kc), synth.bf16_bits(vc)
+    c = dict(synth.CONFIGS["A"], B=B, G=G, Hq=Hq, D=D, S=S, L=L, k=k)
+    for s in range(3):
+        idx_d, cnt_d = st.step(qr[s], ql, use_graph=True)
+        torch.cuda.synchronize()
+        idx, cnt = oracle_step(oracle, c, kr_h, synth.bf16_bits(qr[s]), S, st.scale)
+        assert np.array_equal(idx_d.cpu().numpy(), idx) and np.array_equal(cnt_d.cpu().numpy(), cnt)
+        slots = st.slot_tok.cpu().numpy()
+        kbh = kb.cpu()
+        for g in range(G):
+            assert sorted(slots[0, g, :cnt[0, g]].tolist()) == idx[0, g, :cnt[0, g]].tolist()
+            for sl in (0, cnt[0, g] // 2, cnt[0, g] - 1):
+                t = int(slots[0, g, sl])
+                assert torch.equal(kbh[1, 0, g, sl], kc[1, 0, g, t])
+        oo, _ = oracle.sparse_attn(synth.bf16_bits(ql), [kh[l] for l in range(L)],
+                                   [vh[l] for l in range(L)], idx, cnt, st.scale)
+        assert np.abs(st.out.cpu().numpy() - oo).max() <= 2e-3
