@@ -249,7 +249,10 @@ extern "C" int spc_sparse_decode_attn(int dtype, const void* q, const void* cons
   // persistent bf16 path: AT2_CTAS_PER_SM CTAs per SM, contiguous chunk-aligned row ranges
   const int kpad = (k + CH - 1) / CH * CH;  // groups padded to whole chunks
   const long long v_total = (long long)n_groups * kpad;
-  const int ncta_target = AT2_CTAS_PER_SM * num_sms();
+#ifndef SPC_ATTN_OVERSUB
+#define SPC_ATTN_OVERSUB 1
+#endif
+  const int ncta_target = AT2_CTAS_PER_SM * num_sms() * SPC_ATTN_OVERSUB;
   long long rpc = (v_total + ncta_target - 1) / ncta_target;
   rpc = (rpc + CH - 1) / CH * CH;
   const int ncta = (int)((v_total + rpc - 1) / rpc);
