@@ -89,3 +89,28 @@ def test_host_validation_without_gpu(libspc):
     # planner: C <= 0 is a capacity error
     c = spc.plan_cfg(10, 100, 2, 1, 1, 1, 2)
     assert libspc.spc_plan_thresholds(ctypes.byref(c), P) == 3
+
+
+def test_plain_c_program_links_against_the_abi(tmp_path, libspc):
+    """The boundary is a C ABI: a C99 program that includes include/spc.h (pedantic, -Werror)
+    links against libspc.so and calls it (no GPU needed for these host entry points)."""
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    src = tmp_path / "use_spc.c"
+    src.write_text(
+        '#include <stdio.h>\n#include "spc.h"\n'
+        "int main(void) {\n"
+        "  spc_plan_cfg c = {180000000000LL, 16060000000LL, 1.3, 32, 8, 128, 1, 32, 2048, 2};\n"
+        "  int64_t th[33];\n"
+        "  if (spc_plan_thresholds(&c, th) != SPC_OK) return 2;\n"
+        "  printf(\"%d %lld %s\\n\", spc_version(), (long long)th[0], spc_status_string(SPC_E_BUDGET));\n"
+        "  return spc_decode_step(NULL, NULL) == SPC_E_NULL ? 0 : 3;\n"
+        "}\n")
+    exe = tmp_path / "use_spc"
+    libdir = os.path.join(root, "paper_2512_00722_b200")
+    subprocess.check_call(["gcc", "-std=c99", "-Wall", "-Wextra", "-pedantic", "-Werror",
+                           "-I", os.path.join(root, "include"), str(src), "-L", libdir, "-lspc",
+                           "-o", str(exe)])
+    out = subprocess.check_output([str(exe)], env=dict(os.environ, LD_LIBRARY_PATH=libdir), text=True)
+    ver, th0, msg = out.split(maxsplit=2)
+    assert int(ver) == 100 and int(th0) == 36788 and "BUDGET" in msg
