@@ -196,7 +196,7 @@ int launch_logits(const uint16_t* kr, const uint16_t* q, const int32_t* seq_len,
                            smem, st, kr, q, seq_len, G, Smax, scale, tpr, ntiles, logits,
                            tile_max, ctr)));
   const int nh = B * G * ALPHA;
-  return launched(launch_k(lg_finalize_kernel, dim3((nh + 3) / 4), dim3(128), 0, st,
+  return launched(launch_k(lg_finalize_kernel, dim3(nh), dim3(256), 0, st,
                            (const float*)tile_max, tpr, nh, head_max, ctr));
 }
 
