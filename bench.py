@@ -54,6 +54,18 @@ def dist_env():
             int(os.environ.get("WORLD_SIZE", "1")))
 
 
+def warm_graphs(st, graphs):
+    """Replay every captured step graph once, untimed, then reset the rolling selection
+    state: a CUDA graph's first launch carries a one-time upload cost that is not part of a
+    decode step (all timed steps are then steady-state launches)."""
+    import torch
+    for g in graphs:
+        g.replay()
+        st.parity ^= 1
+    torch.cuda.synchronize()
+    st.reset_state()
+
+
 def traffic_of(key):
     """ncu DRAM bytes per launch recorded in profiles/traffic.json (None if absent)."""
     try:
@@ -250,7 +262,7 @@ def bench_ours(args):
     seq_graphs = st.capture_sequence([(i % NSETS, qr[i], ql[i % 2]) for i in range(nsteps)])
     launches_per_step = (spc.launch_count() - n0) // (2 * NSETS + nsteps)
     stream = torch.cuda.current_stream()
-    st.reset_state()
+    warm_graphs(st, seq_graphs)
 
     def one_step(i):
         seq_graphs[i].replay()
@@ -343,6 +355,11 @@ def bench_ours(args):
     out_h = torch.empty(st.out.shape, dtype=torch.float32).pin_memory()
     e2 = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
     bi = bo = 0
+    for j in range(max(args.warmup, 2 * NSETS)):  # untimed: every (set, parity) graph once
+        st.use_set(j % NSETS)
+        st.step_host(q_ret_h, q_llm_h, out_h, use_graph=True)
+    st.sync_host()
+    torch.cuda.synchronize()
     e2[0].record(stream)
     for j in range(args.steps):
         st.use_set(j % NSETS)
@@ -617,7 +634,7 @@ def bench_grow(args):
     n0 = spc.launch_count()
     seq_graphs = st.capture_sequence([(0, qr[i], ql[i % 2]) for i in range(nsteps)])
     launches_per_step = (spc.launch_count() - n0) // nsteps
-    st.reset_state()
+    warm_graphs(st, seq_graphs)
     seq.fill_(S0)
     stream = torch.cuda.current_stream()
 
@@ -742,7 +759,7 @@ def bench_offload(args):
     n0 = spc.launch_count()
     seq_graphs = st.capture_sequence([(0, qr[i], ql[i % 2]) for i in range(nsteps)])
     launches_per_step = (spc.launch_count() - n0) // nsteps
-    st.reset_state()
+    warm_graphs(st, seq_graphs)
     kb.zero_()
     vb.zero_()
     stream = torch.cuda.current_stream()

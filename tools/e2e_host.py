@@ -19,11 +19,15 @@ qr = synth.retrieval_queries(2, B, Hq, G, D, seed=1, device=dev)
 ql = synth.llm_queries(1, L, B, Hq, D, seed=1, device=dev)[0]
 seq = torch.full((B,), S, dtype=torch.int32, device=dev)
 st = DecodeStep(kr, [kc[l] for l in range(L)], [vc[l] for l in range(L)], seq, L, Hq, k)
+NSETS = int(os.environ.get("E2E_SETS", "3"))
+for _ in range(NSETS - 1):
+    st.add_input_set(kr.clone(), [x.clone() for x in kc], [x.clone() for x in vc])
 st.step(qr[0], ql)
 st.capture()
 qh, lh = qr[1].cpu().pin_memory(), ql.cpu().pin_memory()
 oh = torch.empty(st.out.shape, dtype=torch.float32).pin_memory()
-for _ in range(20):
+for j in range(20):
+    st.use_set(j % NSETS)
     st.step_host(qh, lh, oh)
 st.sync_host()
 torch.cuda.synchronize()
@@ -31,7 +35,8 @@ N = 300
 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 a.record()
 t0 = time.perf_counter()
-for _ in range(N):
+for j in range(N):
+    st.use_set(j % NSETS)
     st.step_host(qh, lh, oh)
 t1 = time.perf_counter()
 st.sync_host()
@@ -39,7 +44,8 @@ b.record()
 torch.cuda.synchronize()
 print(f"host {1e6 * (t1 - t0) / N:.1f} us per step_host call; GPU {a.elapsed_time(b) * 1e3 / N:.1f} us per step")
 a.record()
-for _ in range(N):
+for j in range(N):
+    st.use_set(j % NSETS)
     st.step(use_graph=True)
 b.record()
 torch.cuda.synchronize()
