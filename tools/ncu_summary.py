@@ -22,6 +22,9 @@ KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "smsp__inst_executed.sum", "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active"]
 
 
+LIBSPC = re.compile(r"spc::|unnamed>::|anonymous namespace")
+
+
 def short(name):
     name = re.sub(r"\(.*", "", name)
     return name.replace("spc::", "").replace("(anonymous namespace)::", "").replace("<unnamed>::", "")
@@ -35,7 +38,7 @@ def launches(path, out, title):
     for r in rows[1:]:
         if len(r) <= vi or r[hdr.index("Metric Name")] != "gpu__time_duration.sum":
             continue
-        if "spc::" not in r[ki]:  # libspc kernels only (not torch set-up / spin kernels)
+        if not LIBSPC.search(r[ki]):  # libspc kernels only (not torch set-up / spin kernels)
             continue
         acc.setdefault(short(r[ki]), []).append(float(r[vi].replace(",", "")) / 1e3)
     total = sum(sum(v) / len(v) for v in acc.values())
