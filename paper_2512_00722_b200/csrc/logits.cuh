@@ -30,10 +30,13 @@
 #ifndef SPC_LG_WARPS
 #define SPC_LG_WARPS 6
 #endif
-constexpr int LG_RPT = 4;                 // rows per lane (2 FFMA2 row pairs)
+#ifndef SPC_LG_RPT
+#define SPC_LG_RPT 4
+#endif
+constexpr int LG_RPT = SPC_LG_RPT;        // rows per lane (LG_RPT / 2 FFMA2 row pairs)
 constexpr int LG_TR = 32 * LG_RPT;        // rows per tile
 constexpr int LG_DCH = 64;                // d per pipeline step (128-byte row pieces)
-constexpr int LG_STAGE = LG_TR * LG_DCH * 2;  // 16 KiB, unpadded (swizzled granules)
+constexpr int LG_STAGE = LG_TR * LG_DCH * 2;  // 16 KiB at 4 rows per lane, unpadded (swizzled granules)
 constexpr int LG_NST = 2;                 // per-warp ring depth: one step loads while one computes
 template <int ALPHA>
 constexpr int lg_warps() {  // warps per CTA (one CTA per SM), bounded by shared memory
