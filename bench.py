@@ -323,8 +323,8 @@ def bench_ours(args):
             spc.elastic_diff(st.idx[prev], st.cnt[prev], st.idx[cur], st.cnt[cur],
                              st.load_tok, st.n_load)
         e[-2].record(stream)
-        spc.sparse_decode_attn(st.q_llm, st.k_tab, st.v_tab, spc.KV_INDEXED, st.idx[cur],
-                               st.cnt[cur], st.rows, k, st.scale, st.out, st.lse, st.ws_attn, G)
+        spc.sparse_decode_attn_kv(st.desc, st.q_llm, spc.KV_INDEXED, st.idx[cur], st.cnt[cur], k,
+                                  st.scale, st.out, st.lse, st.ws_attn)
         e[-1].record(stream)
         torch.cuda.synchronize()
         for i, p in enumerate(phases):
@@ -442,7 +442,7 @@ def bench_ours(args):
                        "n_load_last_step": n_load_tot, "with_frontend": fe},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "kernel": "attn_bf16_kernel (spc_sparse_decode_attn, all layers)",
+                         "kernel": "attn_tma_kernel + tma_merge_kernel (spc_sparse_decode_attn_kv, all layers)",
                          "algorithmic_bytes_per_launch": attn_bytes,
                          "peak_source": f"{peak_src} (MEASURED_PEAKS.json hbm_gbs)"},
             "cpu_baseline": cpu,

@@ -273,6 +273,36 @@ int spc_sparse_decode_attn(int dtype, const void* q, const void* const* k_layers
                            int G, int D, int rows, int k, float scale, float* out, float* lse,
                            void* ws, size_t ws_bytes, spc_stream_t stream);
 
+/* ------------------------------------------------------------------------
+ * spc_kv_desc_init / spc_sparse_decode_attn_kv — the same attention (O10, reading
+ * R15; Eq.1 restricted to the selected rows) with the selected rows
+ * gathered by the TMA unit (tile::gather4, 4 rows per request) instead of per-thread
+ * copies: the hot path's kernel.
+ *
+ * spc_kv_desc_init is a SETUP call (synchronous, not capturable, once per KV cache):
+ * it encodes one TMA descriptor per layer for K and for V, each over the layer's
+ * [B*G*rows][D] bf16 tensor, and copies them to `desc` (DEVICE memory of
+ * spc_kv_desc_bytes(L) bytes, 64-byte aligned, caller-owned; valid as long as the
+ * cache allocations it describes).  k_layers / v_layers here are HOST arrays of L
+ * device pointers (16-byte aligned; HBM, not mapped host memory).
+ * Errors: SPC_E_NULL, SPC_E_SHAPE (sizes <= 0, B*G*rows >= 2^31), SPC_E_UNSUPPORTED
+ * (D not 64/128), SPC_E_RANGE (misaligned desc or layer pointer), SPC_E_CUDA.
+ *
+ * spc_sparse_decode_attn_kv: arguments as spc_sparse_decode_attn, with the KV cache
+ * given by `kv_desc` (from spc_kv_desc_init with the same L, B, G, D, rows) instead of
+ * pointer tables; bf16 only.  kv_mode SPC_KV_INDEXED or SPC_KV_SLOTS (then the desc
+ * describes the [B][G][k][D] budget buffers and rows = k).  Same workspace
+ * (spc_attn_workspace, zero-filled once; not shared by calls executing at the same
+ * time).  Results agree with spc_sparse_decode_attn within the O10 tolerance.
+ * ---------------------------------------------------------------------- */
+size_t spc_kv_desc_bytes(int L);
+int spc_kv_desc_init(void* desc, const void* const* k_layers, const void* const* v_layers, int L,
+                     int B, int G, int D, int rows);
+int spc_sparse_decode_attn_kv(const void* kv_desc, const void* q, int kv_mode, const int32_t* idx,
+                              const int32_t* count, int L, int layer_begin, int layer_end, int B,
+                              int Hq, int G, int D, int rows, int k, float scale, float* out,
+                              float* lse, void* ws, size_t ws_bytes, spc_stream_t stream);
+
 /* spc_attn_merge — log-sum-exp merge of P partial attentions, O12.
  * o_parts [P][n][D] f32, lse_parts [P][n] f32 (-inf = empty part);
  * out [n][D] = sum_p e^{lse_p - M} o_p / sum_p e^{lse_p - M}, M = max_p lse_p;
@@ -414,6 +444,8 @@ typedef struct {
   float* lse;                     /* [L][B][Hq] or NULL */
   void* ws;
   size_t ws_bytes;
+  const void* kv_desc;            /* NULL, or spc_kv_desc_init of k_layers / v_layers:
+                                     the attention then runs spc_sparse_decode_attn_kv */
 } spc_step_args;
 size_t spc_decode_step_workspace(int L, int B, int Hq, int G, int D, int Smax, int k);
 int spc_decode_step(const spc_step_args* args, spc_stream_t stream);

@@ -4,22 +4,18 @@
 // retrieval head selected, mapped per KV head (P:324 torch.gather; GQA group
 // sets P:328), renormalised over the subset (reading R15).
 //
-// Split-K flash-decode.  Work item = (layer, request b, KV group g, chunk of
-// 128 selected rows).  The selected K and V rows (256 B each for d = 128 bf16)
-// are gathered straight from the full cache by per-row cp.async.bulk copies
-// (INDEXED) or read from the budget slots (SLOTS) into padded shared rows; no
-// compacted copy is materialised in HBM.  All alpha query heads of the group
-// share each K/V row (GQA: one read of the row serves alpha heads).
-//
-// bf16 path: the contraction [alpha x D]·[D x rows] and [alpha x rows]·[rows x D]
-// runs on mma.sync m16n8k16 (heads padded to 16 rows of the A operand; the
-// score accumulator fragments are re-used as the A operand of P·V, P split
-// into bf16 hi + lo so P keeps ~16 mantissa bits).  The kernel is HBM-bound;
-// the tensor cores only remove the FMA/shuffle instruction load.
-// fp32 path: CUDA-core dot products (used for the 1e-5 tolerance tests).
-//
-// Each CTA writes (m, l, o) partials; the last CTA of a (layer, b, g) merges
-// them with the log-sum-exp rule (O12).
+// Split-K flash-decode, three kernels:
+//  * attn_tma_kernel + tma_merge_kernel (spc_sparse_decode_attn_kv, the hot path): the
+//    selected K and V rows are gathered straight from the cache by the TMA unit
+//    (tile::gather4, 4 rows per request, per-layer descriptors from spc_kv_desc_init);
+//    one producer warp and one mma.sync consumer warp per CTA, 4 CTAs per SM; per-CTA
+//    (m, l, o) partials merged by a PDL-chained merge kernel (attn_tma.cuh).
+//  * attn_bf16_kernel (spc_sparse_decode_attn, pointer tables: any device-addressable
+//    layer pointers): per-warp 16-byte cp.async rings + the same mma.sync math, partials
+//    merged by the CTA completing a group (attn_bf16.cuh).
+//  * attn_f32_kernel: CUDA-core dot products for fp32 inputs (the 1e-5 tolerance tests).
+// All alpha query heads of a group share each K/V row (GQA: one read serves alpha heads);
+// no compacted copy of the selected rows is materialised in HBM.
 #include "common.cuh"
 
 namespace spc {
@@ -99,6 +95,7 @@ __device__ void merge_partials(const float* part_o, const float* part_ml, int ns
 }
 
 #include "attn_bf16.cuh"
+#include "attn_tma.cuh"
 
 // ---------------------------------------------------------------- fp32 / CUDA-core path
 template <int D, int ALPHA>
@@ -280,6 +277,106 @@ extern "C" int spc_sparse_decode_attn(int dtype, const void* q, const void* cons
   }
   AT(64, 1) AT(64, 2) AT(64, 4) AT(64, 8) AT(128, 1) AT(128, 2) AT(128, 4) AT(128, 8)
 #undef AT
+  return SPC_E_UNSUPPORTED;
+}
+
+extern "C" size_t spc_kv_desc_bytes(int L) { return L > 0 ? (size_t)2 * L * sizeof(CUtensorMap) : 0; }
+
+extern "C" int spc_kv_desc_init(void* desc, const void* const* k_layers, const void* const* v_layers,
+                                int L, int B, int G, int D, int rows) {
+  if (!desc || !k_layers || !v_layers) return SPC_E_NULL;
+  if (L <= 0 || B <= 0 || G <= 0 || rows <= 0) return SPC_E_SHAPE;
+  if (!(D == 64 || D == 128)) return SPC_E_UNSUPPORTED;
+  if ((uintptr_t)desc % 64) return SPC_E_RANGE;
+  const uint64_t n_rows = (uint64_t)B * G * rows;
+  if (n_rows >= (1ull << 31)) return SPC_E_SHAPE;  // TMA row coordinates are int32
+  CUtensorMap* h = (CUtensorMap*)std::calloc(2 * (size_t)L, sizeof(CUtensorMap));
+  if (!h) return SPC_E_CUDA;
+  int rc = SPC_OK;
+  for (int l = 0; l < L && rc == SPC_OK; ++l) {
+    if (!k_layers[l] || !v_layers[l] || (uintptr_t)k_layers[l] % 16 || (uintptr_t)v_layers[l] % 16) {
+      rc = !k_layers[l] || !v_layers[l] ? SPC_E_NULL : SPC_E_RANGE;
+      break;
+    }
+    rc = make_tmap_rows_bf16(h + l, k_layers[l], n_rows, (uint32_t)D);
+    if (rc == SPC_OK) rc = make_tmap_rows_bf16(h + L + l, v_layers[l], n_rows, (uint32_t)D);
+  }
+  if (rc == SPC_OK) {
+    const cudaError_t e = cudaMemcpy(desc, h, 2 * (size_t)L * sizeof(CUtensorMap), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+      set_cuda_error(e);
+      rc = SPC_E_CUDA;
+    }
+  }
+  std::free(h);
+  return rc;
+}
+
+namespace spc {
+namespace {
+// per-device, per-instantiation "max dynamic smem" attribute (thread-safe)
+template <int DD, int AA>
+int tma_attr() {
+  static std::atomic<uint64_t> done{0};  // bit per device ordinal < 64
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return launched(e);
+  const uint64_t bit = dev < 64 ? (1ull << dev) : 0ull;
+  if (bit && (done.load(std::memory_order_acquire) & bit)) return SPC_OK;
+  e = cudaFuncSetAttribute(attn_tma_kernel<DD, AA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           TmSmem<DD>::BYTES);
+  if (e != cudaSuccess) {
+    set_cuda_error(e);
+    return SPC_E_CUDA;
+  }
+  done.fetch_or(bit, std::memory_order_acq_rel);
+  return SPC_OK;
+}
+}  // namespace
+}  // namespace spc
+
+extern "C" int spc_sparse_decode_attn_kv(const void* kv_desc, const void* q, int kv_mode,
+                                         const int32_t* idx, const int32_t* count, int L,
+                                         int layer_begin, int layer_end, int B, int Hq, int G, int D,
+                                         int rows, int k, float scale, float* out, float* lse,
+                                         void* ws, size_t ws_bytes, spc_stream_t stream) {
+  if (!kv_desc || !q || !count || !out) return SPC_E_NULL;
+  if (kv_mode == SPC_KV_INDEXED && !idx) return SPC_E_NULL;
+  if (kv_mode != SPC_KV_INDEXED && kv_mode != SPC_KV_SLOTS) return SPC_E_RANGE;
+  if (L <= 0 || B <= 0 || Hq <= 0 || G <= 0 || Hq % G || rows <= 0) return SPC_E_SHAPE;
+  if (k < 1 || k > SPC_MAX_K) return SPC_E_BUDGET;
+  if (kv_mode == SPC_KV_SLOTS && rows < k) return SPC_E_SHAPE;
+  if ((uint64_t)B * G * rows >= (1ull << 31)) return SPC_E_SHAPE;
+  if (layer_begin < 0 || layer_end > L || layer_begin > layer_end) return SPC_E_RANGE;
+  if ((uintptr_t)kv_desc % 64) return SPC_E_RANGE;
+  if (layer_begin == layer_end) return SPC_OK;
+  if (!ws || ws_bytes < spc_attn_workspace(L, B, Hq, D, k)) return SPC_E_WORKSPACE;
+  const int alpha = Hq / G;
+  if (!(D == 64 || D == 128) || !(alpha == 1 || alpha == 2 || alpha == 4 || alpha == 8))
+    return SPC_E_UNSUPPORTED;
+  AttnWs w = attn_ws_layout(ws, L, B, Hq, D, k);
+  const int n_groups = (layer_end - layer_begin) * B * G;
+  const int kpad = (k + TM_RPS - 1) / TM_RPS * TM_RPS;
+  const long long v_total = (long long)n_groups * kpad;
+  const int ncta_target = TM_CTAS * num_sms();
+  long long rpc = (v_total + ncta_target - 1) / ncta_target;
+  rpc = (rpc + TM_RPS - 1) / TM_RPS * TM_RPS;
+  const int ncta = (int)((v_total + rpc - 1) / rpc);
+  cudaStream_t st = as_stream(stream);
+  const CUtensorMap* maps = (const CUtensorMap*)kv_desc;
+#define ATK(DD, AA)                                                                               \
+  if (D == DD && alpha == AA) {                                                                   \
+    SPC_TRY((tma_attr<DD, AA>()));                                                                \
+    SPC_TRY(launched(launch_k(attn_tma_kernel<DD, AA>, dim3(ncta), dim3(TM_THREADS),             \
+                              TmSmem<DD>::BYTES, st, (const uint16_t*)q, maps, L, kv_mode, idx,   \
+                              count, layer_begin, B, G, rows, k, kpad, scale,                     \
+                              (int)(rpc / TM_RPS), n_groups, w.segstride, w.part_o, w.part_ml)));  \
+    return launched(launch_k(tma_merge_kernel<DD, AA>, dim3((n_groups * AA + 3) / 4), dim3(128), \
+                             0, st, w.part_o, w.part_ml, kpad / TM_RPS, (int)(rpc / TM_RPS),      \
+                             n_groups, B, G, layer_begin, w.segstride, out, lse));                \
+  }
+  ATK(64, 1) ATK(64, 2) ATK(64, 4) ATK(64, 8) ATK(128, 1) ATK(128, 2) ATK(128, 4) ATK(128, 8)
+#undef ATK
   return SPC_E_UNSUPPORTED;
 }
 

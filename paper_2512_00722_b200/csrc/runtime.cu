@@ -1,5 +1,5 @@
 // runtime.cu — status strings, launch counter, device queries, TMA descriptor
-// encoding.  Part of libspc.so (see include/spc.h).
+// encoding (row-gather maps of spc_kv_desc_init).  Part of libspc.so (see include/spc.h).
 #include <cudaTypedefs.h>
 
 #include <cstdio>
@@ -41,20 +41,21 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   return fn;
 }
 
-int make_tmap_3d_bf16(CUtensorMap* map, const void* base, uint64_t d0, uint64_t d1, uint64_t d2,
-                      uint32_t box0, uint32_t box1, CUtensorMapSwizzle swz) {
+// 2-D row-gather descriptor of a bf16 [n_rows][D] tensor: boxes of 64 elements x 1 row
+// (one 128-byte half row) with the 128-byte swizzle, for tile::gather4 loads (attn_tma.cuh).
+int make_tmap_rows_bf16(CUtensorMap* map, const void* base, uint64_t n_rows, uint32_t D) {
   auto enc = get_encode();
   if (!enc) {
     snprintf(g_err, sizeof(g_err), "cuTensorMapEncodeTiled unavailable");
     return SPC_E_CUDA;
   }
-  cuuint64_t dims[3] = {d0, d1, d2};
-  cuuint64_t strides[2] = {d0 * 2, d0 * d1 * 2};
-  cuuint32_t box[3] = {box0, box1, 1};
-  cuuint32_t estr[3] = {1, 1, 1};
-  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides,
-                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  cuuint64_t dims[2] = {D, n_rows};
+  cuuint64_t strides[1] = {(cuuint64_t)D * 2};
+  cuuint32_t box[2] = {64, 1};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box,
+                   estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     snprintf(g_err, sizeof(g_err), "cuTensorMapEncodeTiled failed (%d)", (int)r);
     return SPC_E_CUDA;

@@ -44,6 +44,10 @@ extern "C" int spc_decode_step(const spc_step_args* a, spc_stream_t stream) {
     SPC_TRY(spc_elastic_diff(a->prev_idx, a->prev_count, a->cur_idx, a->cur_count, B, G, k,
                              nullptr, a->load_tok, nullptr, a->n_load, nullptr, nullptr, stream));
   }
+  if (a->kv_desc)
+    return spc_sparse_decode_attn_kv(a->kv_desc, a->q_llm, SPC_KV_INDEXED, a->cur_idx, a->cur_count, L,
+                                     0, L, B, Hq, G, D, a->rows, k, a->scale, a->out, a->lse,
+                                     ws + s_b + t_b, a_b, stream);
   return spc_sparse_decode_attn(SPC_BF16, a->q_llm, a->k_layers, a->v_layers, SPC_KV_INDEXED,
                                 a->cur_idx, a->cur_count, L, 0, L, B, Hq, G, D, a->rows, k,
                                 a->scale, a->out, a->lse, ws + s_b + t_b, a_b, stream);

@@ -3,7 +3,8 @@
 Step: spc_score (LOGITS, NORM, GROUP) -> spc_topk (force the
 newest token, R10) -> spc_elastic_diff against the previous step's selection
  -> [SLOTS mode: spc_gather_kv of the new rows into budget slots] ->
-spc_sparse_decode_attn over all L layers (one launch).  In INDEXED mode with
+spc_sparse_decode_attn_kv (TMA row gathers; spc_sparse_decode_attn for fp32) over all L
+layers (one launch + its LSE merge).  In INDEXED mode with
 Smax <= 135168 the NORM..diff calls are the single fused spc_select launch.
 
 The step state (previous selection, slot map) ping-pongs between two buffers,
@@ -58,6 +59,10 @@ class DecodeStep:
         self.rows = kv_rows if kv_rows is not None else self.k_layers[0].shape[2]
         self.k_tab = spc.ptr_table(self.k_layers, self.dev)
         self.v_tab = spc.ptr_table(self.v_layers, self.dev)
+        # bf16 attention runs spc_sparse_decode_attn_kv (TMA row gathers) over per-layer
+        # descriptors of the caches (INDEXED) or of the budget buffers (SLOTS)
+        self.desc = self._make_desc(self.k_layers, self.v_layers, kr.shape[0], kr.shape[1],
+                                    self.rows if mode != "slots" else k, kr.shape[3])
         if mode == "slots":
             assert k_src_layers is not None
             self.k_src, self.v_src = list(k_src_layers), list(v_src_layers)
@@ -94,7 +99,7 @@ class DecodeStep:
         self.parity = 0
         # input sets: address-distinct copies of (kr, K, V) that the step can rotate through
         # (benchmarks use this instead of an L2 flush); set 0 is the one given above
-        self.sets = [(self.kr, self.k_tab, self.v_tab, [self.k_layers, self.v_layers])]
+        self.sets = [(self.kr, self.k_tab, self.v_tab, [self.k_layers, self.v_layers], self.desc)]
         self.cur_set = 0
         self.graphs = {}
         self.fe = None  # retrieval-head front-end (set_frontend)
@@ -116,15 +121,22 @@ class DecodeStep:
     def lse(self):
         return self.lses[self.last]
 
+    def _make_desc(self, k_layers, v_layers, B, G, rows, D):
+        if self.kv_dtype != torch.bfloat16 or not k_layers[0].is_cuda:
+            return None
+        return spc.KvDesc(k_layers, v_layers, B, G, rows, D)
+
     def add_input_set(self, kr, k_layers, v_layers):
         """Register another (retrieval keys, K layers, V layers) copy; returns its index."""
-        self.sets.append((kr, spc.ptr_table(list(k_layers), self.dev),
-                          spc.ptr_table(list(v_layers), self.dev), [k_layers, v_layers]))
+        k_layers, v_layers = list(k_layers), list(v_layers)
+        self.sets.append((kr, spc.ptr_table(k_layers, self.dev), spc.ptr_table(v_layers, self.dev),
+                          [k_layers, v_layers],
+                          self._make_desc(k_layers, v_layers, self.B, self.G, self.rows, self.D)))
         return len(self.sets) - 1
 
     def use_set(self, i: int):
         self.cur_set = i
-        self.kr, self.k_tab, self.v_tab, _ = self.sets[i]
+        self.kr, self.k_tab, self.v_tab, _, self.desc = self.sets[i]
 
     def set_frontend(self, emb, norm_w, w_qk, inv_freq, mscale: float, eps: float = 1e-5):
         """Start every step with the retrieval head's front-end (spc_rethead_qk, NEXT-1): the
@@ -183,9 +195,17 @@ class DecodeStep:
                               self.k_tab, self.v_tab,
                               dtype=spc.BF16 if self.kv_dtype == torch.bfloat16 else spc.F32,
                               stream=stream)
-            spc.sparse_decode_attn(q_llm, self.k_tab, self.v_tab, spc.KV_SLOTS, None,
-                                   self.cnt[cur], self.k, self.k, self.scale, out, lse,
-                                   self.ws_attn, self.G, stream=stream)
+            if self.desc is not None:
+                spc.sparse_decode_attn_kv(self.desc, q_llm, spc.KV_SLOTS, None, self.cnt[cur],
+                                          self.k, self.scale, out, lse, self.ws_attn, stream=stream)
+            else:
+                spc.sparse_decode_attn(q_llm, self.k_tab, self.v_tab, spc.KV_SLOTS, None,
+                                       self.cnt[cur], self.k, self.k, self.scale, out, lse,
+                                       self.ws_attn, self.G, stream=stream)
+        elif self.desc is not None:
+            spc.sparse_decode_attn_kv(self.desc, q_llm, spc.KV_INDEXED, self.idx[cur],
+                                      self.cnt[cur], self.k, self.scale, out, lse, self.ws_attn,
+                                      stream=stream)
         else:
             spc.sparse_decode_attn(q_llm, self.k_tab, self.v_tab, spc.KV_INDEXED,
                                    self.idx[cur], self.cnt[cur], self.rows, self.k, self.scale,

@@ -30,6 +30,7 @@ EXPORTS = [
     "spc_attn_merge", "spc_select", "spc_rethead_qk", "spc_plan_mem_part",
     "spc_plan_thresholds", "spc_plan_max_resident", "spc_plan_step", "spc_mla_workspace",
     "spc_mla_sparse_attn", "spc_decode_step_workspace", "spc_decode_step",
+    "spc_kv_desc_bytes", "spc_kv_desc_init", "spc_sparse_decode_attn_kv",
 ]
 
 
@@ -46,7 +47,7 @@ class StepArgs(ctypes.Structure):
                                         "logits", "head_max", "head_sumfix", "group_score",
                                         "prev_idx", "prev_count", "cur_idx", "cur_count",
                                         "load_tok", "n_load", "out", "lse", "ws")] + \
-        [("ws_bytes", ctypes.c_size_t)]
+        [("ws_bytes", ctypes.c_size_t), ("kv_desc", ctypes.c_void_p)]
 
 
 class PlanCfg(ctypes.Structure):
@@ -109,6 +110,11 @@ def load_library(path: str = LIB_PATH):
     L.spc_sparse_decode_attn.argtypes = [i32, P, P, P, i32, P, P, i32, i32, i32, i32, i32, i32,
                                          i32, i32, i32, f32, P, P, P, sz, P]
     L.spc_attn_merge.argtypes = [P, P, i32, i32, i32, P, P, P]
+    L.spc_kv_desc_bytes.argtypes = [i32]
+    L.spc_kv_desc_bytes.restype = sz
+    L.spc_kv_desc_init.argtypes = [P, P, P, i32, i32, i32, i32, i32]
+    L.spc_sparse_decode_attn_kv.argtypes = [P, P, i32, P, P, i32, i32, i32, i32, i32, i32, i32,
+                                            i32, i32, f32, P, P, P, sz, P]
     L.spc_select.argtypes = [P, P, P, i32, i32, i32, i32, i32, i32, P, P, P, P, P, P, P, P, P, P,
                              P]
     for name in EXPORTS:  # every symbol must resolve (raises AttributeError otherwise)
@@ -290,7 +296,8 @@ def decode_step(args: "StepArgs", stream=None):
 
 def make_step_args(q_ret, kr, seq_len, q_llm, k_tab, v_tab, rows: int, k: int, scale: float,
                    logits, head_max, head_sumfix, group_score, prev_idx, prev_count, cur_idx,
-                   cur_count, load_tok, n_load, out, lse, ws, force_last: bool = True) -> StepArgs:
+                   cur_count, load_tok, n_load, out, lse, ws, force_last: bool = True,
+                   kv_desc=None) -> StepArgs:
     L, B, Hq, D = q_llm.shape
     G = kr.shape[1]
     ptr = lambda t: None if t is None else int(t.data_ptr())  # noqa: E731
@@ -298,7 +305,7 @@ def make_step_args(q_ret, kr, seq_len, q_llm, k_tab, v_tab, rows: int, k: int, s
                     ptr(q_ret), ptr(kr), ptr(seq_len), ptr(q_llm), ptr(k_tab), ptr(v_tab),
                     ptr(logits), ptr(head_max), ptr(head_sumfix), ptr(group_score), ptr(prev_idx),
                     ptr(prev_count), ptr(cur_idx), ptr(cur_count), ptr(load_tok), ptr(n_load),
-                    ptr(out), ptr(lse), ptr(ws), ws.numel())
+                    ptr(out), ptr(lse), ptr(ws), ws.numel(), ptr(kv_desc))
 
 
 def sparse_decode_attn(q, k_tab, v_tab, kv_mode: int, idx, count, rows: int, k: int, scale: float,
@@ -309,6 +316,42 @@ def sparse_decode_attn(q, k_tab, v_tab, kv_mode: int, idx, count, rows: int, k: 
                                         _p(idx), _p(count), L, layer_begin, layer_end, B, Hq, G, D,
                                         rows, k, float(scale), _p(out), _p(lse), _p(ws),
                                         ws.numel(), _s(stream)), "spc_sparse_decode_attn")
+
+
+class KvDesc:
+    """spc_kv_desc_init: the per-layer TMA descriptors of an LLM KV cache, held in a device
+    buffer.  k_layers / v_layers: L bf16 tensors, each holding a [B][G][rows][D] cache from
+    its first element (4-D tensors of that shape, or flat views with B, G, rows, D given).
+    The tensors must outlive the descriptor (it keeps references)."""
+
+    def __init__(self, k_layers, v_layers, B=None, G=None, rows=None, D=None):
+        L = len(k_layers)
+        if B is None:
+            B, G, rows, D = k_layers[0].shape
+        for t in list(k_layers) + list(v_layers):
+            assert t.dtype == torch.bfloat16 and t.is_contiguous() and t.is_cuda
+            assert t.numel() >= B * G * rows * D
+        self.L, self.B, self.G, self.rows, self.D = L, B, G, rows, D
+        self._keep = (list(k_layers), list(v_layers))
+        nbytes = int(lib().spc_kv_desc_bytes(L))
+        self.buf = torch.empty(nbytes, dtype=torch.uint8, device=k_layers[0].device)
+        kp = (ctypes.c_void_p * L)(*[t.data_ptr() for t in k_layers])
+        vp = (ctypes.c_void_p * L)(*[t.data_ptr() for t in v_layers])
+        _check(lib().spc_kv_desc_init(_p(self.buf), kp, vp, L, B, G, D, rows), "spc_kv_desc_init")
+
+    def data_ptr(self) -> int:
+        return self.buf.data_ptr()
+
+
+def sparse_decode_attn_kv(desc: KvDesc, q, kv_mode: int, idx, count, k: int, scale: float, out,
+                          lse, ws, layer_begin: int = 0, layer_end=None, stream=None):
+    """spc_sparse_decode_attn_kv: the attention with TMA row gathers (bf16)."""
+    L, B, Hq, D = q.shape
+    layer_end = L if layer_end is None else layer_end
+    _check(lib().spc_sparse_decode_attn_kv(_p(desc.buf), _p(q), kv_mode, _p(idx), _p(count), L,
+                                           layer_begin, layer_end, B, Hq, desc.G, D, desc.rows, k,
+                                           float(scale), _p(out), _p(lse), _p(ws), ws.numel(),
+                                           _s(stream)), "spc_sparse_decode_attn_kv")
 
 
 def select(logits, head_max, seq_len, G: int, k: int, head_sumfix, group_score, out_idx,

@@ -178,7 +178,8 @@ def test_batch_level_step_selects_one_set_per_request(oracle):
 def test_native_decode_step_equals_pipeline(S, B, G):
     """spc_decode_step (one C call: score -> select -> attention, or the separate calls when
     the fused select does not apply) is bit-identical to DecodeStep over three steps with
-    the previous selection rolled by the caller."""
+    the previous selection rolled by the caller (the attention through the same TMA
+    descriptors, spc_step_args.kv_desc)."""
     Hq, D, L, k = 4 * G, 64, 2, 256
     dev = torch.device("cuda")
     kr = synth.retrieval_keys(B, G, S, D, seed=12, device=dev)
@@ -200,7 +201,8 @@ def test_native_decode_step_equals_pipeline(S, B, G):
     for s in range(3):
         cur, prev = s % 2, 1 - s % 2
         a = spc.make_step_args(qr[s], kr, seq, ql, ktab, vtab, S, k, st.scale, lg, hm, F, gs,
-                               idx[prev], cnt[prev], idx[cur], cnt[cur], lt, nl, out, lse, ws)
+                               idx[prev], cnt[prev], idx[cur], cnt[cur], lt, nl, out, lse, ws,
+                               kv_desc=st.desc)
         spc.decode_step(a)
         ia, ca = st.step(qr[s], ql)
         torch.cuda.synchronize()
