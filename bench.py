@@ -294,7 +294,8 @@ def bench_ours(args):
     cnt_tot = int(st.cnt[st.parity ^ 1].sum().item())
 
     # ---- per-kernel breakdown: eager steps with events between the phases (same stream)
-    phases = ["logits", "select", "attn"] if st.fused else ["score", "topk", "diff", "attn"]
+    phases = (["score_select", "attn"] if st.one_launch else
+              ["logits", "select", "attn"] if st.fused else ["score", "topk", "diff", "attn"])
     acc = {p: 0.0 for p in phases}
     reps = max(3, min(args.steps, 12))
     for j in range(reps):
@@ -306,7 +307,11 @@ def bench_ours(args):
         # the events then time the kernels back to back, not the host's launch latency
         torch.cuda._sleep(4_000_000)
         e[0].record(stream)
-        if st.fused:
+        if st.one_launch:
+            spc.score_select(st.q_ret, st.kr, st.seq_len, st.scale, k, st.head_max, st.head_sumfix,
+                             st.gs, st.idx[cur], st.cnt[cur], st.idx[prev], st.cnt[prev],
+                             st.load_tok, st.n_load, st.ws_ss, force_last=True)
+        elif st.fused:
             spc.score(st.q_ret, st.kr, st.seq_len, G, st.scale, st.logits, st.head_max,
                       st.head_sumfix, st.gs, st.ws_score, phases=spc.SCORE_LOGITS)
             e[1].record(stream)

@@ -163,6 +163,34 @@ int spc_topk_filter(int32_t* idx, const float* val, int32_t* count, const uint64
                     int k, int id_stride, int id_offset, spc_stream_t stream);
 
 /* ------------------------------------------------------------------------
+ * spc_score_select — the whole single-device selection of a decode step in ONE
+ * persistent launch: spc_score(LOGITS) + spc_select, bit-identical to them (O1..O8:
+ * Eq.1, group max P:328, top-k P:267, S_now - S_last P:374).  Each SM keeps the
+ * logits of its own key tiles in shared memory; the phases meet at grid-wide barriers
+ * (the launch is cooperative: all CTAs co-resident).
+ * q [B][Hq][D] bf16, kr [B][G][Smax][D] bf16 (16-byte aligned); logits [B][Hq][Smax]
+ * f32 is written when non-NULL (tokens >= seq_len untouched); head_max [B][Hq],
+ * head_sumfix [B][Hq], group_score [B][G][Smax] (0 past seq_len), out_idx / out_count,
+ * load_tok / n_load, evict_tok / n_evict (may be NULL) as spc_select; prev_idx rows
+ * ascending.  ws >= spc_score_select_workspace(B, Hq, G, Smax) bytes, zero-filled once
+ * (the kernel leaves it zero-filled); not shared by calls executing at the same time.
+ * Supported when spc_score_select_supported() returns 1: D in {64,128}, alpha in
+ * {1,2,4,8}, 1 <= k <= SPC_MAX_K, and B*G*ceil(Smax/128) key tiles spread over the SMs
+ * at <= 16 tiles per SM (config B: 2048 tiles, 14 per SM) -- SPC_E_UNSUPPORTED
+ * otherwise (use spc_score + spc_select or the separate calls).
+ * Errors: SPC_E_NULL, SPC_E_SHAPE, SPC_E_BUDGET, SPC_E_RANGE (alignment),
+ * SPC_E_WORKSPACE, SPC_E_UNSUPPORTED, SPC_E_CUDA.
+ * ---------------------------------------------------------------------- */
+int spc_score_select_supported(int B, int Hq, int G, int D, int Smax, int k);
+size_t spc_score_select_workspace(int B, int Hq, int G, int Smax);
+int spc_score_select(const void* q, const void* kr, const int32_t* seq_len, int B, int Hq, int G,
+                     int D, int Smax, float scale, int k, int force_last, float* logits,
+                     float* head_max, int64_t* head_sumfix, float* group_score, int32_t* out_idx,
+                     int32_t* out_count, const int32_t* prev_idx, const int32_t* prev_count,
+                     int32_t* load_tok, int32_t* n_load, int32_t* evict_tok, int32_t* n_evict,
+                     void* ws, size_t ws_bytes, spc_stream_t stream);
+
+/* ------------------------------------------------------------------------
  * spc_select — the single-device step from the logits to the elastic diff in ONE
  * launch: spc_score(NORM | GROUP) + spc_topk(id_stride 1, id_offset 0) +
  * spc_elastic_diff(INDEXED mode, slot_tok = NULL), bit-identical to those

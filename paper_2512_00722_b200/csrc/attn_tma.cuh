@@ -57,22 +57,6 @@ __device__ __forceinline__ void tm_gather4(uint32_t dst, const CUtensorMap* map,
       "l"(map), "r"(bar), "r"(col), "r"(r0), "r"(r1), "r"(r2), "r"(r3)
       : "memory");
 }
-__device__ __forceinline__ void tm_arrive(uint32_t bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
-}
-__device__ __forceinline__ void tm_expect(uint32_t bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void tm_wait(uint32_t bar, uint32_t ph) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n"
-      "TMW_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-      "@!p bra TMW_%=;\n\t}" ::"r"(bar),
-      "r"(ph)
-      : "memory");
-}
-
 // Debug trace (-DSPC_TRACE builds, spc_debug_set_trace): per CTA c < 2048,
 // g_trace[4096 + 4c + i] = %globaltimer at (0) entry after the PDL wait, (1) the consumer's
 // first stage landed, (2) the consumer's last stage done (the CTA's end).

@@ -8,6 +8,7 @@
 #include <stdint.h>
 
 #include <atomic>
+#include <cstdio>
 #include <cstdlib>
 
 #include "../../include/spc.h"
@@ -86,6 +87,9 @@ int num_sms();
 // Encode the row-gather TMA descriptor of a bf16 [n_rows][D] tensor (driver entry point
 // fetched through cudart): 64-element x 1-row boxes, 128-byte swizzle.
 int make_tmap_rows_bf16(CUtensorMap* map, const void* base, uint64_t n_rows, uint32_t D);
+// ... and the tile-streaming one: boxes of 64 elements x box_rows rows, 128-byte swizzle.
+int make_tmap_tile_bf16(CUtensorMap* map, const void* base, uint64_t n_rows, uint32_t D,
+                        uint32_t box_rows);
 
 // --------------------------------------------------------------- device side
 __device__ __forceinline__ void spc_pdl_entry() {
@@ -211,6 +215,37 @@ __device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
 // ------------------------------------------------------------- TMA descriptors
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
+}
+// mbarrier arrive / arrive.expect_tx / parity wait on 32-bit shared addresses
+__device__ __forceinline__ void tm_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void tm_expect(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void tm_wait(uint32_t bar, uint32_t ph) {
+#ifdef SPC_SS_DEBUG
+  for (long long n = 0;; ++n) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(bar), "r"(ph)
+        : "memory");
+    if (ok) return;
+    if (n == (1ll << 24)) {
+      printf("mbarrier stuck: cta %d tid %d bar %u phase %u\n", blockIdx.x, threadIdx.x, bar, ph);
+      return;
+    }
+  }
+#endif
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "TMW_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra TMW_%=;\n\t}" ::"r"(bar),
+      "r"(ph)
+      : "memory");
 }
 __device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(map) : "memory");

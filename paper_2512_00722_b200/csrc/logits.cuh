@@ -269,3 +269,218 @@ __global__ void __launch_bounds__(256) lg_finalize_kernel(const float* __restric
   }
   (void)nheads;
 }
+
+// ------------------------------------------------------------------------------------
+// logits_tma_kernel — the same phase (O1 chains, O2 per-tile maxima, same outputs) with the
+// key tiles streamed by the TMA unit.  One CTA per SM = one producer warp + LT_NC consumer
+// warps over a ring of half-tile stages (128 rows x 64 d = 16 KiB, 2-D tensor-map boxes
+// with the 128-byte swizzle: granule g of row r at g ^ (r & 7), the layout the consumer's
+// conflict-free LDS.128 expects).  The producer lane issues, per stage, one
+// cp.async.bulk.tensor.2d box (and on a tile's first stage a 1-D bulk copy of the group's
+// raw bf16 query), completion counted on the stage's mbarrier; consumers take whole tiles
+// round robin, each from its own ring of K stages, run the unchanged FFMA2 inner loop and
+// release each stage.  CTA c owns the
+// contiguous tiles [c*n/grid, (c+1)*n/grid).  Measured (tools/tmatile.cu): 64 MiB streamed
+// by 16 KiB TMA boxes in 12.65 us per back-to-back launch vs 12.41 us for an LDG.128 stream
+// -- the consumers no longer spend issue slots on 16-byte copies.
+#ifndef SPC_LT_NC
+#define SPC_LT_NC 4
+#endif
+constexpr int LT_NC = SPC_LT_NC;     // consumer warps
+constexpr int LT_STAGE = LG_TR * 128;  // 128 rows x 128 bytes
+template <int D, int ALPHA>
+struct LtSmem {
+  static constexpr int NCH = D / 64;
+  static constexpr int QRAW = ALPHA * D * 2;
+  static constexpr int QF = D * ALPHA * 4;
+  static constexpr int NST0 = (232448 - 2048 - LT_NC * QF) / (LT_STAGE + QRAW);
+  static constexpr int K = (NST0 > 12 ? 12 : NST0) / LT_NC;  // stages per consumer ring
+  static constexpr int NST = K * LT_NC;
+  static_assert(K >= 1, "ring too shallow");
+  static constexpr int QSLOT_OFF = NST * LT_STAGE;
+  static constexpr int QF_OFF = QSLOT_OFF + NST * QRAW;
+  static constexpr int BYTES = 1024 + QF_OFF + LT_NC * QF;
+};
+
+// O1 on one TMA stage (128 rows x 64 d, 128-byte swizzle): lane l accumulates rows
+// l + 32 r (r < LG_RPT) of the tile, alpha sequential fp32 chains per row, d ascending
+// (chunk c covers d = 64 c .. 64 c + 63), FFMA2 on row pairs with the query value as a
+// scalar-broadcast operand.  qf: the warp's fp32 [D][ALPHA] query table.
+template <int D, int ALPHA>
+__device__ __forceinline__ void lt_stage_math(float2 (&acc)[ALPHA][LG_RPT / 2], uint32_t kc,
+                                              uint32_t qf_s, const float* qf, int c, int lane) {
+  const uint32_t swz = (uint32_t)(lane & 7) << 4;
+  const uint32_t kl = kc + (uint32_t)lane * 128u;
+#ifdef SPC_LT_NOMATH  // debug builds only: the load pipeline alone
+  if (lane < 0)
+#endif
+#pragma unroll 2
+    for (int u = 0; u < 8; ++u) {  // 16-byte granule = 8 consecutive d
+      uint4 w[LG_RPT];
+      const uint32_t ka = kl + (((uint32_t)u << 4) ^ swz);
+#pragma unroll
+      for (int r = 0; r < LG_RPT; ++r) w[r] = lds128(ka + r * 32 * 128);
+      const uint32_t qd = qf_s + (uint32_t)(c * 64 + u * 8) * ALPHA * 4;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        float2 kk[LG_RPT / 2];
+#pragma unroll
+        for (int p = 0; p < LG_RPT / 2; ++p) {
+          const uint32_t x0 = (&w[2 * p].x)[e >> 1], x1 = (&w[2 * p + 1].x)[e >> 1];
+          kk[p] = (e & 1) ? make_float2(bf16hi(x0), bf16hi(x1)) : make_float2(bf16lo(x0), bf16lo(x1));
+        }
+#pragma unroll
+        for (int j = 0; j < ALPHA; j += 4) {
+          if (ALPHA >= 4) {
+            const float4 q4 = lds128f(qd + (uint32_t)(e * ALPHA + j) * 4);
+#pragma unroll
+            for (int p = 0; p < LG_RPT / 2; ++p) {
+              acc[j][p] = ffma2(kk[p], make_float2(q4.x, q4.x), acc[j][p]);
+              acc[j + 1][p] = ffma2(kk[p], make_float2(q4.y, q4.y), acc[j + 1][p]);
+              acc[j + 2][p] = ffma2(kk[p], make_float2(q4.z, q4.z), acc[j + 2][p]);
+              acc[j + 3][p] = ffma2(kk[p], make_float2(q4.w, q4.w), acc[j + 3][p]);
+            }
+          } else if (ALPHA == 2) {
+            const float2 q2 = lds64f(qd + (uint32_t)(e * ALPHA) * 4);
+#pragma unroll
+            for (int p = 0; p < LG_RPT / 2; ++p) {
+              acc[0][p] = ffma2(kk[p], make_float2(q2.x, q2.x), acc[0][p]);
+              acc[ALPHA - 1][p] = ffma2(kk[p], make_float2(q2.y, q2.y), acc[ALPHA - 1][p]);
+            }
+          } else {
+            const float q1 = qf[c * 64 + u * 8 + e];
+#pragma unroll
+            for (int p = 0; p < LG_RPT / 2; ++p) acc[0][p] = ffma2(kk[p], make_float2(q1, q1), acc[0][p]);
+          }
+        }
+      }
+    }
+}
+
+template <int D, int ALPHA>
+__global__ void __launch_bounds__(32 * (LT_NC + 1), 1) logits_tma_kernel(
+    const __grid_constant__ CUtensorMap kmap, const uint16_t* __restrict__ q,
+    const int32_t* __restrict__ seq_len, int G, int Smax, float scale, int tpr, int ntiles,
+    float* __restrict__ logits, float* __restrict__ tile_max) {
+  using SM = LtSmem<D, ALPHA>;
+  constexpr int NCH = SM::NCH, NST = SM::NST;
+  __shared__ __align__(8) uint64_t full[NST], empty[NST];
+  extern __shared__ __align__(16) uint8_t lt_raw[];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int Hq = G * ALPHA;
+  const uint32_t base = (smem_u32(lt_raw) + 1023u) & ~1023u;
+  uint8_t* basep = lt_raw + (base - smem_u32(lt_raw));
+  const uint32_t full0 = smem_u32(&full[0]), empty0 = smem_u32(&empty[0]);
+  const int t_begin = (int)(((long long)blockIdx.x * ntiles) / gridDim.x);
+  const int t_end = (int)(((long long)(blockIdx.x + 1) * ntiles) / gridDim.x);
+  if (tid == 0) {
+    for (int s = 0; s < NST; ++s) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(full0 + 8 * s));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(empty0 + 8 * s));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    prefetch_tmap(&kmap);
+  }
+  __syncthreads();
+  spc_pdl_entry();
+  // a tile is active when its first row is below its request's seq_len
+  auto active = [&](int tile) {
+    const int bg = tile / tpr;
+    return (tile - bg * tpr) * LG_TR < __ldg(seq_len + bg / G);
+  };
+  if (warp == LT_NC) {
+    // ------------------------------------------------------------ producer (lane 0)
+    if (lane == 0) {
+      int nt = 0;  // active-tile counter
+      for (int tile = t_begin; tile < t_end; ++tile) {
+        const int bg = tile / tpr, tt = tile - bg * tpr;
+        if (!active(tile)) {  // an empty tile (ragged batch): its maxima are -inf
+          const int b = bg / G, g = bg - b * G;
+          for (int j = 0; j < ALPHA; ++j)
+            tile_max[((size_t)b * Hq + g * ALPHA + j) * tpr + tt] = -INFINITY;
+          continue;
+        }
+        const int w = nt % LT_NC, n = nt / LT_NC;  // consumer warp and its tile count
+        ++nt;
+        for (int c = 0; c < NCH; ++c) {
+          const int j = n * NCH + c;  // sequence number in warp w's ring
+          const int s = w * SM::K + j % SM::K;
+          if (j >= SM::K) tm_wait(empty0 + 8 * s, ((j / SM::K) - 1) & 1);
+          const uint32_t fb = full0 + 8 * s;
+          tm_expect(fb, LT_STAGE + (c == 0 ? SM::QRAW : 0));
+          asm volatile(
+              "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+              " [%0], [%1, {%2, %3}], [%4];" ::"r"(base + s * LT_STAGE),
+              "l"(&kmap), "r"(64 * c), "r"(bg * Smax + tt * LG_TR), "r"(fb)
+              : "memory");
+          if (c == 0) {
+            const int b = bg / G, g = bg - b * G;
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                    base + SM::QSLOT_OFF + s * SM::QRAW),
+                "l"(q + ((size_t)b * Hq + g * ALPHA) * D), "r"(SM::QRAW), "r"(fb)
+                : "memory");
+          }
+        }
+      }
+    }
+    return;
+  }
+  // -------------------------------------------------------------- consumers
+  float* qf = (float*)(basep + SM::QF_OFF + warp * SM::QF);
+  const uint32_t qf_s = smem_u32(qf);
+  // per-warp rings: every ring has one consumer that waits for every one of its stages
+  // in order, so a parity wait is never more than one phase ahead of its barrier
+  // (consumers sharing one ring and skipping each other's stages can alias phases)
+  int nt = 0;  // active-tile counter
+  for (int tile = t_begin; tile < t_end; ++tile) {
+    if (!active(tile)) continue;
+    const int mine = (nt % LT_NC) == warp, n = nt / LT_NC;
+    ++nt;
+    if (!mine) continue;
+    const int bg = tile / tpr, t0 = (tile - bg * tpr) * LG_TR;
+    const int b = bg / G, g = bg - b * G;
+    const int S = __ldg(seq_len + b);
+    float2 acc[ALPHA][LG_RPT / 2];
+#pragma unroll
+    for (int j = 0; j < ALPHA; ++j)
+#pragma unroll
+      for (int p = 0; p < LG_RPT / 2; ++p) acc[j][p] = make_float2(0.f, 0.f);
+    for (int c = 0; c < NCH; ++c) {
+      const int j = n * NCH + c;
+      const int s = warp * SM::K + j % SM::K;
+      tm_wait(full0 + 8 * s, (j / SM::K) & 1);
+      const uint32_t kc = base + s * LT_STAGE;
+      if (c == 0) {  // raw [ALPHA][D] bf16 -> fp32 [D][ALPHA]
+        const uint16_t* qr = (const uint16_t*)(basep + SM::QSLOT_OFF + s * SM::QRAW);
+        for (int e = lane; e < ALPHA * D; e += 32) {
+          const int j = e / D, d = e - j * D;
+          qf[d * ALPHA + j] = __uint_as_float((uint32_t)qr[e] << 16);
+        }
+        __syncwarp();
+      }
+      lt_stage_math<D, ALPHA>(acc, kc, qf_s, qf, c, lane);
+      __syncwarp();
+      if (lane == 0) tm_arrive(empty0 + 8 * s);  // stage consumed
+    }
+    // O1 final multiply by scale, store, O2 tile max -> tile_max
+    float tm = 0.0f;
+#pragma unroll
+    for (int j = 0; j < ALPHA; ++j) {
+      float* o = logits + ((size_t)b * Hq + g * ALPHA + j) * Smax + t0;
+      float m = -INFINITY;
+#pragma unroll
+      for (int r = 0; r < LG_RPT; ++r) {  // row lane + 32 r = pair r/2, half r%2
+        const int row = lane + 32 * r;
+        const float sv = __fmul_rn((r & 1) ? acc[j][r >> 1].y : acc[j][r >> 1].x, scale);
+        if (t0 + row < S && t0 + row < Smax) {
+          o[row] = sv;
+          m = fmaxf(m, sv);
+        }
+      }
+      m = warp_max(m);
+      if (lane == j) tm = m;
+    }
+    if (lane < ALPHA) tile_max[((size_t)b * Hq + g * ALPHA + lane) * tpr + (tile - bg * tpr)] = tm;
+  }
+}

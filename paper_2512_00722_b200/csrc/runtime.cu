@@ -41,9 +41,14 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   return fn;
 }
 
-// 2-D row-gather descriptor of a bf16 [n_rows][D] tensor: boxes of 64 elements x 1 row
-// (one 128-byte half row) with the 128-byte swizzle, for tile::gather4 loads (attn_tma.cuh).
+// 2-D descriptors of a bf16 [n_rows][D] tensor with the 128-byte swizzle: row gathers
+// (boxes of 64 elements x 1 row, tile::gather4 loads, attn_tma.cuh) and tile streams
+// (64 elements x box_rows rows, logits_tma_kernel).
 int make_tmap_rows_bf16(CUtensorMap* map, const void* base, uint64_t n_rows, uint32_t D) {
+  return make_tmap_tile_bf16(map, base, n_rows, D, 1);
+}
+int make_tmap_tile_bf16(CUtensorMap* map, const void* base, uint64_t n_rows, uint32_t D,
+                        uint32_t box_rows) {
   auto enc = get_encode();
   if (!enc) {
     snprintf(g_err, sizeof(g_err), "cuTensorMapEncodeTiled unavailable");
@@ -51,7 +56,7 @@ int make_tmap_rows_bf16(CUtensorMap* map, const void* base, uint64_t n_rows, uin
   }
   cuuint64_t dims[2] = {D, n_rows};
   cuuint64_t strides[1] = {(cuuint64_t)D * 2};
-  cuuint32_t box[2] = {64, 1};
+  cuuint32_t box[2] = {64, box_rows};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box,
                    estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,

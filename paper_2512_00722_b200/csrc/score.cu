@@ -181,21 +181,41 @@ template <int D, int ALPHA>
 int launch_logits(const uint16_t* kr, const uint16_t* q, const int32_t* seq_len, int B, int G,
                   int Smax, float scale, float* logits, float* tile_max, unsigned* ctr,
                   float* head_max, cudaStream_t st) {
-  const size_t smem = LgSmem<D, ALPHA>::BYTES;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(logits_kernel<D, ALPHA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
-    attr = true;
-  }
   const int tpr = (Smax + LG_TR - 1) / LG_TR;
   const int ntiles = B * G * tpr;
-  const int nw = (ntiles + 1) / 2;  // >= 2 tiles per warp
-  const int ncta = max(1, min(num_sms(), (nw + lg_warps<ALPHA>() - 1) / lg_warps<ALPHA>()));
-  SPC_TRY(launched(launch_k(logits_kernel<D, ALPHA>, dim3(ncta), dim3(32 * lg_warps<ALPHA>()),
-                           smem, st, kr, q, seq_len, G, Smax, scale, tpr, ntiles, logits,
-                           tile_max, ctr)));
   const int nh = B * G * ALPHA;
+  if ((long long)B * G * Smax < (1ll << 31)) {  // TMA-fed kernel (int32 row coordinates)
+    static std::atomic<uint64_t> done{0};  // max-dynamic-smem attribute, per device
+    int dev = 0;
+    SPC_TRY(launched(cudaGetDevice(&dev)));
+    const uint64_t bit = dev < 64 ? 1ull << dev : 0ull;
+    if (!bit || !(done.load(std::memory_order_acquire) & bit)) {
+      const cudaError_t e = cudaFuncSetAttribute(logits_tma_kernel<D, ALPHA>,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 LtSmem<D, ALPHA>::BYTES);
+      if (e != cudaSuccess) return launched(e);
+      done.fetch_or(bit, std::memory_order_acq_rel);
+    }
+    CUtensorMap map;
+    SPC_TRY(make_tmap_tile_bf16(&map, kr, (uint64_t)B * G * Smax, D, LG_TR));
+    const int ncta = max(1, min(num_sms(), ntiles));
+    SPC_TRY(launched(launch_k(logits_tma_kernel<D, ALPHA>, dim3(ncta), dim3(32 * (LT_NC + 1)),
+                              LtSmem<D, ALPHA>::BYTES, st, map, q, seq_len, G, Smax, scale, tpr,
+                              ntiles, logits, tile_max)));
+  } else {
+    const size_t smem = LgSmem<D, ALPHA>::BYTES;
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(logits_kernel<D, ALPHA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)smem);
+      attr = true;
+    }
+    const int nw = (ntiles + 1) / 2;  // >= 2 tiles per warp
+    const int ncta = max(1, min(num_sms(), (nw + lg_warps<ALPHA>() - 1) / lg_warps<ALPHA>()));
+    SPC_TRY(launched(launch_k(logits_kernel<D, ALPHA>, dim3(ncta), dim3(32 * lg_warps<ALPHA>()),
+                             smem, st, kr, q, seq_len, G, Smax, scale, tpr, ntiles, logits,
+                             tile_max, ctr)));
+  }
   return launched(launch_k(lg_finalize_kernel, dim3(nh), dim3(256), 0, st,
                            (const float*)tile_max, tpr, nh, head_max, ctr));
 }
@@ -305,7 +325,7 @@ extern "C" int spc_score(int dtype, const void* q, const void* kr, const int32_t
   if (!(D == 64 || D == 128) || !(alpha == 1 || alpha == 2 || alpha == 4 || alpha == 8))
     return SPC_E_UNSUPPORTED;
   if (!ws || ws_bytes < spc_score_workspace(B, Hq, Smax)) return SPC_E_WORKSPACE;
-  if (((uintptr_t)kr & 15) != 0) return SPC_E_RANGE;
+  if (((uintptr_t)kr & 15) != 0 || ((uintptr_t)q & 15) != 0) return SPC_E_RANGE;
   cudaStream_t st = as_stream(stream);
   ScoreWs w = score_ws_layout(ws, B, Hq, Smax);
 

@@ -5,7 +5,8 @@ newest token, R10) -> spc_elastic_diff against the previous step's selection
  -> [SLOTS mode: spc_gather_kv of the new rows into budget slots] ->
 spc_sparse_decode_attn_kv (TMA row gathers; spc_sparse_decode_attn for fp32) over all L
 layers (one launch + its LSE merge).  In INDEXED mode with
-Smax <= 135168 the NORM..diff calls are the single fused spc_select launch.
+Smax <= 135168 the NORM..diff calls are the single fused spc_select launch, and where
+spc_score_select applies (config B) LOGITS through the diff are ONE persistent launch.
 
 The step state (previous selection, slot map) ping-pongs between two buffers,
 so two CUDA graphs (even / odd step) replay the whole step with one launch
@@ -26,7 +27,7 @@ class DecodeStep:
     def __init__(self, kr: torch.Tensor, k_layers, v_layers, seq_len: torch.Tensor, L: int,
                  Hq: int, k: int, mode: str = "indexed", force_last: bool = True, scale=None,
                  kv_rows=None, k_src_layers=None, v_src_layers=None, fused=None,
-                 src_rows=None, src_strides=None, retrieval: str = "head"):
+                 src_rows=None, src_strides=None, retrieval: str = "head", one_launch=False):
         """kr: retrieval keys [B][G][Smax][D] bf16.  k_layers/v_layers: L tensors [B][G][rows][D]
         (INDEXED: the full caches; SLOTS: the budget buffers [B][G][k][D], with
         k_src_layers/v_src_layers the full caches, device or mapped host).  src_strides =
@@ -47,6 +48,13 @@ class DecodeStep:
                       and kr.shape[0] * kr.shape[1] * 8 <= n_sm and retrieval == "head") \
             if fused is None else fused
         self.B, self.G, self.Smax, self.D = kr.shape
+        # one_launch: spc_score_select (LOGITS through the diff in ONE persistent cooperative
+        # launch, bit-identical) instead of spc_score(LOGITS) + spc_select.  Off by default:
+        # measured slower on config B (47 us in-kernel vs ~41 us for the two launches; its
+        # three grid-wide barriers cost ~2 us each)
+        self.one_launch = bool(one_launch) and (
+            mode == "indexed" and retrieval == "head" and kr.dtype == torch.bfloat16
+            and spc.score_select_supported(kr.shape[0], Hq, kr.shape[1], kr.shape[3], kr.shape[2], k))
         self.L, self.Hq, self.k = L, Hq, k
         self.alpha = Hq // self.G
         self.mode = mode
@@ -94,6 +102,8 @@ class DecodeStep:
         self._h2d = self._d2h = None  # copy streams of step_host, created on first use
         self._ev = {}
         self.ws_score = spc.alloc_workspace(spc.score_workspace(B, Hq, self.Smax), dev)
+        self.ws_ss = spc.alloc_workspace(
+            spc.score_select_workspace(B, Hq, G, self.Smax) if self.one_launch else 1, dev)
         self.ws_topk = spc.alloc_workspace(spc.topk_workspace(B, G, self.Smax, k), dev)
         self.ws_attn = spc.alloc_workspace(spc.attn_workspace(L, B, Hq, D, k), dev)
         self.parity = 0
@@ -164,7 +174,12 @@ class DecodeStep:
             spc.rethead_qk(self.tokens[parity], f["emb"], f["norm_w"], f["eps"], f["w_qk"], f["inv"],
                            f["mscale"], self.fe_pos, self.Hq, self.G, q_ret, self.kr,
                            stream=stream)
-        if self.fused:
+        if self.one_launch:
+            spc.score_select(q_ret, self.kr, self.seq_len, self.scale, self.k, self.head_max,
+                             self.head_sumfix, self.gs, self.idx[cur], self.cnt[cur], self.idx[prev],
+                             self.cnt[prev], self.load_tok, self.n_load, self.ws_ss,
+                             force_last=self.force_last, stream=stream)
+        elif self.fused:
             # LOGITS, then NORM + GROUP + top-k + diff in one cluster launch (spc_select)
             spc.score(q_ret, self.kr, self.seq_len, self.G, self.scale, self.logits,
                       self.head_max, self.head_sumfix, self.gs, self.ws_score,

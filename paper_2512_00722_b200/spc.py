@@ -31,6 +31,7 @@ EXPORTS = [
     "spc_plan_thresholds", "spc_plan_max_resident", "spc_plan_step", "spc_mla_workspace",
     "spc_mla_sparse_attn", "spc_decode_step_workspace", "spc_decode_step",
     "spc_kv_desc_bytes", "spc_kv_desc_init", "spc_sparse_decode_attn_kv",
+    "spc_score_select_supported", "spc_score_select_workspace", "spc_score_select",
 ]
 
 
@@ -110,6 +111,11 @@ def load_library(path: str = LIB_PATH):
     L.spc_sparse_decode_attn.argtypes = [i32, P, P, P, i32, P, P, i32, i32, i32, i32, i32, i32,
                                          i32, i32, i32, f32, P, P, P, sz, P]
     L.spc_attn_merge.argtypes = [P, P, i32, i32, i32, P, P, P]
+    L.spc_score_select_supported.argtypes = [i32, i32, i32, i32, i32, i32]
+    L.spc_score_select_workspace.argtypes = [i32, i32, i32, i32]
+    L.spc_score_select_workspace.restype = sz
+    L.spc_score_select.argtypes = [P, P, P, i32, i32, i32, i32, i32, f32, i32, i32, P, P, P, P, P,
+                                   P, P, P, P, P, P, P, P, sz, P]
     L.spc_kv_desc_bytes.argtypes = [i32]
     L.spc_kv_desc_bytes.restype = sz
     L.spc_kv_desc_init.argtypes = [P, P, P, i32, i32, i32, i32, i32]
@@ -352,6 +358,27 @@ def sparse_decode_attn_kv(desc: KvDesc, q, kv_mode: int, idx, count, k: int, sca
                                            layer_begin, layer_end, B, Hq, desc.G, D, desc.rows, k,
                                            float(scale), _p(out), _p(lse), _p(ws), ws.numel(),
                                            _s(stream)), "spc_sparse_decode_attn_kv")
+
+
+def score_select_supported(B: int, Hq: int, G: int, D: int, Smax: int, k: int) -> bool:
+    return bool(lib().spc_score_select_supported(B, Hq, G, D, Smax, k))
+
+
+def score_select_workspace(B: int, Hq: int, G: int, Smax: int) -> int:
+    return int(lib().spc_score_select_workspace(B, Hq, G, Smax))
+
+
+def score_select(q, kr, seq_len, scale: float, k: int, head_max, head_sumfix, group_score, out_idx,
+                 out_count, prev_idx, prev_count, load_tok, n_load, ws, logits=None, evict_tok=None,
+                 n_evict=None, force_last: bool = True, stream=None):
+    """spc_score_select: LOGITS + NORM + GROUP + top-k + INDEXED diff in one launch."""
+    B, G, Smax, D = kr.shape
+    Hq = q.shape[1]
+    _check(lib().spc_score_select(_p(q), _p(kr), _p(seq_len), B, Hq, G, D, Smax, float(scale), k,
+                                  int(force_last), _p(logits), _p(head_max), _p(head_sumfix),
+                                  _p(group_score), _p(out_idx), _p(out_count), _p(prev_idx),
+                                  _p(prev_count), _p(load_tok), _p(n_load), _p(evict_tok),
+                                  _p(n_evict), _p(ws), ws.numel(), _s(stream)), "spc_score_select")
 
 
 def select(logits, head_max, seq_len, G: int, k: int, head_sumfix, group_score, out_idx,
