@@ -359,14 +359,17 @@ int spc_attn_merge(const float* o_parts, const float* lse_parts, int P, int n, i
  * inv_freq [D/2] f32 (the caller's rotary table, e.g. YaRN-scaled); mscale
  *          multiplies cos and sin (YaRN attention scaling; 1 = plain RoPE)
  * pos      [B] int32 DEVICE: the new token's position = keys already cached,
- *          0 <= pos < Smax
+ *          0 <= pos < Smax; or NULL: pos[b] = seq_len_out[b] - 1, read on the device
+ *          (a decode loop whose seq_len already counts the new token, e.g. a growing
+ *          context that advances seq_len in place every step)
  * q_out    [B][Hq][D] bf16 out (the query spc_score takes)
  * kr       [B][G][Smax][D] bf16 in/out: row pos[b] of every group written
- * seq_len_out [B] int32 out or NULL: pos + 1 (the seq_len spc_score takes)
+ * seq_len_out [B] int32: with pos, out (pos + 1, the seq_len spc_score takes) or NULL;
+ *          with pos NULL, in (unchanged)
  * x_out    [B][H] bf16 out or NULL: xn (the normalised input)
  * Supported: D in {64, 128}, H % 8 == 0, B <= 16, B*H*2 <= 200 KiB.
- * Errors: SPC_E_NULL, SPC_E_SHAPE, SPC_E_RANGE (16-byte alignment of emb,
- * w_qk), SPC_E_UNSUPPORTED, SPC_E_CUDA.
+ * Errors: SPC_E_NULL (also: pos and seq_len_out both NULL), SPC_E_SHAPE, SPC_E_RANGE
+ * (16-byte alignment of emb, w_qk), SPC_E_UNSUPPORTED, SPC_E_CUDA.
  * ---------------------------------------------------------------------- */
 int spc_rethead_qk(const int32_t* token, const void* emb, int V, int H, const void* norm_w,
                    float eps, const void* w_qk, const float* inv_freq, float mscale,

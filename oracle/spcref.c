@@ -351,15 +351,28 @@ static uint16_t f_to_bf16_rn(float f) { /* IEEE RN-even of a finite float to bf1
   return (uint16_t)(u >> 16);
 }
 
+/* Reading R22: r = 1/sqrt(mean(x^2) + eps) with the sum of squares made
+ * exact and order-free: e = ilogb(max|x|), F = sum_h trunc(x_h^2 * 2^(46-2e)) as int64
+ * (each term exact in double and < 2^48), mean = fl64(fl64(F) * 2^(2e-46) / H),
+ * r = fl32(fl64(1 / fl64(sqrt(mean + eps)))); then t = bf16(fl32(x r)), xn = bf16(fl32(w t)). */
 void spcref_rmsnorm_bf16(const uint16_t* x, const uint16_t* w, int H, double eps, uint16_t* out) {
-  double ss = 0.0;
+  float mx = 0.0f;
+  for (int h = 0; h < H; ++h) {
+    const float a = fabsf(bf16_to_f(x[h]));
+    if (a > mx) mx = a;
+  }
+  const int e = mx > 0.0f ? ilogbf(mx) : 0;
+  const double sc = mx > 0.0f ? ldexp(1.0, 46 - 2 * e) : 1.0;
+  long long F = 0;
   for (int h = 0; h < H; ++h) {
     const double v = (double)bf16_to_f(x[h]);
-    ss += v * v;
+    F += (long long)((v * v) * sc); /* C conversion truncates toward zero */
   }
-  const double r = 1.0 / sqrt(ss / (double)H + eps);
+  const double ss = mx > 0.0f ? ldexp((double)F, 2 * e - 46) : 0.0;
+  const double mean = ss / (double)H;
+  const float r = (float)(1.0 / sqrt(mean + (double)(float)eps));
   for (int h = 0; h < H; ++h) {
-    const float t = bf16_to_f(f_to_bf16_rn((float)((double)bf16_to_f(x[h]) * r)));
+    const float t = bf16_to_f(f_to_bf16_rn(bf16_to_f(x[h]) * r));
     const float wv = w ? bf16_to_f(w[h]) : 1.0f;
     out[h] = f_to_bf16_rn(wv * t);
   }

@@ -11,7 +11,8 @@
 //
 // Per request b (DESIGN.md §3 R22-R24):
 //   x   = emb[token[b]]                                   (bf16 row of H)
-//   xn  = bf16(w * bf16(x * r)),  r = 1 / sqrt(mean(x^2) + eps)   (HF Llama RMSNorm)
+//   xn  = bf16(w * bf16(x * r)),  r = 1 / sqrt(mean(x^2) + eps)   (HF Llama RMSNorm; the sum
+//         of squares an exact fixed-point integer sum, R22, so xn is bit-exact)
 //   pre = W_qk xn  (fp32 accumulation; rows [0, Hq*D) = W_q, [Hq*D, (Hq+G)*D) = W_k)
 //   RoPE on the pairs (i, i + D/2) of every head (rotate_half convention), angle
 //   a = fl32(pos[b] * inv_freq[i]), c = cos(a) * mscale, s = sin(a) * mscale
@@ -30,6 +31,22 @@
 
 namespace spc {
 namespace {
+
+// R22: the RMSNorm reciprocal r = 1 / sqrt(mean(x^2) + eps), determinised so
+// the oracle reproduces it bit for bit: e = ilogb(max |x|); F = sum_h trunc(x_h^2 2^(46-2e))
+// as int64 (every term exact in fp64 and < 2^48, so the integer sum is exact and
+// order-free); mean = RN64(RN64(F) 2^(2e-46) / H); r = RN32(RN64(1 / RN64(sqrt(mean + eps)))).
+__device__ __forceinline__ double rms_term_scale(float mx) {
+  return mx > 0.f ? ldexp(1.0, 46 - 2 * ilogbf(mx)) : 1.0;
+}
+__device__ __forceinline__ long long rms_term(float v, double sc) {
+  return __double2ll_rz(__dmul_rn(__dmul_rn((double)v, (double)v), sc));
+}
+__device__ __forceinline__ float rms_r(long long F, float mx, int H, float eps) {
+  const double ss = mx > 0.f ? ldexp(__ll2double_rn(F), 2 * ilogbf(mx) - 46) : 0.0;
+  const double mean = __ddiv_rn(ss, (double)H);
+  return __double2float_rn(__ddiv_rn(1.0, __dsqrt_rn(__dadd_rn(mean, (double)eps))));
+}
 
 constexpr int RH_WARPS = 8;
 #ifndef SPC_RH_UNR
@@ -60,23 +77,29 @@ __global__ void __launch_bounds__(RH_WARPS * 32, RH_CPS) rethead_kernel(
   extern __shared__ __align__(16) uint8_t rh_smem[];
   uint16_t* xs = reinterpret_cast<uint16_t*>(rh_smem);  // [B][H] normalised inputs
   __shared__ float red[RH_WARPS];
+  __shared__ long long redl[RH_WARPS];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
   // ---- RMSNorm of the B embedding rows (every CTA; the rows are L2-resident)
   for (int b = 0; b < B; ++b) {
     const uint16_t* x = emb + (size_t)token[b] * H;
-    float ss = 0.f;
-    for (int h = tid; h < H; h += RH_WARPS * 32) {
-      const float v = bf16_to_f32(x[h]);
-      ss = fmaf(v, v, ss);
-    }
-    ss = warp_sum(ss);
-    if (lane == 0) red[warp] = ss;
+    float mx = 0.f;  // max |x| (exact, order-free)
+    for (int h = tid; h < H; h += RH_WARPS * 32) mx = fmaxf(mx, fabsf(bf16_to_f32(x[h])));
+    mx = warp_max(mx);
+    if (lane == 0) red[warp] = mx;
     __syncthreads();
-    float tot = 0.f;
 #pragma unroll
-    for (int w = 0; w < RH_WARPS; ++w) tot += red[w];
-    const float r = 1.0f / sqrtf(tot / (float)H + eps);
+    for (int w = 0; w < RH_WARPS; ++w) mx = fmaxf(mx, red[w]);
+    const double sc = rms_term_scale(mx);
+    long long F = 0;
+    for (int h = tid; h < H; h += RH_WARPS * 32) F += rms_term(bf16_to_f32(x[h]), sc);
+    F = warp_sum_ll(F);
+    if (lane == 0) redl[warp] = F;
+    __syncthreads();
+    F = 0;
+#pragma unroll
+    for (int w = 0; w < RH_WARPS; ++w) F += redl[w];
+    const float r = rms_r(F, mx, H, eps);
     for (int h = tid; h < H; h += RH_WARPS * 32) {
       const float t = bf16_to_f32(f32_to_bf16_rn(bf16_to_f32(x[h]) * r));
       const float wv = norm_w ? bf16_to_f32(norm_w[h]) : 1.0f;
@@ -86,7 +109,7 @@ __global__ void __launch_bounds__(RH_WARPS * 32, RH_CPS) rethead_kernel(
     }
     __syncthreads();  // red[] is reused by the next request
   }
-  if (seq_len_out && blockIdx.x == 0 && tid < B) seq_len_out[tid] = pos[tid] + 1;
+  if (pos && seq_len_out && blockIdx.x == 0 && tid < B) seq_len_out[tid] = pos[tid] + 1;
 
   // ---- row pairs (i, i + D/2) of head hh: warp-strided over the grid
   const int half = D / 2;
@@ -142,7 +165,7 @@ __global__ void __launch_bounds__(RH_WARPS * 32, RH_CPS) rethead_kernel(
 #pragma unroll
     for (int b = 0; b < BT; ++b) {
       if (lane == b && b < B) {
-        const int pb = pos[b];
+        const int pb = pos ? pos[b] : seq_len_out[b] - 1;  // pos NULL: seq_len counts the new token
         const float ang = (float)pb * inv_freq[i];
         float sn, cs;
         sincosf(ang, &sn, &cs);
@@ -206,19 +229,24 @@ __global__ void __launch_bounds__(RM_WARPS * 32, 1) rethead_mma_kernel(
       continue;
     }
     const uint4* x = reinterpret_cast<const uint4*>(emb + (size_t)token[b] * H);
-    float ss = 0.f;
+    float mx = 0.f;  // R22: max |x|, then the exact fixed-point sum of squares
     for (int c = lane; c < nchunk; c += 32) {
       const uint4 v = __ldg(x + c);
       const uint32_t* pv = &v.x;
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const float lo = bf16lo(pv[e]), hi = bf16hi(pv[e]);
-        ss = fmaf(lo, lo, ss);
-        ss = fmaf(hi, hi, ss);
-      }
+      for (int e = 0; e < 4; ++e) mx = fmaxf(mx, fmaxf(fabsf(bf16lo(pv[e])), fabsf(bf16hi(pv[e]))));
     }
-    ss = warp_sum(ss);
-    const float r = 1.0f / sqrtf(ss / (float)H + eps);
+    mx = warp_max(mx);
+    const double sc = rms_term_scale(mx);
+    long long F = 0;
+    for (int c = lane; c < nchunk; c += 32) {
+      const uint4 v = __ldg(x + c);
+      const uint32_t* pv = &v.x;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) F += rms_term(bf16lo(pv[e]), sc) + rms_term(bf16hi(pv[e]), sc);
+    }
+    F = warp_sum_ll(F);
+    const float r = rms_r(F, mx, H, eps);
     for (int c = lane; c < nchunk; c += 32) {
       const uint4 v = __ldg(x + c);
       const uint4 wv = norm_w ? __ldg(reinterpret_cast<const uint4*>(norm_w) + c)
@@ -238,7 +266,7 @@ __global__ void __launch_bounds__(RM_WARPS * 32, 1) rethead_mma_kernel(
       if (x_out && blockIdx.x == 0) reinterpret_cast<uint4*>(x_out + (size_t)b * H)[c] = ov;
     }
   }
-  if (seq_len_out && blockIdx.x == 0 && tid < B) seq_len_out[tid] = pos[tid] + 1;
+  if (pos && seq_len_out && blockIdx.x == 0 && tid < B) seq_len_out[tid] = pos[tid] + 1;
   __syncthreads();
 
   const int half = D / 2;
@@ -303,7 +331,7 @@ __global__ void __launch_bounds__(RM_WARPS * 32, 1) rethead_mma_kernel(
           const int b = n * 8 + 2 * tig + col;
           if (b < B) {
             const float u = s[col], vv = s[2 + col];  // row gid: pair first, gid + 8: partner
-            const int pb = pos[b];
+            const int pb = pos ? pos[b] : seq_len_out[b] - 1;  // pos NULL: seq_len counts the new token
             float sn, cs;
             sincosf((float)pb * inv, &sn, &cs);
             cs *= mscale;
@@ -330,7 +358,8 @@ extern "C" int spc_rethead_qk(const int32_t* token, const void* emb, int V, int 
                               const float* inv_freq, float mscale, const int32_t* pos, int B,
                               int Hq, int G, int D, int Smax, void* q_out, void* kr,
                               int32_t* seq_len_out, void* x_out, spc_stream_t stream) {
-  if (!token || !emb || !w_qk || !inv_freq || !pos || !q_out || !kr) return SPC_E_NULL;
+  if (!token || !emb || !w_qk || !inv_freq || (!pos && !seq_len_out) || !q_out || !kr)
+    return SPC_E_NULL;
   if (V <= 0 || H <= 0 || B <= 0 || Hq <= 0 || G <= 0 || Hq % G || Smax <= 0) return SPC_E_SHAPE;
   if (!(D == 64 || D == 128) || H % 8 || H > 16384 || B > 16) return SPC_E_UNSUPPORTED;
   if (((uintptr_t)emb & 15) || ((uintptr_t)w_qk & 15)) return SPC_E_RANGE;

@@ -153,10 +153,11 @@ class DecodeStep:
         step then takes token ids (tokens[parity], [B] int32) instead of retrieval queries;
         the front-end writes the query into q_rets[parity] and the token's key into row
         seq_len - 1 of the retrieval key cache (the newest position, Z6), then the step
-        scores it.  Graphs captured before this call are dropped."""
+        scores it -- seq_len is read on the device every step, so a growing context (seq_len
+        advanced in place) appends every new key at its own row.  Graphs captured before this
+        call are dropped."""
         self.fe = dict(emb=emb, norm_w=norm_w, w_qk=w_qk, inv=inv_freq, mscale=float(mscale),
                        eps=float(eps))
-        self.fe_pos = (self.seq_len - 1).to(torch.int32).contiguous()
         self.tokens = [torch.zeros(self.B, dtype=torch.int32, device=self.dev) for _ in range(2)]
         self.graphs = {}
 
@@ -171,9 +172,11 @@ class DecodeStep:
         out, lse = self.outs[parity], self.lses[parity]
         if self.fe is not None:  # token -> query + appended key (NEXT-1)
             f = self.fe
+            # position = seq_len - 1, read on the device every step (pos = NULL): a loop that
+            # advances seq_len in place appends each new key at its own row
             spc.rethead_qk(self.tokens[parity], f["emb"], f["norm_w"], f["eps"], f["w_qk"], f["inv"],
-                           f["mscale"], self.fe_pos, self.Hq, self.G, q_ret, self.kr,
-                           stream=stream)
+                           f["mscale"], None, self.Hq, self.G, q_ret, self.kr,
+                           seq_len_out=self.seq_len, stream=stream)
         if self.one_launch:
             spc.score_select(q_ret, self.kr, self.seq_len, self.scale, self.k, self.head_max,
                              self.head_sumfix, self.gs, self.idx[cur], self.cnt[cur], self.idx[prev],
