@@ -48,6 +48,7 @@ def lib():
                                    ctypes.c_uint32)
         L.spcref_exp.argtypes = [f32]
         L.spcref_exp.restype = f32
+        L.spcref_exp_array.argtypes = [P, P, ctypes.c_longlong]
         L.spcref_exp_max_ulp.argtypes = [u32, u32, P]
         L.spcref_exp_max_ulp.restype = f64
         L.spcref_logits.argtypes = [P, P, P, i32, i32, i32, i32, i32, f32, P, P]
@@ -99,6 +100,14 @@ def _bf16_bits(a) -> np.ndarray:
 # ---------------------------------------------------------------- O3
 def spc_exp(x: float) -> float:
     return float(lib().spcref_exp(ctypes.c_float(x)))
+
+
+def exp_array(x):
+    """O3 over a float32 array (spcref_exp elementwise)."""
+    x = np.ascontiguousarray(x, dtype=np.float32)
+    y = np.empty_like(x)
+    lib().spcref_exp_array(_p(x), _p(y), x.size)
+    return y
 
 
 def exp_max_ulp(lo_bits: int, hi_bits: int):

@@ -66,6 +66,11 @@ float spcref_exp(float x) {
   return p * two_n;
 }
 
+/* O3 elementwise over an array (the exhaustive GPU bit-identity sweep). */
+void spcref_exp_array(const float* x, float* y, long long n) {
+  for (long long i = 0; i < n; ++i) y[i] = spcref_exp(x[i]);
+}
+
 double spcref_exp_max_ulp(uint32_t lo_bits, uint32_t hi_bits, uint64_t* n_subnormal) {
   double worst = 0.0;
   uint64_t sub = 0;

@@ -20,6 +20,7 @@ extern "C" {
 
 /* O3: the contract's exponential for x <= 0. */
 float spcref_exp(float x);
+void spcref_exp_array(const float* x, float* y, long long n);
 
 /* Max |spcref_exp(x) - exp(x)| in ulps of the float result, over every float
  * x whose bit pattern lies in [lo_bits, hi_bits] (negative floats: sign bit

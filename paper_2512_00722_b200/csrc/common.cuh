@@ -171,10 +171,16 @@ __device__ __forceinline__ unsigned long long f2_splat(float a) { return f2_pack
 // per element bit-identical to spc_exp_dev).
 __device__ __forceinline__ float2 spc_exp2_dev(float x0, float x1) {
   const unsigned long long x = f2_pack(x0, x1);
-  const unsigned long long t = f2_mul(x, f2_splat(__uint_as_float(0x3FB8AA3Bu)));
-  const unsigned long long big = f2_add(t, f2_splat(12582912.0f));
+  // t = RN(x log2 e) and big = RN(t + 1.5 2^23) as SCALAR ops: ptxas contracts a packed
+  // mul.rn.f32x2 feeding an add.rn.f32x2 into one FFMA2 (a single rounding), which moves the
+  // rint tie points x log2 e = k + 1/2 and flipped 12 of the 1.12e9 exp inputs by one ulp
+  // (tests/test_gpu_score.py::test_exp_exhaustive_bit_identity); scalar FMUL / FADD keep
+  // both roundings of O3
+  const float b0 = __fadd_rn(__fmul_rn(x0, __uint_as_float(0x3FB8AA3Bu)), 12582912.0f);
+  const float b1 = __fadd_rn(__fmul_rn(x1, __uint_as_float(0x3FB8AA3Bu)), 12582912.0f);
+  const unsigned long long big = f2_pack(b0, b1);
   const unsigned long long n = f2_add(big, f2_splat(-12582912.0f));
-  const float2 bigf = f2_unpack(big);
+  const float2 bigf = make_float2(b0, b1);
   const float2 nf = f2_unpack(n);
   const unsigned long long nn = f2_pack(-nf.x, -nf.y);
   unsigned long long r = f2_fma(nn, f2_splat(__uint_as_float(0x3F317200u)), x);

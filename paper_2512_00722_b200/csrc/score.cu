@@ -275,6 +275,24 @@ int launch_group(const float* logits, const float* head_max, const int64_t* sumf
                            head_max, sumfix, seq_len, G, Smax, gs));
 }
 
+// Debug (tools / tests only; not in include/spc.h): the device O3 exp on an array, scalar
+// (spc_exp_dev) or packed f32x2 (spc_exp2_dev, the form NORM / GROUP / select run).
+__global__ void exp_debug_kernel(const float* __restrict__ x, float* __restrict__ y, long long n,
+                                 int packed) {
+  for (long long i = 2 * ((long long)blockIdx.x * blockDim.x + threadIdx.x); i < n;
+       i += 2ll * gridDim.x * blockDim.x) {
+    const float a = x[i], b = i + 1 < n ? x[i + 1] : 0.f;
+    if (packed) {
+      const float2 e = spc_exp2_dev(a, b);
+      y[i] = e.x;
+      if (i + 1 < n) y[i + 1] = e.y;
+    } else {
+      y[i] = spc_exp_dev(a);
+      if (i + 1 < n) y[i + 1] = spc_exp_dev(b);
+    }
+  }
+}
+
 struct ScoreWs {
   float* tile_max;     // [B][Hq][tiles of LG_TR rows] LOGITS: per-tile head maxima
   unsigned* lg_ctr;    // LOGITS: tile-claim counter
@@ -303,6 +321,13 @@ ScoreWs score_ws_layout(void* ws, int B, int Hq, int Smax) {
 }  // namespace spc
 
 using namespace spc;
+
+extern "C" int spc_debug_exp(const float* x, float* y, long long n, int packed, spc_stream_t stream) {
+  if (!x || !y || n < 0) return SPC_E_NULL;
+  if (n == 0) return SPC_OK;
+  exp_debug_kernel<<<4 * num_sms(), 256, 0, as_stream(stream)>>>(x, y, n, packed);
+  return launched();
+}
 
 extern "C" size_t spc_score_workspace(int B, int Hq, int Smax) {
   if (B <= 0 || Hq <= 0 || Smax <= 0) return 0;

@@ -178,3 +178,34 @@ def test_batch_level_score_and_topk(oracle, Hq, G, Smax, seq_list):
     for gg in range(G):
         assert np.array_equal(idx[:, gg].cpu().numpy(), oidx[:, 0])
         assert np.array_equal(cnt[:, gg].cpu().numpy(), ocnt[:, 0])
+
+
+def test_exp_exhaustive_bit_identity(oracle):
+    """O3 exhaustively: every float32 in [-87.5, -0] (1,118,765,057 values) through the device
+    exp -- scalar spc_exp_dev and the packed f32x2 form the NORM / GROUP / select kernels run
+    -- is bit-identical to the oracle's spcref_exp."""
+    import ctypes
+    L = spc.lib()
+    L.spc_debug_exp.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_longlong, ctypes.c_int,
+                                ctypes.c_void_p]
+    dev = torch.device("cuda")
+    lo = 0x80000000
+    hi = int(np.frombuffer(np.float32(-87.5).tobytes(), np.uint32)[0])
+    chunk = 1 << 24
+    x_d = torch.empty(chunk, dtype=torch.float32, device=dev)
+    y1 = torch.empty(chunk, dtype=torch.float32, device=dev)
+    y2 = torch.empty(chunk, dtype=torch.float32, device=dev)
+    total = 0
+    for start in range(lo, hi + 1, chunk):
+        n = min(chunk, hi + 1 - start)
+        xb = np.arange(start, start + n, dtype=np.uint64).astype(np.uint32)
+        x = xb.view(np.float32)
+        x_d[:n].copy_(torch.from_numpy(x))
+        for packed, y in ((0, y1), (1, y2)):
+            assert L.spc_debug_exp(x_d.data_ptr(), y.data_ptr(), n, packed, None) == 0
+        want = oracle.exp_array(x).view(np.uint32)
+        torch.cuda.synchronize()
+        assert np.array_equal(y1[:n].cpu().numpy().view(np.uint32), want), hex(start)
+        assert np.array_equal(y2[:n].cpu().numpy().view(np.uint32), want), hex(start)
+        total += n
+    assert total == hi - lo + 1 == 1118765057

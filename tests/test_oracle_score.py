@@ -120,14 +120,18 @@ def test_weights_match_fp64_softmax(oracle):
 
 
 def test_group_max_paper_example(oracle):
-    """P:328 / S:113: weight rows [0.2,0.8] and [0.9,0.1] in one group -> [0.9, 0.8]."""
+    """P:328 / S:113: weight rows [0.2,0.7] and [0.9,0.1] of one group -> [0.9, 0.7].  Each row
+    is completed by a padding position (0.1, 0.0) so that it is a head's softmax (Eq.1); the
+    logits are log(w) (-100 for the zero weight: spc_exp returns exactly 0 below -87)."""
     case = GOLD["group_max"][0]
-    w = np.array(case["weights"], np.float64)
-    lg = np.log(w).astype(np.float32)[None]  # logits whose softmax is w (rows sum to 1)
+    w = np.concatenate([np.array(case["weights"], np.float64),
+                        np.array(case["pad"], np.float64)[:, None]], axis=1)
+    assert np.allclose(w.sum(axis=1), 1.0)
+    lg = np.where(w > 0, np.log(np.maximum(w, 1e-300)), -100.0).astype(np.float32)[None]
     hm = lg.max(axis=-1)
-    F = oracle.norm(lg, hm, [2])
-    gs = oracle.group(lg, hm, F, [2], 1)
-    assert np.allclose(gs[0, 0], case["expect"], atol=1e-6)
+    F = oracle.norm(lg, hm, [3])
+    gs = oracle.group(lg, hm, F, [3], 1)  # G = 1: the two heads form one group (alpha = 2)
+    assert np.allclose(gs[0, 0, :2], case["expect"], atol=1e-6)
 
 
 def test_group_alpha1_identity_and_mqa(oracle):
