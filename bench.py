@@ -37,12 +37,17 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default=None,
-                    help="A/B (single GPU, replicas for N>1), C (B=16, growing 128K context), "
-                         "D (KV in pinned host memory, B=4), E (context-sharded) or R (the "
-                         "retrieval head's front-end, NEXT-1) or M (MLA sparse attention, NEXT-3); default B at "
-                         "N=1, E at N>1")
+                    help="A/B (single GPU; one replica per GPU for N>1, with config E "
+                         "context-sharded over the N GPUs attached), C (B=16, growing 128K "
+                         "context), D (KV in pinned host memory, B=4), E (context-sharded "
+                         "alone) or R (the retrieval head's front-end, NEXT-1) or M (MLA sparse "
+                         "attention, NEXT-3); default B")
     ap.add_argument("--batch", type=int, default=1, help="config R: requests per step (<= 16)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-sharded", action="store_true",
+                    help="N > 1: skip the attached config-E context-sharded measurement")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="launch plumbing only (CPU, gloo): spawn / rendezvous / max over ranks")
     ap.add_argument("--kv-layout", default="token", choices=["token", "layer"],
                     help="config D host KV layout: token-major records (one contiguous record "
                          "per token) or layer-major [L][B][G][rows][D]")
@@ -52,6 +57,59 @@ def parse():
 def dist_env():
     return (int(os.environ.get("RANK", "0")), int(os.environ.get("LOCAL_RANK", "0")),
             int(os.environ.get("WORLD_SIZE", "1")))
+
+
+def init_pg(dev=None):
+    """The process group of a multi-rank run (NCCL on GPUs, gloo for --dry-run), created
+    once per process; None at world size 1."""
+    if dist_env()[2] == 1:
+        return None
+    import torch.distributed as dist
+    if not dist.is_initialized():
+        if dev is not None:
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
+    return dist
+
+
+def free_port():
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def spawn_ranks(n):
+    """`bench.py --gpus N` outside torchrun: re-run this command as N ranks on this node
+    (torch.distributed.run, rendezvous on 127.0.0.1) and exit with its status."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", f"--master-port={free_port()}",
+           os.path.abspath(__file__), *sys.argv[1:]]
+    sys.exit(subprocess.call(cmd))
+
+
+def dry_run(args):
+    """--dry-run: the launch plumbing alone, on CPU (no GPU, no kernels): every rank joins the
+    gloo group, takes the max of a per-rank time over ranks, and rank 0 prints the JSON line
+    shape with n_gpus = world size (tests/test_bench_launch.py)."""
+    import torch
+    rank, _, world = dist_env()
+    pg = init_pg()
+    t = torch.tensor([float(rank + 1)], dtype=torch.float64)
+    if pg:
+        pg.barrier()
+        pg.all_reduce(t, op=pg.ReduceOp.MAX)
+    if rank == 0:
+        print(json.dumps({"metric": METRIC, "value": None, "unit": "tokens/s", "n_gpus": world,
+                          "steps": args.steps, "warmup": args.warmup, "dry_run": True,
+                          "max_over_ranks": float(t.item()),
+                          "config": {"workload": "dry run (launch plumbing only)"}}), flush=True)
+    if pg:
+        pg.barrier()
+        pg.destroy_process_group()
 
 
 def warm_graphs(st, graphs):
@@ -215,7 +273,7 @@ def bench_reference(args):
 
 
 # ------------------------------------------------------------------ GPU
-def bench_ours(args):
+def bench_ours(args, attach=None):
     import torch
 
     from paper_2512_00722_b200 import build as spc_build
@@ -228,11 +286,7 @@ def bench_ours(args):
             spc_build.build()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    pg = None
-    if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
-        pg = dist
+    pg = init_pg(dev)
     key = args.config
     c = synth.CONFIGS[key]
     B, G, Hq, D, S, L, k = c["B"], c["G"], c["Hq"], c["D"], c["S"], c["L"], c["k"]
@@ -456,14 +510,16 @@ def bench_ours(args):
             "gpu_launches": launches_per_step * args.steps,
             "clocks": clocks,
         }
+        if attach:
+            line["config"].update(attach)
         print(json.dumps(line), flush=True)
     if pg:
         pg.barrier()
-        pg.destroy_process_group()
 
 
-def bench_sharded(args):
-    """Config E: one 1M-token context sharded over the N ranks (t mod N), NCCL collectives."""
+def bench_sharded(args, embedded=False):
+    """Config E: one 1M-token context sharded over the N ranks (t mod N), NCCL collectives.
+    embedded: return the measurement (rank 0) instead of printing the JSON line."""
     import torch
 
     from paper_2512_00722_b200 import build as spc_build
@@ -476,10 +532,7 @@ def bench_sharded(args):
             spc_build.build()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    tdist = None
-    if world > 1:
-        import torch.distributed as tdist
-        tdist.init_process_group("nccl", device_id=dev)
+    tdist = init_pg(dev)
     key = "E"
     c = synth.CONFIGS[key]
     B, G, Hq, D, S, L, k = c["B"], c["G"], c["Hq"], c["D"], c["S"], c["L"], c["k"]
@@ -583,8 +636,9 @@ def bench_sharded(args):
         pass
     peak = float(peaks.get("hbm_gbs", 6650.0))
     achieved = rank_bytes / (ms_per_step * 1e-3) / 1e9
+    line = None
     if rank == 0:
-        print(json.dumps({
+        line = {
             "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
@@ -601,10 +655,14 @@ def bench_sharded(args):
             "e2e": e2e,
             "gpu_launches": launches_per_step * args.steps,
             "clocks": clocks,
-        }), flush=True)
+        }
+        if not embedded:
+            print(json.dumps(line), flush=True)
     if tdist is not None:
         tdist.barrier()
-        tdist.destroy_process_group()
+    del st, kr, kc, vc
+    torch.cuda.empty_cache()
+    return line
 
 
 def bench_grow(args):
@@ -1060,23 +1118,40 @@ def main():
     if args.warmup < 3:
         args.warmup = 3
     world = dist_env()[2]
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        spawn_ranks(args.gpus)  # does not return
+    if args.dry_run:
+        dry_run(args)
+        return
+    if "WORLD_SIZE" in os.environ and world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     if args.config is None:
-        args.config = "B" if world == 1 else "E"
+        args.config = "B"
     if args.impl == "reference":
         bench_reference(args)
+    elif args.config == "B" and world > 1:
+        # the same workload at every N (config B, one request per GPU: weak scaling, no
+        # data-path collective), plus config E's 1M-token context sharded over the N ranks
+        # (strong scaling, the north star's multi-GPU target) attached to the same line
+        sharded = None if args.no_sharded else bench_sharded(args, embedded=True)
+        bench_ours(args, attach={"context_sharded_E": sharded})
+    elif args.config == "E":
+        bench_sharded(args)
+    elif args.config == "C":
+        bench_grow(args)
+    elif args.config == "D":
+        bench_offload(args)
+    elif args.config == "R":
+        bench_frontend(args)
+    elif args.config == "M":
+        bench_mla(args)
     else:
-        if args.config == "E":
-            bench_sharded(args)
-        elif args.config == "C":
-            bench_grow(args)
-        elif args.config == "D":
-            bench_offload(args)
-        elif args.config == "R":
-            bench_frontend(args)
-        elif args.config == "M":
-            bench_mla(args)
-        else:
-            bench_ours(args)
+        bench_ours(args)
+    if world > 1:
+        import torch.distributed as dist
+        if dist.is_initialized():
+            dist.barrier()
+            dist.destroy_process_group()
 
 
 if __name__ == "__main__":

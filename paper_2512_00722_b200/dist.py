@@ -6,12 +6,12 @@ step (BASELINE config E):
 
   1. LOGITS on the local keys            -> all-reduce MAX of head_max   (exact)
   2. NORM with the global max            -> all-reduce SUM of int64 sums (exact)
-  3. GROUP; local top-k with global ids  -> all-gather of (value, pos, count)
+  3. GROUP; local top-k with global ids  -> ONE all-gather of packed (value, pos, count)
   4. global threshold = k-th composite of the union (spc_topk_merge); each rank
      keeps its entries >= threshold (spc_topk_filter): the union equals the
      single-device selection bit for bit (O13)
   5. sparse attention over the local rows for all L layers
-                                         -> all-gather of (o, lse); LSE merge (O12)
+                                         -> ONE all-gather of packed (o, lse); LSE merge (O12)
 
 Every compute step is a libspc call (``SpcOps``); collectives are
 torch.distributed calls on the current stream (NCCL over NVLink on a GPU box).
@@ -96,11 +96,17 @@ class SpcOps:
         return t
 
     def _seq(self, st):
-        key = ("seq_loc", tuple(st.S))
-        t = st.bufs.get(key)
-        if t is None:  # filled once (outside any graph capture)
-            t = st.bufs[key] = torch.tensor(st.local_seq(), dtype=torch.int32,
-                                            device=st.kr.device)
+        """The local seq_len buffer: one per state, refreshed in place when S changes (a
+        decode loop that advances S reuses it; refresh outside graph capture)."""
+        t = st.bufs.get("seq_loc")
+        key = tuple(st.S)
+        if t is None:
+            t = st.bufs["seq_loc"] = torch.tensor(st.local_seq(), dtype=torch.int32,
+                                                  device=st.kr.device)
+            st.bufs["seq_key"] = key
+        elif st.bufs.get("seq_key") != key:
+            t.copy_(torch.tensor(st.local_seq(), dtype=torch.int32))
+            st.bufs["seq_key"] = key
         return t
 
     def _score(self, st, phases, head_max=None, sumfix=None):
@@ -174,12 +180,18 @@ class SpcOps:
         if ws is None:
             ws = st.bufs["ws_attn"] = spc.alloc_workspace(spc.attn_workspace(L, B, Hq, D, st.k),
                                                          dev)
-        if "ktab" not in st.bufs:
-            st.bufs["ktab"] = spc.ptr_table(st.k_layers, dev)
-            st.bufs["vtab"] = spc.ptr_table(st.v_layers, dev)
         rows = st.k_layers[0].shape[2]
-        spc.sparse_decode_attn(st.q_llm, st.bufs["ktab"], st.bufs["vtab"], spc.KV_INDEXED, pos,
-                               cnt, rows, st.k, st.scale, out, lse, ws, st.G)
+        if st.k_layers[0].dtype == torch.bfloat16:  # TMA row gathers over the layer descriptors
+            if "kvdesc" not in st.bufs:
+                st.bufs["kvdesc"] = spc.KvDesc(st.k_layers, st.v_layers)
+            spc.sparse_decode_attn_kv(st.bufs["kvdesc"], st.q_llm, spc.KV_INDEXED, pos, cnt, st.k,
+                                      st.scale, out, lse, ws)
+        else:
+            if "ktab" not in st.bufs:
+                st.bufs["ktab"] = spc.ptr_table(st.k_layers, dev)
+                st.bufs["vtab"] = spc.ptr_table(st.v_layers, dev)
+            spc.sparse_decode_attn(st.q_llm, st.bufs["ktab"], st.bufs["vtab"], spc.KV_INDEXED, pos,
+                                   cnt, rows, st.k, st.scale, out, lse, ws, st.G)
         return out, lse
 
     def attn_merge(self, st, o_parts, lse_parts):
@@ -221,9 +233,30 @@ def phase_merge(ops, st, o_all, lse_all):
     return ops.attn_merge(st, o_all, lse_all)
 
 
+def _gather_packed(parts, P, group):
+    """ONE all-gather of several tensors of one rank: their bytes are packed into a flat
+    buffer, gathered into [P][nbytes], and returned as dense per-part tensors [P][...]."""
+    import torch.distributed as dist
+    words = [t.contiguous().view(torch.uint8).reshape(-1) for t in parts]
+    send = torch.cat(words)
+    recv = torch.empty(P * send.numel(), dtype=torch.uint8, device=send.device)
+    dist.all_gather_into_tensor(recv, send, group=group)  # flat [P * n]: NCCL and gloo
+    recv = recv.view(P, send.numel())
+    out, off = [], 0
+    for t, w in zip(parts, words):
+        # one small contiguous copy per part: the kernels take dense [P][...] operands
+        out.append(recv[:, off:off + w.numel()].view(t.dtype).reshape((P,) + tuple(t.shape))
+                   .contiguous())
+        off += w.numel()
+    return out
+
+
 def run_distributed(ops, st: ShardState, group=None):
     """One sharded step on this rank; collectives through torch.distributed (NCCL for
-    CUDA tensors, gloo for CPU tensors).  Returns (local pos, count, merged o, merged lse)."""
+    CUDA tensors, gloo for CPU tensors).  FOUR collectives per step: the
+    all-reduce MAX of head_max, the all-reduce SUM of the int64 normalisers, ONE all-gather
+    of the packed (value, position, count) candidates and ONE all-gather of the packed
+    (o, lse) partials.  Returns (local pos, count, merged o, merged lse)."""
     import torch.distributed as dist
     P = st.P
     hm = phase_logits(ops, st)
@@ -231,19 +264,10 @@ def run_distributed(ops, st: ShardState, group=None):
     F = phase_norm(ops, st, hm)
     dist.all_reduce(F, op=dist.ReduceOp.SUM, group=group)
     val, pos, cnt = phase_candidates(ops, st, hm, F)
-    gv = [torch.empty_like(val) for _ in range(P)]
-    gp = [torch.empty_like(pos) for _ in range(P)]
-    gc = [torch.empty_like(cnt) for _ in range(P)]
-    dist.all_gather(gv, val.contiguous(), group=group)
-    dist.all_gather(gp, pos.contiguous(), group=group)
-    dist.all_gather(gc, cnt.contiguous(), group=group)
-    lpos, lcnt, o, lse = phase_select_attend(ops, st, torch.stack(gv), torch.stack(gp),
-                                             torch.stack(gc))
-    go = [torch.empty_like(o) for _ in range(P)]
-    gl = [torch.empty_like(lse) for _ in range(P)]
-    dist.all_gather(go, o.contiguous(), group=group)
-    dist.all_gather(gl, lse.contiguous(), group=group)
-    out, lse_m = phase_merge(ops, st, torch.stack(go), torch.stack(gl))
+    gv, gp, gc = _gather_packed([val, pos, cnt], P, group)
+    lpos, lcnt, o, lse = phase_select_attend(ops, st, gv, gp, gc)
+    go, gl = _gather_packed([o, lse], P, group)
+    out, lse_m = phase_merge(ops, st, go.contiguous(), gl.contiguous())
     return lpos, lcnt, out, lse_m
 
 

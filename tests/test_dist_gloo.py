@@ -88,3 +88,45 @@ def test_shard_plan():
             last = S - 1
             r = sdist.owner(last, P)
             assert (last - r) // P == sdist.local_len(S, P, r) - 1  # last local position
+
+
+def count_worker(rank, P, port, S, k, out_path):
+    """One sharded step with every torch.distributed collective counted."""
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from oracle_ops import OracleOps
+    from paper_2512_00722_b200 import dist as sdist
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                            world_size=P)
+    calls = []
+    names = ("all_reduce", "all_gather", "all_gather_into_tensor", "broadcast", "reduce_scatter",
+             "all_to_all", "all_gather_object", "reduce", "gather", "scatter")
+    saved = {n: getattr(dist, n) for n in names if hasattr(dist, n)}
+
+    def wrap(n, f):
+        def g(*a, **kw):
+            calls.append(n)
+            return f(*a, **kw)
+        return g
+    for n, f in saved.items():
+        setattr(dist, n, wrap(n, f))
+    kr, kl, vl, qr, ql = global_inputs(S, seed=4)
+    st = sdist.make_shard(rank, P, kr, kl, vl, qr, ql, [S], k)
+    sdist.run_distributed(OracleOps(), st)
+    for n, f in saved.items():
+        setattr(dist, n, f)
+    if rank == 0:
+        with open(out_path, "w") as fh:
+            fh.write(",".join(calls))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_sharded_step_uses_four_collectives(tmp_path):
+    """the sharded step crosses the ranks four times -- all-reduce MAX,
+    all-reduce SUM, one packed candidate all-gather, one packed (o, lse) all-gather."""
+    out_path = str(tmp_path / "calls.txt")
+    mp.start_processes(count_worker, args=(2, free_port(), 500, 64, out_path), nprocs=2, join=True,
+                       start_method="spawn")
+    calls = open(out_path).read().split(",")
+    assert calls == ["all_reduce", "all_reduce", "all_gather_into_tensor", "all_gather_into_tensor"]
