@@ -21,10 +21,15 @@
  *  - bf16 tensors are passed as raw 16-bit words (IEEE bfloat16 bit pattern).
  *  - Errors: host-checkable argument errors are reported as a spc_status
  *    BEFORE anything is enqueued (nothing aborts, nothing throws across the
- *    ABI).  Data-dependent contract violations (unsorted index lists, index >=
- *    seq_len, slot map inconsistent with the previous set) are undefined
- *    behaviour unless stated.  SPC_E_CUDA means a CUDA launch error; its text
- *    is available from spc_last_cuda_error().
+ *    ABI).  Data-dependent contract violations (index out of range -> SPC_E_RANGE
+ *    (S:178), unsorted / duplicated index list or slot map inconsistent with the
+ *    previous set -> SPC_E_STATE, more new rows than free slots ->
+ *    SPC_E_BUDGET, NaN keys or scores -> SPC_E_RANGE (reading R20)) are
+ *    checked on the device only by a library built with SPC_DEBUG (libspc_debug.so,
+ *    spc_debug_build() == 1): the first violation is recorded with its source line
+ *    and returned by spc_check_device_errors(); in release builds they are
+ *    undefined behaviour.  SPC_E_CUDA means a CUDA error; its text (and a device
+ *    violation's location) is available from spc_last_cuda_error().
  *  - Index lists are int32, ascending, padded with -1 after `count` entries.
  */
 #ifndef SPC_H_
@@ -59,6 +64,12 @@ enum { SPC_MAX_SEQ = 1 << 23 }; /* O4's fixed-point sum is exact for S < 2^23   
 const char* spc_status_string(int status);
 const char* spc_last_cuda_error(void);
 int spc_version(void);
+/* 1 when this library was built with SPC_DEBUG (device-side contract checks), else 0. */
+int spc_debug_build(void);
+/* Synchronises `stream`; returns SPC_E_CUDA on a CUDA error, else the first device-side
+ * contract violation recorded since the last call (SPC_DEBUG builds; cleared by the call;
+ * location via spc_last_cuda_error()), else SPC_OK.  Not capturable in a CUDA graph. */
+int spc_check_device_errors(spc_stream_t stream);
 /* Number of kernels this library has launched since it was loaded (all
  * threads).  Used by bench.py to report how many of its own kernels ran. */
 uint64_t spc_launch_count(void);

@@ -10,6 +10,7 @@ from concurrent.futures import ThreadPoolExecutor
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libspc.so")
+DEBUG_LIB = os.path.join(HERE, "libspc_debug.so")  # -DSPC_DEBUG: device-side contract checks
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC,-O2", "-Xptxas", "-O3", "--expt-relaxed-constexpr"]
@@ -24,10 +25,10 @@ def _deps():
         os.path.join(HERE, "..", "include", "spc.h")]
 
 
-def up_to_date() -> bool:
-    if not os.path.exists(LIB):
+def up_to_date(lib: str = LIB) -> bool:
+    if not os.path.exists(lib):
         return False
-    t = os.path.getmtime(LIB)
+    t = os.path.getmtime(lib)
     return all(os.path.getmtime(p) <= t for p in _deps())
 
 
@@ -36,6 +37,8 @@ def build(force: bool = False, verbose: bool = False, out: str = LIB, defines=()
     debug builds written elsewhere than the product library."""
     if out == LIB and not defines and not force and up_to_date():
         return LIB
+    if out == DEBUG_LIB and not force and up_to_date(DEBUG_LIB):
+        return DEBUG_LIB
     objdir = os.path.join(HERE, "build" if not defines else "build_" + "_".join(defines).lower())
     os.makedirs(objdir, exist_ok=True)
 
@@ -61,5 +64,11 @@ def build(force: bool = False, verbose: bool = False, out: str = LIB, defines=()
     return out
 
 
+def build_debug(force: bool = False) -> str:
+    """libspc_debug.so: the same sources with SPC_DEBUG (device contract checks)."""
+    return build(force=force, out=DEBUG_LIB, defines=["SPC_DEBUG"])
+
+
 if __name__ == "__main__":
     print(build(force="--force" in sys.argv, verbose=True))
+    print(build_debug(force="--force" in sys.argv))

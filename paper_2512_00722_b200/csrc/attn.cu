@@ -257,12 +257,7 @@ extern "C" int spc_sparse_decode_attn(int dtype, const void* q, const void* cons
   if (D == DD && alpha == AA) {                                                                 \
     if (dtype == SPC_BF16) {                                                                    \
       const int smem = PSmem<DD, AA>::BYTES;                                                    \
-      static bool attr = false;                                                                 \
-      if (!attr) {                                                                              \
-        cudaFuncSetAttribute(attn_bf16_kernel<DD, AA>,                                          \
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, smem);                \
-        attr = true;                                                                            \
-      }                                                                                         \
+      SPC_TRY(smem_attr((const void*)attn_bf16_kernel<DD, AA>, smem));                          \
       (void)launch_k(attn_bf16_kernel<DD, AA>, dim3(ncta), dim3(AT2_THREADS), smem, st,      \
           (const uint16_t*)q, k_layers, v_layers, kv_mode, idx, count, layer_begin, B, G, rows, \
           k, kpad, scale, (int)(rpc / CH), n_groups, w.segstride, w.part_o, w.part_ml, w.cnt,   \
@@ -312,29 +307,6 @@ extern "C" int spc_kv_desc_init(void* desc, const void* const* k_layers, const v
   return rc;
 }
 
-namespace spc {
-namespace {
-// per-device, per-instantiation "max dynamic smem" attribute (thread-safe)
-template <int DD, int AA>
-int tma_attr() {
-  static std::atomic<uint64_t> done{0};  // bit per device ordinal < 64
-  int dev = 0;
-  cudaError_t e = cudaGetDevice(&dev);
-  if (e != cudaSuccess) return launched(e);
-  const uint64_t bit = dev < 64 ? (1ull << dev) : 0ull;
-  if (bit && (done.load(std::memory_order_acquire) & bit)) return SPC_OK;
-  e = cudaFuncSetAttribute(attn_tma_kernel<DD, AA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           TmSmem<DD>::BYTES);
-  if (e != cudaSuccess) {
-    set_cuda_error(e);
-    return SPC_E_CUDA;
-  }
-  done.fetch_or(bit, std::memory_order_acq_rel);
-  return SPC_OK;
-}
-}  // namespace
-}  // namespace spc
-
 extern "C" int spc_sparse_decode_attn_kv(const void* kv_desc, const void* q, int kv_mode,
                                          const int32_t* idx, const int32_t* count, int L,
                                          int layer_begin, int layer_end, int B, int Hq, int G, int D,
@@ -366,7 +338,7 @@ extern "C" int spc_sparse_decode_attn_kv(const void* kv_desc, const void* q, int
   const CUtensorMap* maps = (const CUtensorMap*)kv_desc;
 #define ATK(DD, AA)                                                                               \
   if (D == DD && alpha == AA) {                                                                   \
-    SPC_TRY((tma_attr<DD, AA>()));                                                                \
+    SPC_TRY(smem_attr((const void*)attn_tma_kernel<DD, AA>, TmSmem<DD>::BYTES));                  \
     SPC_TRY(launched(launch_k(attn_tma_kernel<DD, AA>, dim3(ncta), dim3(TM_THREADS),             \
                               TmSmem<DD>::BYTES, st, (const uint16_t*)q, maps, L, kv_mode, idx,   \
                               count, layer_begin, B, G, rows, k, kpad, scale,                     \

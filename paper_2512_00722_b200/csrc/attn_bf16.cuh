@@ -323,6 +323,14 @@ __global__ void __launch_bounds__(AT2_THREADS, AT2_CTAS_PER_SM) attn_bf16_kernel
 #pragma unroll
       for (int t = 0; t < RPL; ++t) tok[t] = r0 + warp * WR + lg * RPL + t;
     }
+#ifdef SPC_DEBUG  // selected rows must be cache rows; a bad one is not read
+#pragma unroll
+    for (int t = 0; t < RPL; ++t)
+      if (t < nrows) {
+        SPC_DCHECK(tok[t] >= 0 && tok[t] < rows, SPC_E_RANGE);
+        if (tok[t] < 0 || tok[t] >= rows) tok[t] = 0;
+      }
+#endif
     const uint32_t dst = wsb + (uint32_t)s * SM::STAGE + (uint32_t)((lg * RPL * RS + col * 8) * 2);
 #pragma unroll
     for (int t = 0; t < RPL; ++t) {

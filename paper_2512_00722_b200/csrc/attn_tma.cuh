@@ -148,8 +148,16 @@ __global__ void __launch_bounds__(TM_THREADS, TM_CTAS) attn_tma_kernel(
         if (j >= n_chunks) break;
         int4 r;
         {
-          const Meta& m = pre[u];
+          Meta& m = pre[u];
           const int nv = min(m.nv, kbud);
+#ifdef SPC_DEBUG  // selected rows must be cache rows; a bad one is zero-filled
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (m.r0 + u < nv) {
+              SPC_DCHECK(m.t[u] >= 0 && m.t[u] < rows, SPC_E_RANGE);
+              if (m.t[u] < 0 || m.t[u] >= rows) m.t[u] = -1 - m.base;
+            }
+#endif
           r.x = m.r0 + 0 < nv ? m.base + m.t[0] : -1;
           r.y = m.r0 + 1 < nv ? m.base + m.t[1] : -1;
           r.z = m.r0 + 2 < nv ? m.base + m.t[2] : -1;

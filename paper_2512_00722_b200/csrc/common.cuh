@@ -83,6 +83,13 @@ inline cudaError_t launch_kc(void (*kern)(KArgs...), dim3 grid, dim3 block, size
   return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
 }
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+// SPC_DEBUG builds: each translation unit's device error word is read (and cleared) through
+// a reader registered here; spc_check_device_errors() polls them all (runtime.cu).
+int register_err_reader(unsigned (*read_and_clear)(), const char* file);
+// The max-dynamic-shared-memory attribute of a kernel (and optionally the non-portable
+// cluster size), set once per (kernel, device, bytes): thread-safe, failures are returned
+// (never remembered as set).
+int smem_attr(const void* kern, int bytes, bool nonportable_cluster = false);
 int num_sms();
 // Encode the row-gather TMA descriptor of a bf16 [n_rows][D] tensor (driver entry point
 // fetched through cudart): 64-element x 1-row boxes, 128-byte swizzle.
@@ -90,6 +97,33 @@ int make_tmap_rows_bf16(CUtensorMap* map, const void* base, uint64_t n_rows, uin
 // ... and the tile-streaming one: boxes of 64 elements x box_rows rows, 128-byte swizzle.
 int make_tmap_tile_bf16(CUtensorMap* map, const void* base, uint64_t n_rows, uint32_t D,
                         uint32_t box_rows);
+
+// ------------------------------------------- SPC_DEBUG device-side contract checks
+// A violated data-dependent contract (include/spc.h: out-of-range index, unsorted set,
+// slot map != previous set, NaN input) records its first spc_status and source line in this
+// translation unit's error word; spc_check_device_errors() returns and clears it.  Release
+// builds compile the checks out.
+#ifdef SPC_DEBUG
+static __device__ unsigned g_spc_dev_err = 0u;  // status | line << 8; one per translation unit
+__device__ __forceinline__ void spc_dev_fail(int code, int line) {
+  atomicCAS(&g_spc_dev_err, 0u, (unsigned)code | ((unsigned)line << 8));
+}
+#define SPC_DCHECK(cond, code)                                  \
+  do {                                                          \
+    if (!(cond)) ::spc::spc_dev_fail((code), __LINE__);         \
+  } while (0)
+static unsigned spc_read_and_clear_err() {
+  unsigned v = 0u, z = 0u;
+  if (cudaMemcpyFromSymbol(&v, g_spc_dev_err, sizeof v) != cudaSuccess) return 0u;
+  cudaMemcpyToSymbol(g_spc_dev_err, &z, sizeof z);
+  return v;
+}
+static const int spc_err_reader_registered = register_err_reader(spc_read_and_clear_err, __BASE_FILE__);
+#else
+#define SPC_DCHECK(cond, code) \
+  do {                         \
+  } while (0)
+#endif
 
 // --------------------------------------------------------------- device side
 __device__ __forceinline__ void spc_pdl_entry() {

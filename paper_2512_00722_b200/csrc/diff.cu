@@ -62,6 +62,16 @@ __global__ void __launch_bounds__(DF_THREADS) diff_kernel(
   for (int i = tid; i < np; i += DF_THREADS) sprev[i] = pv[i];
   for (int i = tid; i < nc; i += DF_THREADS) scur[i] = cv[i];
   __syncthreads();
+#ifdef SPC_DEBUG  // both lists ascending, no duplicates, ids >= 0
+  for (int i = tid; i < np; i += DF_THREADS) {
+    SPC_DCHECK(sprev[i] >= 0, SPC_E_RANGE);
+    SPC_DCHECK(i == 0 || sprev[i - 1] < sprev[i], SPC_E_STATE);
+  }
+  for (int i = tid; i < nc; i += DF_THREADS) {
+    SPC_DCHECK(scur[i] >= 0, SPC_E_RANGE);
+    SPC_DCHECK(i == 0 || scur[i - 1] < scur[i], SPC_E_STATE);
+  }
+#endif
   if (use_bm) {
     for (int i = tid; i < np; i += DF_THREADS) atomicOr(&bm_prev[sprev[i] >> 5], 1u << (sprev[i] & 31));
     for (int i = tid; i < nc; i += DF_THREADS) atomicOr(&bm_cur[scur[i] >> 5], 1u << (scur[i] & 31));
@@ -120,6 +130,21 @@ __global__ void __launch_bounds__(DF_THREADS) diff_kernel(
   // slot reuse: freed slots (empty or token not in cur) in ascending slot order
   if (slot_tok) {
     int32_t* st = slot_tok + (size_t)row * k;
+#ifdef SPC_DEBUG  // the non-empty slots hold exactly the previous set
+    {
+      int c = 0;
+      for (int s2 = tid; s2 < k; s2 += DF_THREADS) {
+        const int t2 = st[s2];
+        if (t2 >= 0) {
+          ++c;
+          SPC_DCHECK(contains(sprev, np, t2), SPC_E_STATE);
+        }
+      }
+      c = block_excl_scan(c, wsum, &total);
+      (void)c;
+      SPC_DCHECK(total == np, SPC_E_STATE);
+    }
+#endif
     int tok[DF_PER];
     cnt = 0;
 #pragma unroll
@@ -130,6 +155,7 @@ __global__ void __launch_bounds__(DF_THREADS) diff_kernel(
       cnt += flag[i];
     }
     pos = block_excl_scan(cnt, wsum, &total);
+    SPC_DCHECK(total >= nl, SPC_E_BUDGET);  // #new <= #freed for consistent inputs (O8)
     int32_t* ls = load_slot + (size_t)row * k;
 #pragma unroll
     for (int i = 0; i < DF_PER; ++i) {
@@ -170,6 +196,10 @@ __global__ void __launch_bounds__(256) gather_kernel(
   for (int i = blockIdx.x * rows_per_block + sub; i < n; i += gridDim.x * rows_per_block) {
     const int t = load_tok[(size_t)bg * kbud + i];
     const int s = load_slot[(size_t)bg * kbud + i];
+#ifdef SPC_DEBUG  // an index out of range is an error (skipped, not read)
+    SPC_DCHECK(t >= 0 && t < Smax && s >= 0 && s < kbud, SPC_E_RANGE);
+    if (t < 0 || t >= Smax || s < 0 || s >= kbud) continue;
+#endif
     const VecT a = ks[src_base + (size_t)t * row_vecs + lane];
     const VecT b = vs[src_base + (size_t)t * row_vecs + lane];
     kd[dst_base + (size_t)s * row_vecs + lane] = a;
@@ -207,6 +237,10 @@ __global__ void __launch_bounds__(GT_WARPS * 32) gather_strided_kernel(
     if (i >= n) continue;
     const long long t = load_tok[(size_t)bg * kbud + i];
     const long long s = load_slot[(size_t)bg * kbud + i];
+#ifdef SPC_DEBUG
+    SPC_DCHECK(t >= 0 && s >= 0 && s < kbud, SPC_E_RANGE);
+    if (t < 0 || s < 0 || s >= kbud) continue;
+#endif
     const size_t soff = (size_t)(bg * bg_stride + t * row_stride) * 2 / 16 + vec;  // 16-B units
     const size_t doff = ((size_t)bg * kbud + s) * vpr + vec;
     for (int l0 = 0; l0 < nl; l0 += SPC_GT_UNR) {
@@ -242,12 +276,8 @@ extern "C" int spc_elastic_diff(const int32_t* prev_idx, const int32_t* prev_cou
   if (B <= 0 || G <= 0) return SPC_E_SHAPE;
   if (k < 1 || k > SPC_MAX_K) return SPC_E_BUDGET;
   const size_t smem = sizeof(int32_t) * 3 * (size_t)k + sizeof(uint32_t) * 2 * DF_BM_WORDS;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(diff_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)(sizeof(int32_t) * 3 * SPC_MAX_K + sizeof(uint32_t) * 2 * DF_BM_WORDS));
-    attr = true;
-  }
+  SPC_TRY(smem_attr((const void*)diff_kernel,
+                    (int)(sizeof(int32_t) * 3 * SPC_MAX_K + sizeof(uint32_t) * 2 * DF_BM_WORDS)));
   return launched(launch_k(diff_kernel, dim3(B * G), dim3(DF_THREADS), smem, as_stream(stream),
                            prev_idx, prev_count, cur_idx, cur_count, k, slot_tok, load_tok,
                            load_slot, n_load, evict_tok, n_evict));

@@ -222,6 +222,7 @@ __global__ void __launch_bounds__(32 * lg_warps<ALPHA>(), 1) logits_kernel(
           const int r = lane + 32 * i;
           const float sv = __fmul_rn((i & 1) ? acc[j][i >> 1].y : acc[j][i >> 1].x, scale);
           if (t0 + r < S) {
+            SPC_DCHECK(sv == sv, SPC_E_RANGE);  // NaN key / query (reading R20)
             o[r] = sv;
             m = fmaxf(m, sv);
           }
@@ -474,6 +475,7 @@ __global__ void __launch_bounds__(32 * (LT_NC + 1), 1) logits_tma_kernel(
         const int row = lane + 32 * r;
         const float sv = __fmul_rn((r & 1) ? acc[j][r >> 1].y : acc[j][r >> 1].x, scale);
         if (t0 + row < S && t0 + row < Smax) {
+          SPC_DCHECK(sv == sv, SPC_E_RANGE);  // NaN key / query (reading R20)
           o[row] = sv;
           m = fmaxf(m, sv);
         }

@@ -370,12 +370,7 @@ extern "C" int spc_rethead_qk(const int32_t* token, const void* emb, int V, int 
   cudaStream_t st = as_stream(stream);
 #define RH(BT)                                                                                    \
   {                                                                                               \
-    static int attr_bytes = 0;                                                                    \
-    if ((int)smem > attr_bytes) {                                                                 \
-      cudaFuncSetAttribute(rethead_kernel<BT>, cudaFuncAttributeMaxDynamicSharedMemorySize,       \
-                           (int)std::max<size_t>(smem, 48 * 1024));                               \
-      attr_bytes = (int)std::max<size_t>(smem, 48 * 1024);                                        \
-    }                                                                                             \
+    SPC_TRY(smem_attr((const void*)rethead_kernel<BT>, 200 * 1024));                              \
     return launched(launch_k(rethead_kernel<BT>, dim3(ncta), dim3(RH_WARPS * 32), smem, st,      \
                              token, (const uint16_t*)emb, H, (const uint16_t*)norm_w, eps,        \
                              (const uint16_t*)w_qk, inv_freq, mscale, pos, B, Hq, G, D, Smax,     \
@@ -391,12 +386,7 @@ extern "C" int spc_rethead_qk(const int32_t* token, const void* emb, int V, int 
       const int nct = std::max(1, std::min(num_sms(), tiles));
 #define RM(NT)                                                                                    \
   {                                                                                               \
-    static bool rm_attr = false;                                                                  \
-    if (!rm_attr) {                                                                               \
-      cudaFuncSetAttribute(rethead_mma_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,   \
-                           200 * 1024);                                                           \
-      rm_attr = true;                                                                             \
-    }                                                                                             \
+    SPC_TRY(smem_attr((const void*)rethead_mma_kernel<NT>, 200 * 1024));                          \
     return launched(launch_k(rethead_mma_kernel<NT>, dim3(nct), dim3(RM_WARPS * 32), msm, st,    \
                              token, (const uint16_t*)emb, H, (const uint16_t*)norm_w, eps,        \
                              (const uint16_t*)w_qk, inv_freq, mscale, pos, B, Hq, G, D, Smax,     \

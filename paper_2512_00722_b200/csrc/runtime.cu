@@ -8,21 +8,66 @@
 
 #include "common.cuh"
 
+#include <set>
+#include <tuple>
+#include <vector>
+
 namespace spc {
 std::atomic<uint64_t> g_launches{0};
+
+struct ErrReader {
+  unsigned (*fn)();
+  const char* file;
+};
+static std::vector<ErrReader>& err_readers() {
+  static std::vector<ErrReader> v;
+  return v;
+}
+static std::mutex g_reader_mu;
+int register_err_reader(unsigned (*read_and_clear)(), const char* file) {
+  std::lock_guard<std::mutex> lk(g_reader_mu);
+  err_readers().push_back({read_and_clear, file});
+  return 1;
+}
 static thread_local char g_err[256] = "";
 
 void set_cuda_error(cudaError_t e) {
   snprintf(g_err, sizeof(g_err), "%s: %s", cudaGetErrorName(e), cudaGetErrorString(e));
 }
 
-int num_sms() {
-  static int n = 0;
+int smem_attr(const void* kern, int bytes, bool nonportable_cluster) {
+  static std::mutex mu;
+  static std::set<std::tuple<const void*, int, int>> done;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) {
+    set_cuda_error(e);
+    return SPC_E_CUDA;
+  }
+  std::lock_guard<std::mutex> lk(mu);
+  const auto key = std::make_tuple(kern, dev, bytes);
+  if (done.count(key)) return SPC_OK;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess && nonportable_cluster)
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  if (e != cudaSuccess) {
+    set_cuda_error(e);
+    return SPC_E_CUDA;
+  }
+  done.insert(key);
+  return SPC_OK;
+}
+
+int num_sms() {  // per device (a process may drive several GPUs)
+  static std::atomic<int> cache[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  int n = cache[dev].load(std::memory_order_relaxed);
   if (!n) {
-    int dev = 0;
-    cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
     if (n <= 0) n = 148;
+    cache[dev].store(n, std::memory_order_relaxed);
   }
   return n;
 }
@@ -86,6 +131,34 @@ const char* spc_status_string(int s) {
   }
 }
 const char* spc_last_cuda_error(void) { return spc::g_err; }
+
+int spc_debug_build(void) {
+#ifdef SPC_DEBUG
+  return 1;
+#else
+  return 0;
+#endif
+}
+
+int spc_check_device_errors(spc_stream_t stream) {
+  cudaError_t e = cudaStreamSynchronize(reinterpret_cast<cudaStream_t>(stream));
+  if (e == cudaSuccess) e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    spc::set_cuda_error(e);
+    return SPC_E_CUDA;
+  }
+  int rc = SPC_OK;
+  std::lock_guard<std::mutex> lk(spc::g_reader_mu);
+  for (const auto& r : spc::err_readers()) {
+    const unsigned v = r.fn();
+    if (v && rc == SPC_OK) {
+      rc = (int)(v & 0xFFu);
+      snprintf(spc::g_err, sizeof(spc::g_err), "device contract violation (%s) at %s:%u",
+               spc_status_string(rc), r.file, v >> 8);
+    }
+  }
+  return rc;
+}
 int spc_version(void) { return 100; }
 uint64_t spc_launch_count(void) { return spc::g_launches.load(); }
 }

@@ -185,17 +185,7 @@ int launch_logits(const uint16_t* kr, const uint16_t* q, const int32_t* seq_len,
   const int ntiles = B * G * tpr;
   const int nh = B * G * ALPHA;
   if ((long long)B * G * Smax < (1ll << 31)) {  // TMA-fed kernel (int32 row coordinates)
-    static std::atomic<uint64_t> done{0};  // max-dynamic-smem attribute, per device
-    int dev = 0;
-    SPC_TRY(launched(cudaGetDevice(&dev)));
-    const uint64_t bit = dev < 64 ? 1ull << dev : 0ull;
-    if (!bit || !(done.load(std::memory_order_acquire) & bit)) {
-      const cudaError_t e = cudaFuncSetAttribute(logits_tma_kernel<D, ALPHA>,
-                                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 LtSmem<D, ALPHA>::BYTES);
-      if (e != cudaSuccess) return launched(e);
-      done.fetch_or(bit, std::memory_order_acq_rel);
-    }
+    SPC_TRY(smem_attr((const void*)logits_tma_kernel<D, ALPHA>, LtSmem<D, ALPHA>::BYTES));
     CUtensorMap map;
     SPC_TRY(make_tmap_tile_bf16(&map, kr, (uint64_t)B * G * Smax, D, LG_TR));
     const int ncta = max(1, min(num_sms(), ntiles));
@@ -204,12 +194,7 @@ int launch_logits(const uint16_t* kr, const uint16_t* q, const int32_t* seq_len,
                               ntiles, logits, tile_max)));
   } else {
     const size_t smem = LgSmem<D, ALPHA>::BYTES;
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(logits_kernel<D, ALPHA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)smem);
-      attr = true;
-    }
+    SPC_TRY(smem_attr((const void*)logits_kernel<D, ALPHA>, (int)smem));
     const int nw = (ntiles + 1) / 2;  // >= 2 tiles per warp
     const int ncta = max(1, min(num_sms(), (nw + lg_warps<ALPHA>() - 1) / lg_warps<ALPHA>()));
     SPC_TRY(launched(launch_k(logits_kernel<D, ALPHA>, dim3(ncta), dim3(32 * lg_warps<ALPHA>()),

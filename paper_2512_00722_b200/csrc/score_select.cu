@@ -312,6 +312,7 @@ __global__ void __launch_bounds__(SS_NT, 1) score_select_kernel(
       int c0 = 0, c1 = 0, c2 = 0;
       for (int i = ht; i < S.np; i += nht) {
         const int t = __ldg(pv + i);
+        SPC_DCHECK(t >= 0 && (i == 0 || __ldg(pv + i - 1) < t), t < 0 ? SPC_E_RANGE : SPC_E_STATE);
         if (t >= S.t0 && t < tend) atomicOr(&bm[(S.u0 + t - S.t0) >> 5], 1u << ((S.u0 + t - S.t0) & 31));
         c0 += t < S.t0;
         c1 += t < tend;
@@ -370,6 +371,7 @@ __global__ void __launch_bounds__(SS_NT, 1) score_select_kernel(
           const int row = lane + 32 * r;
           const float sv = __fmul_rn((r & 1) ? acc[j][r >> 1].y : acc[j][r >> 1].x, scale);
           if (t0 + row < len) {
+            SPC_DCHECK(sv == sv, SPC_E_RANGE);  // NaN key / query (reading R20)
             lgout[((size_t)b * Hq + g * ALPHA + j) * Smax + t0 + row] = sv;
             m = fmaxf(m, sv);
           }
@@ -862,17 +864,7 @@ int ss_launch(const uint16_t* q, const uint16_t* kr, const int32_t* seq_len, int
               float* group_score, int32_t* out_idx, int32_t* out_count, const int32_t* prev_idx,
               const int32_t* prev_count, int32_t* load_tok, int32_t* n_load, int32_t* evict_tok,
               int32_t* n_evict, SsWs w, int ncta, cudaStream_t st) {
-  static std::atomic<uint64_t> done{0};  // max-dynamic-smem attribute, per device
-  int dev = 0;
-  cudaError_t e = cudaGetDevice(&dev);
-  if (e != cudaSuccess) return launched(e);
-  const uint64_t bit = dev < 64 ? 1ull << dev : 0ull;
-  if (!bit || !(done.load(std::memory_order_acquire) & bit)) {
-    e = cudaFuncSetAttribute(score_select_kernel<DD, AA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             SsSmem<DD, AA>::BYTES);
-    if (e != cudaSuccess) return launched(e);
-    done.fetch_or(bit, std::memory_order_acq_rel);
-  }
+  SPC_TRY(smem_attr((const void*)score_select_kernel<DD, AA>, SsSmem<DD, AA>::BYTES));
   const int tpr = (Smax + LG_TR - 1) / LG_TR;
   CUtensorMap map;
   SPC_TRY(make_tmap_tile_bf16(&map, kr, (uint64_t)B * G * Smax, DD, LG_TR));

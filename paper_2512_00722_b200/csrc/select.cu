@@ -200,6 +200,13 @@ __global__ void __launch_bounds__(ST, 1) select_kernel(
   int pvr[PVR];
 #pragma unroll
   for (int i = 0; i < PVR; ++i) pvr[i] = tid + i * ST < np ? pv[tid + i * ST] : -1;
+#ifdef SPC_DEBUG  // the previous selection: ascending, no duplicates, ids >= 0
+  if (rank == 0)
+    for (int i = tid; i < np; i += ST) {
+      SPC_DCHECK(pv[i] >= 0, SPC_E_RANGE);
+      SPC_DCHECK(i == 0 || pv[i - 1] < pv[i], SPC_E_STATE);
+    }
+#endif
   float m[ALPHA];
 #pragma unroll
   for (int j = 0; j < ALPHA; ++j) m[j] = head_max[(size_t)b * Hq + g * ALPHA + j];
@@ -628,15 +635,7 @@ int launch_select(const float* logits, const float* head_max, const int32_t* seq
                   const int32_t* prev_count, int32_t* load_tok, int32_t* n_load,
                   int32_t* evict_tok, int32_t* n_evict, cudaStream_t st) {
   auto kern = select_kernel<AA, (AA > 4 ? 1 : 2), SCL>;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)sizeof(SelSm<SCL>));
-    if (e == cudaSuccess && SCL > 8)
-      e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    if (e != cudaSuccess) return launched(e);
-    attr = true;
-  }
+  SPC_TRY(smem_attr((const void*)kern, (int)sizeof(SelSm<SCL>), SCL > 8));
   return launched(launch_kc(kern, dim3(SCL, B * G), dim3(ST), sizeof(SelSm<SCL>), st, SCL,
                             logits, head_max, seq_len, G, Smax, k, force_last, head_sumfix,
                             group_score, out_idx, out_count, prev_idx, prev_count, load_tok,

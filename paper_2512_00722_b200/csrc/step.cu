@@ -21,7 +21,25 @@ extern "C" size_t spc_decode_step_workspace(int L, int B, int Hq, int G, int D, 
 extern "C" int spc_decode_step(const spc_step_args* a, spc_stream_t stream) {
   if (!a) return SPC_E_NULL;
   const int L = a->L, B = a->B, Hq = a->Hq, G = a->G, D = a->D, Smax = a->Smax, k = a->k;
-  if (!a->ws) return SPC_E_NULL;
+  // every argument of every call is checked here, before the first launch: an error never
+  // leaves the selection state half-written
+  if (!a->ws || !a->q_ret || !a->kr || !a->seq_len || !a->q_llm || !a->logits || !a->head_max ||
+      !a->head_sumfix || !a->group_score || !a->prev_idx || !a->prev_count || !a->cur_idx ||
+      !a->cur_count || !a->load_tok || !a->n_load || !a->out)
+    return SPC_E_NULL;
+  if (!a->kv_desc && (!a->k_layers || !a->v_layers)) return SPC_E_NULL;
+  if (L <= 0 || B <= 0 || Hq <= 0 || G <= 0 || Hq % G || Smax <= 0 || a->rows <= 0)
+    return SPC_E_SHAPE;
+  if (k < 1 || k > SPC_MAX_K) return SPC_E_BUDGET;
+  if (Smax >= SPC_MAX_SEQ) return SPC_E_RANGE;
+  {
+    const int alpha = Hq / G;
+    if (!(D == 64 || D == 128) || !(alpha == 1 || alpha == 2 || alpha == 4 || alpha == 8))
+      return SPC_E_UNSUPPORTED;
+  }
+  if (((uintptr_t)a->kr & 15) || ((uintptr_t)a->q_ret & 15)) return SPC_E_RANGE;
+  if (a->kv_desc && ((uintptr_t)a->kv_desc % 64 || (uint64_t)B * G * a->rows >= (1ull << 31)))
+    return SPC_E_RANGE;
   if (a->ws_bytes < spc_decode_step_workspace(L, B, Hq, G, D, Smax, k)) return SPC_E_WORKSPACE;
   uint8_t* ws = (uint8_t*)a->ws;
   const size_t s_b = align_up(spc_score_workspace(B, Hq, Smax), 256);

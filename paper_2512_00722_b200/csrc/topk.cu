@@ -447,14 +447,6 @@ __global__ void __launch_bounds__(SEL_THREADS) filter_kernel(
   if (tid == 0) count[row] = total;
 }
 
-int set_big_smem(const void* fn, size_t bytes) {
-  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-  if (e != cudaSuccess) {
-    set_cuda_error(e);
-    return SPC_E_CUDA;
-  }
-  return SPC_OK;
-}
 
 }  // namespace
 }  // namespace spc
@@ -479,11 +471,7 @@ extern "C" int spc_topk(const float* val, const int32_t* seq_len, int B, int G, 
   if (k < 1 || k > SPC_MAX_K) return SPC_E_BUDGET;
   if (n_cols >= SPC_MAX_SEQ || id_stride < 1 || id_offset < 0) return SPC_E_RANGE;
   if ((long long)n_cols * id_stride + id_offset >= 0x7FFFFFFFLL) return SPC_E_RANGE;
-  static bool attr = false;
-  if (!attr) {
-    SPC_TRY(set_big_smem((const void*)topk_cluster_kernel, sizeof(ClSmem)));
-    attr = true;
-  }
+  SPC_TRY(smem_attr((const void*)topk_cluster_kernel, (int)sizeof(ClSmem)));
   return launched(launch_k(topk_cluster_kernel, dim3(CL, B * G), dim3(SEL_THREADS),
                            sizeof(ClSmem), as_stream(stream), val, seq_len, G, n_cols, k,
                            force_last, id_stride, id_offset, out_idx, out_val, out_count,
@@ -505,11 +493,7 @@ extern "C" int spc_topk_merge(const float* cand_val, const int32_t* cand_pos,
   if (!cand_val || !cand_pos || !cand_count || !out_thresh) return SPC_E_NULL;
   if (P < 1 || P > 64 || R < 1) return SPC_E_SHAPE;
   if (k < 1 || k > SPC_MAX_K) return SPC_E_BUDGET;
-  static bool attr = false;
-  if (!attr) {
-    SPC_TRY(set_big_smem((const void*)merge_kernel, sizeof(SelSmem)));
-    attr = true;
-  }
+  SPC_TRY(smem_attr((const void*)merge_kernel, (int)sizeof(SelSmem)));
   return launched(launch_k(merge_kernel, dim3(R), dim3(SEL_THREADS), sizeof(SelSmem),
                            as_stream(stream), cand_val, cand_pos, cand_count, P, R, k,
                            (unsigned long long*)out_thresh));

@@ -16,6 +16,7 @@ import torch
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libspc.so")
+DEBUG_LIB_PATH = os.path.join(HERE, "libspc_debug.so")  # SPC_DEBUG: device contract checks
 
 BF16, F32 = 0, 1
 SCORE_LOGITS, SCORE_NORM, SCORE_GROUP, SCORE_ALL, SCORE_BATCH = 1, 2, 4, 7, 16
@@ -32,6 +33,7 @@ EXPORTS = [
     "spc_mla_sparse_attn", "spc_decode_step_workspace", "spc_decode_step",
     "spc_kv_desc_bytes", "spc_kv_desc_init", "spc_sparse_decode_attn_kv",
     "spc_score_select_supported", "spc_score_select_workspace", "spc_score_select",
+    "spc_debug_build", "spc_check_device_errors",
 ]
 
 
@@ -111,6 +113,8 @@ def load_library(path: str = LIB_PATH):
     L.spc_sparse_decode_attn.argtypes = [i32, P, P, P, i32, P, P, i32, i32, i32, i32, i32, i32,
                                          i32, i32, i32, f32, P, P, P, sz, P]
     L.spc_attn_merge.argtypes = [P, P, i32, i32, i32, P, P, P]
+    L.spc_debug_build.restype = i32
+    L.spc_check_device_errors.argtypes = [P]
     L.spc_score_select_supported.argtypes = [i32, i32, i32, i32, i32, i32]
     L.spc_score_select_workspace.argtypes = [i32, i32, i32, i32]
     L.spc_score_select_workspace.restype = sz
@@ -194,6 +198,12 @@ def topk_merge_workspace(P: int, R: int, k: int) -> int:
 
 def attn_workspace(L: int, B: int, Hq: int, D: int, k: int) -> int:
     return int(lib().spc_attn_workspace(L, B, Hq, D, k))
+
+
+def check_device_errors(stream=None) -> int:
+    """spc_check_device_errors: synchronise and return (and clear) the first device-side
+    contract violation (SPC_DEBUG builds) as a spc_status code; 0 = none."""
+    return int(lib().spc_check_device_errors(_s(stream)))
 
 
 def alloc_workspace(nbytes: int, device) -> torch.Tensor:

@@ -78,7 +78,14 @@ def test_host_validation_without_gpu(libspc):
     a.L, a.B, a.Hq, a.G, a.D, a.Smax, a.rows, a.k = 32, 1, 32, 8, 128, 32768, 32768, 2048
     assert libspc.spc_decode_step(ctypes.byref(a), st) == 1  # ws NULL
     a.ws, a.ws_bytes = 16, 8
+    assert libspc.spc_decode_step(ctypes.byref(a), st) == 1  # the other buffers NULL: checked first
+    for name, _ in spc.StepArgs._fields_:
+        if name not in ("L", "B", "Hq", "G", "D", "Smax", "rows", "k", "force_last", "scale",
+                        "ws_bytes", "lse", "kv_desc"):
+            setattr(a, name, 64)
     assert libspc.spc_decode_step(ctypes.byref(a), st) == 6  # workspace too small
+    a.k = 5000
+    assert libspc.spc_decode_step(ctypes.byref(a), st) == 3  # budget: before any launch
     assert libspc.spc_decode_step_workspace(32, 1, 32, 8, 128, 32768, 2048) > 0
     # MLA: unsupported latent width, budget, workspace
     assert libspc.spc_mla_sparse_attn(P, P, P, P, P, P, 1, 1, 16, 100, 64, 256, 64, 128, 128, 0.1,
