@@ -186,6 +186,9 @@ __global__ void __launch_bounds__(ST, 1) select_kernel(
   const float* lg = logits + ((size_t)b * Hq + g * ALPHA) * Smax + s0;
   const int np = min(max(prev_count[bg], 0), k);
   const int32_t* pv = prev_idx + (size_t)bg * k;
+  // every CTA of the cluster must have started before any remote shared-memory write (the
+  // NORM partials below): arrive now, wait right before the first push (hidden latency)
+  cl.barrier_arrive();
   sel_mark(0);
 
   // ---- prologue: logits of the first NC chunks and the previous selection in flight
@@ -297,6 +300,7 @@ __global__ void __launch_bounds__(ST, 1) select_kernel(
     if (lane == 0) s.wred[warp][j] = v;
   }
   __syncthreads();
+  cl.barrier_wait();
   if (tid < ALPHA) {
     long long t = 0;
 #pragma unroll

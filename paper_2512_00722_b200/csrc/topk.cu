@@ -297,6 +297,8 @@ __device__ void cluster_select(ClSmem& s, cg::cluster_group& cl, const KeyFn& ke
     }
     cl.sync();
     T = s.T;
+  } else {
+    cl.sync();  // no cut: every CTA must have started before the remote writes below
   }
   // ---- 4. ordered compaction over the cluster
   const int seg = s1 - s0;
