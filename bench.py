@@ -765,10 +765,13 @@ def bench_offload(args):
     """Config D (offloaded KV): S = 262,144, k = 2048, the LLM KV in pinned host memory,
     SLOTS mode: each step spc_gather_kv copies only the newly selected rows (elastic load)
     over PCIe into the HBM budget buffers, then attention reads the buffers.  Host RAM on
-    the box (196 GB) cannot hold config D's 1.1 TB of KV, so B = 4 requests (per-request
-    traffic is unchanged; bytes scale with B) over 8 physical layers aliased at distinct row
-    offsets (34 GB pinned).  Reports the PCIe bytes moved per step against the measured
-    pinned host->device copy bandwidth."""
+    the box (196 GB) cannot hold config D's 1.1 TB of KV, so B = 8 requests by default
+    (--batch; per-request traffic is unchanged, bytes scale with B) over 8 physical layers
+    aliased at distinct row offsets (70 GB pinned at B = 8).  Reports the PCIe bytes moved
+    per step against the measured pinned host->device copy bandwidth, and the same step with
+    the asynchronous prefetch dataflow: the gather of layer group j on a side
+    stream overlapping the attention of group j-1 (4 groups of 8 layers = whole 4 KiB
+    records), with the fraction of the attention hidden under the gather."""
     import torch
 
     from paper_2512_00722_b200 import build as spc_build
@@ -779,7 +782,8 @@ def bench_offload(args):
         spc_build.build()
     dev = torch.device("cuda", 0)
     c = synth.CONFIGS["D"]
-    B, G, Hq, D, S, L, k = 4, c["G"], c["Hq"], c["D"], c["S"], c["L"], c["k"]
+    B = args.batch if args.batch > 1 else 8
+    G, Hq, D, S, L, k = c["G"], c["Hq"], c["D"], c["S"], c["L"], c["k"]
     PHYS, OFF = 8, 1024
     nsteps = args.warmup + args.steps
     rows = S + (L // PHYS - 1) * OFF
@@ -818,39 +822,57 @@ def bench_offload(args):
     qr = synth.retrieval_queries(nsteps + 1, B, Hq, G, D, seed=seed, device=dev)
     ql = synth.llm_queries(2, L, B, Hq, D, seed=seed, device=dev)
     seq = torch.full((B,), S, dtype=torch.int32, device=dev)
-    st = DecodeStep(kr, [kb[l] for l in range(L)], [vb[l] for l in range(L)], seq, L, Hq, k,
-                    mode="slots", k_src_layers=k_src, v_src_layers=v_src, kv_rows=k,
-                    src_rows=rows, src_strides=src_strides)
-    st.step(qr[0], ql[0])
-    n0 = spc.launch_count()
-    seq_graphs = st.capture_sequence([(0, qr[i], ql[i % 2]) for i in range(nsteps)])
-    launches_per_step = (spc.launch_count() - n0) // nsteps
-    warm_graphs(st, seq_graphs)
-    kb.zero_()
-    vb.zero_()
     stream = torch.cuda.current_stream()
-    loaded = torch.zeros((), dtype=torch.int64, device=dev)
 
-    def one_step(i):
-        seq_graphs[i].replay()
-        st.parity ^= 1
-        loaded.add_(st.n_load.sum())
+    def measure(groups):
+        """(ms per step, rows loaded per step, launches per step, clocks, step object)"""
+        kb.zero_()
+        vb.zero_()
+        st = DecodeStep(kr, [kb[l] for l in range(L)], [vb[l] for l in range(L)], seq, L, Hq, k,
+                        mode="slots", k_src_layers=k_src, v_src_layers=v_src, kv_rows=k,
+                        src_rows=rows, src_strides=src_strides, prefetch_groups=groups)
+        st.step(qr[0], ql[0])
+        n0 = spc.launch_count()
+        seq_graphs = st.capture_sequence([(0, qr[i], ql[i % 2]) for i in range(nsteps)])
+        per_step = (spc.launch_count() - n0) // nsteps
+        warm_graphs(st, seq_graphs)
+        kb.zero_()
+        vb.zero_()
+        loaded = torch.zeros((), dtype=torch.int64, device=dev)
 
-    for i in range(args.warmup):
-        one_step(i)
-    torch.cuda.synchronize()
-    loaded.zero_()
-    sampler = ClockSampler(0)
-    sampler.start()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for j in range(args.steps):
-        one_step(args.warmup + j)
-    e1.record(stream)
-    torch.cuda.synchronize()
-    clocks = sampler.stop()
-    ms = e0.elapsed_time(e1) / args.steps
-    rows_loaded = int(loaded.item()) / args.steps
+        def one_step(i):
+            seq_graphs[i].replay()
+            st.parity ^= 1
+            loaded.add_(st.n_load.sum())
+
+        for i in range(args.warmup):
+            one_step(i)
+        torch.cuda.synchronize()
+        loaded.zero_()
+        sampler = ClockSampler(0)
+        sampler.start()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for j in range(args.steps):
+            one_step(args.warmup + j)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        clk = sampler.stop()
+        return e0.elapsed_time(e1) / args.steps, int(loaded.item()) / args.steps, per_step, clk, st
+
+    ms, rows_loaded, launches_per_step, clocks, st = measure(1)
+    ms_pipe, _, launches_pipe, clocks_pipe, st_pipe = measure(4)
+    # attention alone over the filled budget buffers (all layers), for the overlap fraction
+    a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    for rep in range(2):
+        a0.record(stream)
+        for _ in range(10):
+            st_pipe._attn_slots(st_pipe.last, st_pipe.q_llms[0], st_pipe.outs[0], st_pipe.lses[0],
+                                0, L, stream)
+        a1.record(stream)
+        torch.cuda.synchronize()
+    attn_ms = a0.elapsed_time(a1) / 10
+    overlap = max(0.0, min(1.0, (ms - ms_pipe) / attn_ms)) if attn_ms > 0 else 0.0
     pcie_bytes = rows_loaded * L * 2 * D * 2
     # denominator: pinned host -> device copy of 1 GiB
     hsrc = torch.empty(1 << 30, dtype=torch.uint8, pin_memory=True)
@@ -870,7 +892,7 @@ def bench_offload(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (seeded; DESIGN.md §5)",
-        "config": {"workload": workload_name(dict(c, B=B), "D") + " (B reduced from 32: host RAM)",
+        "config": {"workload": workload_name(dict(c, B=B), "D") + " (B reduced from 32: host RAM of the box)",
                    "kv": (f"LLM KV in pinned host memory, token-major records [{PHYS} layers][K,V]"
                           f"[D] (4 KiB) per token, layer l = physical l % {PHYS} of the record "
                           f"of token t + (l // {PHYS}) * {OFF}" if token_major else
@@ -884,7 +906,16 @@ def bench_offload(args):
                    "rows_loaded_per_step": rows_loaded,
                    "elastic_reuse": round(1 - rows_loaded / (B * G * k), 4),
                    "pcie_bytes_per_step": pcie_bytes,
-                   "pinned_h2d_copy_gbs": round(h2d, 1)},
+                   "pinned_h2d_copy_gbs": round(h2d, 1),
+                   "prefetch_pipeline": {
+                       "what": "gather of layer group j (8 layers) on a prefetch stream, "
+                               "attention of group j waiting on its event (P:350, P:374)",
+                       "groups": 4, "ms_per_step": ms_pipe, "serial_ms_per_step": ms,
+                       "attention_alone_ms": attn_ms,
+                       "attention_hidden_frac": round(overlap, 3),
+                       "pcie_gbs": round(pcie_bytes / (ms_pipe * 1e-3) / 1e9, 1),
+                       "tokens_per_s": B / (ms_pipe * 1e-3), "gpu_launches_per_step": launches_pipe,
+                       "clocks": clocks_pipe}},
         "roofline": {"bound": "pcie", "achieved": achieved, "peak": h2d, "unit": "GB/s",
                      "frac": achieved / h2d, "traffic": None,
                      "kernel": "whole step, PCIe bytes of the elastic gather / step time",

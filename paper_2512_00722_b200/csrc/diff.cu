@@ -319,7 +319,16 @@ extern "C" int spc_gather_kv_strided(int dtype, const void* const* k_src, const 
   if (!(vpr == 8 || vpr == 16) || (row_stride * 2) % 16 || (bg_stride * 2) % 16)
     return SPC_E_UNSUPPORTED;
   const int tpb = GT_WARPS * (32 / (2 * vpr));
-  dim3 grid((unsigned)std::min((k + tpb - 1) / tpb, 64), B * G);
+  // PCIe-bound: a few MB in flight saturate the link, so the grid is capped at half the SMs
+  // in total -- the other half stays free for the attention of the previous layer group
+  // (the prefetch pipeline of DecodeStep); env SPC_GATHER_CTAS overrides (tools)
+  static const int cap_env = [] {
+    const char* e = std::getenv("SPC_GATHER_CTAS");
+    return e ? std::atoi(e) : 0;
+  }();
+  const int cap = cap_env > 0 ? cap_env : std::max(1, num_sms() / 2);
+  const int nx = std::max(1, std::min((k + tpb - 1) / tpb, (cap + B * G - 1) / (B * G)));
+  dim3 grid((unsigned)nx, B * G);
   return launched(launch_k(gather_strided_kernel, grid, dim3(GT_WARPS * 32), 0,
                            as_stream(stream), k_src, v_src, row_stride, bg_stride, k, vpr,
                            layer_begin, layer_end - layer_begin, load_tok, load_slot, n_load,

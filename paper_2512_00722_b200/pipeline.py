@@ -27,14 +27,17 @@ class DecodeStep:
     def __init__(self, kr: torch.Tensor, k_layers, v_layers, seq_len: torch.Tensor, L: int,
                  Hq: int, k: int, mode: str = "indexed", force_last: bool = True, scale=None,
                  kv_rows=None, k_src_layers=None, v_src_layers=None, fused=None,
-                 src_rows=None, src_strides=None, retrieval: str = "head", one_launch=False):
+                 src_rows=None, src_strides=None, retrieval: str = "head", one_launch=False,
+                 prefetch_groups: int = 1):
         """kr: retrieval keys [B][G][Smax][D] bf16.  k_layers/v_layers: L tensors [B][G][rows][D]
         (INDEXED: the full caches; SLOTS: the budget buffers [B][G][k][D], with
         k_src_layers/v_src_layers the full caches, device or mapped host).  src_strides =
         (row_stride, bg_stride) in elements: the sources are strided views (e.g. the layers of
         token-major KV records) and the elastic load uses spc_gather_kv_strided.
         retrieval: "head" (head-level, the paper's choice: group max) or "batch"
-        (batch-level: one set per request from the sum over all heads; NEXT-3)."""
+        (batch-level: one set per request from the sum over all heads; NEXT-3).
+        prefetch_groups (SLOTS): gather / attend the layers in this many groups, the gather of
+        group j on a prefetch stream overlapping the attention of group j-1."""
         assert retrieval in ("head", "batch")
         self.retrieval = retrieval
         self.dev = kr.device
@@ -79,6 +82,13 @@ class DecodeStep:
             self.v_src_tab = spc.ptr_table(self.v_src, self.dev)
             self.src_rows = src_rows if src_rows is not None else self.k_src[0].shape[2]
             self.src_strides = src_strides
+        # SLOTS: the layers are gathered and attended in `prefetch_groups` groups; with more
+        # than one, group j's gather (prefetch stream) overlaps group j-1's attention
+        n = max(1, min(int(prefetch_groups), L))
+        self.layer_groups = [(L * j // n, L * (j + 1) // n) for j in range(n)]
+        if mode == "slots" and n > 1:
+            self._pf_stream = torch.cuda.Stream(device=kr.device)
+            self._pf_events = [torch.cuda.Event() for _ in range(n + 1)]
         B, G, Hq, D, dev = self.B, self.G, Hq, self.D, self.dev
         f32, i32 = torch.float32, torch.int32
         # step inputs and outputs are double-buffered by step parity, so the host copies of
@@ -202,24 +212,26 @@ class DecodeStep:
                              self.load_tok, self.n_load, slot_tok=self.slot_tok,
                              load_slot=self.load_slot, stream=stream)
         if self.mode == "slots":
-            if self.src_strides is not None:
-                spc.gather_kv_strided(self.k_src_tab, self.v_src_tab, self.src_strides[0],
-                                      self.src_strides[1], self.L, self.B, self.G, self.D, self.k,
-                                      self.load_tok, self.load_slot, self.n_load, self.k_tab,
-                                      self.v_tab, stream=stream)
+            main = torch.cuda.current_stream(self.dev) if stream is None else stream
+            groups = self.layer_groups
+            if len(groups) == 1:
+                self._gather(0, self.L, main)
+                self._attn_slots(cur, q_llm, out, lse, 0, self.L, main)
             else:
-                spc.gather_kv(self.k_src_tab, self.v_src_tab, self.L, self.B, self.G, self.D,
-                              self.src_rows, self.k, self.load_tok, self.load_slot, self.n_load,
-                              self.k_tab, self.v_tab,
-                              dtype=spc.BF16 if self.kv_dtype == torch.bfloat16 else spc.F32,
-                              stream=stream)
-            if self.desc is not None:
-                spc.sparse_decode_attn_kv(self.desc, q_llm, spc.KV_SLOTS, None, self.cnt[cur],
-                                          self.k, self.scale, out, lse, self.ws_attn, stream=stream)
-            else:
-                spc.sparse_decode_attn(q_llm, self.k_tab, self.v_tab, spc.KV_SLOTS, None,
-                                       self.cnt[cur], self.k, self.k, self.scale, out, lse,
-                                       self.ws_attn, self.G, stream=stream)
+                # asynchronous prefetch ("concurrent execution of computation and KV
+                # cache prefetching"; elastic loading in that dataflow): the elastic
+                # gather of layer group j runs on the prefetch stream while the attention of
+                # group j - 1 runs on the step's stream; group j's attention waits only for
+                # group j's gather event
+                ev = self._pf_events
+                ev[0].record(main)
+                self._pf_stream.wait_event(ev[0])
+                for j, (l0, l1) in enumerate(groups):
+                    self._gather(l0, l1, self._pf_stream)
+                    ev[j + 1].record(self._pf_stream)
+                for j, (l0, l1) in enumerate(groups):
+                    main.wait_event(ev[j + 1])
+                    self._attn_slots(cur, q_llm, out, lse, l0, l1, main)
         elif self.desc is not None:
             spc.sparse_decode_attn_kv(self.desc, q_llm, spc.KV_INDEXED, self.idx[cur],
                                       self.cnt[cur], self.k, self.scale, out, lse, self.ws_attn,
@@ -228,6 +240,31 @@ class DecodeStep:
             spc.sparse_decode_attn(q_llm, self.k_tab, self.v_tab, spc.KV_INDEXED,
                                    self.idx[cur], self.cnt[cur], self.rows, self.k, self.scale,
                                    out, lse, self.ws_attn, self.G, stream=stream)
+
+    def _gather(self, l0, l1, stream):
+        """The elastic load (O9) of layers [l0, l1): the new tokens' rows into their slots."""
+        if self.src_strides is not None:
+            spc.gather_kv_strided(self.k_src_tab, self.v_src_tab, self.src_strides[0],
+                                  self.src_strides[1], self.L, self.B, self.G, self.D, self.k,
+                                  self.load_tok, self.load_slot, self.n_load, self.k_tab,
+                                  self.v_tab, layer_begin=l0, layer_end=l1, stream=stream)
+        else:
+            spc.gather_kv(self.k_src_tab, self.v_src_tab, self.L, self.B, self.G, self.D,
+                          self.src_rows, self.k, self.load_tok, self.load_slot, self.n_load,
+                          self.k_tab, self.v_tab, layer_begin=l0, layer_end=l1,
+                          dtype=spc.BF16 if self.kv_dtype == torch.bfloat16 else spc.F32,
+                          stream=stream)
+
+    def _attn_slots(self, cur, q_llm, out, lse, l0, l1, stream):
+        if self.desc is not None:
+            spc.sparse_decode_attn_kv(self.desc, q_llm, spc.KV_SLOTS, None, self.cnt[cur], self.k,
+                                      self.scale, out, lse, self.ws_attn, layer_begin=l0,
+                                      layer_end=l1, stream=stream)
+        else:
+            spc.sparse_decode_attn(q_llm, self.k_tab, self.v_tab, spc.KV_SLOTS, None,
+                                   self.cnt[cur], self.k, self.k, self.scale, out, lse,
+                                   self.ws_attn, self.G, layer_begin=l0, layer_end=l1,
+                                   stream=stream)
 
     def step(self, q_ret=None, q_llm=None, use_graph: bool = False):
         """Run one decode step on device tensors (copied into the step's input buffers)."""

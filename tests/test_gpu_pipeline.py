@@ -248,11 +248,14 @@ def test_native_decode_step_equals_pipeline(S, B, G):
         assert torch.equal(st.out, out)
 
 
-def test_offload_step_token_major_records(oracle):
+@pytest.mark.parametrize("groups", [1, 3])
+def test_offload_step_token_major_records(oracle, groups):
     """The config-D path at small size: LLM KV as token-major records in pinned host memory
     ([B][G][S][L][2][D]), SLOTS mode with spc_gather_kv_strided over PCIe: over three steps
     the selection is bit-exact, the budget slots hold exactly the selected tokens' rows, and
-    the attention matches the oracle."""
+    the attention matches the oracle -- with one gather, and with the per-layer-group
+    prefetch pipeline (gather of group j on a side stream, attention of group j waiting on
+    its event)."""
     B, G, Hq, D, S, L, k = 1, 2, 8, 64, 3000, 3, 256
     dev = torch.device("cuda")
     kr = synth.retrieval_keys(B, G, S, D, seed=21, device=dev)
@@ -266,7 +269,8 @@ def test_offload_step_token_major_records(oracle):
     seq = torch.full((B,), S, dtype=torch.int32, device=dev)
     st = DecodeStep(kr, [kb[l] for l in range(L)], [vb[l] for l in range(L)], seq, L, Hq, k,
                     mode="slots", k_src_layers=k_src, v_src_layers=v_src, kv_rows=k, src_rows=S,
-                    src_strides=(L * 2 * D, S * L * 2 * D))
+                    src_strides=(L * 2 * D, S * L * 2 * D), prefetch_groups=groups)
+    assert len(st.layer_groups) == groups
     kr_h = synth.bf16_bits(kr)
     kc = rec[..., 0, :].permute(3, 0, 1, 2, 4).contiguous()  # [L][B][G][S][D]
     vc = rec[..., 1, :].permute(3, 0, 1, 2, 4).contiguous()
@@ -283,7 +287,8 @@ def test_offload_step_token_major_records(oracle):
             assert sorted(slots[0, g, :cnt[0, g]].tolist()) == idx[0, g, :cnt[0, g]].tolist()
             for sl in (0, cnt[0, g] // 2, cnt[0, g] - 1):
                 t = int(slots[0, g, sl])
-                assert torch.equal(kbh[1, 0, g, sl], kc[1, 0, g, t])
+                for l in range(L):
+                    assert torch.equal(kbh[l, 0, g, sl], kc[l, 0, g, t])
         oo, _ = oracle.sparse_attn(synth.bf16_bits(ql), [kh[l] for l in range(L)],
                                    [vh[l] for l in range(L)], idx, cnt, st.scale)
         assert np.abs(st.out.cpu().numpy() - oo).max() <= 2e-3
