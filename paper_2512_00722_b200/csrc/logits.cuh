@@ -362,18 +362,17 @@ template <int D, int ALPHA>
 __global__ void __launch_bounds__(32 * (LT_NC + 1), 1) logits_tma_kernel(
     const __grid_constant__ CUtensorMap kmap, const uint16_t* __restrict__ q,
     const int32_t* __restrict__ seq_len, int G, int Smax, float scale, int tpr, int ntiles,
-    float* __restrict__ logits, float* __restrict__ tile_max) {
+    float* __restrict__ logits, float* __restrict__ tile_max, unsigned* __restrict__ ctr) {
   using SM = LtSmem<D, ALPHA>;
-  constexpr int NCH = SM::NCH, NST = SM::NST;
+  constexpr int NCH = SM::NCH, NST = SM::NST, K = SM::K;
   __shared__ __align__(8) uint64_t full[NST], empty[NST];
+  __shared__ int stage_tile[NST];  // tile id of a tile's first stage (-1: end of the work)
   extern __shared__ __align__(16) uint8_t lt_raw[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int Hq = G * ALPHA;
   const uint32_t base = (smem_u32(lt_raw) + 1023u) & ~1023u;
   uint8_t* basep = lt_raw + (base - smem_u32(lt_raw));
   const uint32_t full0 = smem_u32(&full[0]), empty0 = smem_u32(&empty[0]);
-  const int t_begin = (int)(((long long)blockIdx.x * ntiles) / gridDim.x);
-  const int t_end = (int)(((long long)(blockIdx.x + 1) * ntiles) / gridDim.x);
   if (tid == 0) {
     for (int s = 0; s < NST; ++s) {
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(full0 + 8 * s));
@@ -384,86 +383,108 @@ __global__ void __launch_bounds__(32 * (LT_NC + 1), 1) logits_tma_kernel(
   }
   __syncthreads();
   spc_pdl_entry();
-  // a tile is active when its first row is below its request's seq_len
-  auto active = [&](int tile) {
-    const int bg = tile / tpr;
-    return (tile - bg * tpr) * LG_TR < __ldg(seq_len + bg / G);
-  };
   if (warp == LT_NC) {
     // ------------------------------------------------------------ producer (lane 0)
+    // tiles come in batches of LT_BATCH consecutive tiles: the CTA's first batch is static,
+    // the next ones are claimed from one grid-wide counter, each claim issued a batch ahead
+    // (its latency hides behind the current batch); the counter balances the SMs, whose
+    // streaming rates differ (config E: 443 tiles per SM)
     if (lane == 0) {
-      int nt = 0;  // active-tile counter
-      for (int tile = t_begin; tile < t_end; ++tile) {
-        const int bg = tile / tpr, tt = tile - bg * tpr;
-        if (!active(tile)) {  // an empty tile (ragged batch): its maxima are -inf
-          const int b = bg / G, g = bg - b * G;
-          for (int j = 0; j < ALPHA; ++j)
-            tile_max[((size_t)b * Hq + g * ALPHA + j) * tpr + tt] = -INFINITY;
-          continue;
-        }
-        const int w = nt % LT_NC, n = nt / LT_NC;  // consumer warp and its tile count
-        ++nt;
-        for (int c = 0; c < NCH; ++c) {
-          const int j = n * NCH + c;  // sequence number in warp w's ring
-          const int s = w * SM::K + j % SM::K;
-          if (j >= SM::K) tm_wait(empty0 + 8 * s, ((j / SM::K) - 1) & 1);
-          const uint32_t fb = full0 + 8 * s;
-          tm_expect(fb, LT_STAGE + (c == 0 ? SM::QRAW : 0));
-          asm volatile(
-              "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
-              " [%0], [%1, {%2, %3}], [%4];" ::"r"(base + s * LT_STAGE),
-              "l"(&kmap), "r"(64 * c), "r"(bg * Smax + tt * LG_TR), "r"(fb)
-              : "memory");
-          if (c == 0) {
+      constexpr int LT_BATCH = 2;
+      int nt = 0;  // tiles handed to consumers
+      int batch = (int)blockIdx.x;
+      int next = (int)gridDim.x + (int)atomicAdd(ctr, 1u);
+      for (;;) {
+        const int t_lo = batch * LT_BATCH;
+        if (t_lo >= ntiles) break;
+        for (int tile = t_lo; tile < min(t_lo + LT_BATCH, ntiles); ++tile) {
+          const int bg = tile / tpr, tt = tile - bg * tpr;
+          if (tt * LG_TR >= __ldg(seq_len + bg / G)) {  // an empty tile (ragged batch)
             const int b = bg / G, g = bg - b * G;
+            for (int j = 0; j < ALPHA; ++j)
+              tile_max[((size_t)b * Hq + g * ALPHA + j) * tpr + tt] = -INFINITY;
+            continue;
+          }
+          const int w = nt % LT_NC, n = nt / LT_NC;  // consumer warp and its tile count
+          ++nt;
+          for (int c = 0; c < NCH; ++c) {
+            const int j = n * NCH + c;  // sequence number in warp w's ring
+            const int s = w * K + j % K;
+            if (j >= K) tm_wait(empty0 + 8 * s, ((j / K) - 1) & 1);
+            const uint32_t fb = full0 + 8 * s;
+            if (c == 0) stage_tile[s] = tile;  // published by the arrive below (release)
+            tm_expect(fb, LT_STAGE + (c == 0 ? SM::QRAW : 0));
             asm volatile(
-                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                    base + SM::QSLOT_OFF + s * SM::QRAW),
-                "l"(q + ((size_t)b * Hq + g * ALPHA) * D), "r"(SM::QRAW), "r"(fb)
+                "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+                " [%0], [%1, {%2, %3}], [%4];" ::"r"(base + s * LT_STAGE),
+                "l"(&kmap), "r"(64 * c), "r"(bg * Smax + tt * LG_TR), "r"(fb)
                 : "memory");
+            if (c == 0) {
+              const int b = bg / G, g = bg - b * G;
+              asm volatile(
+                  "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                      base + SM::QSLOT_OFF + s * SM::QRAW),
+                  "l"(q + ((size_t)b * Hq + g * ALPHA) * D), "r"(SM::QRAW), "r"(fb)
+                  : "memory");
+            }
           }
         }
+        batch = next;
+        if (batch * LT_BATCH < ntiles) next = (int)gridDim.x + (int)atomicAdd(ctr, 1u);
+      }
+      // end of the work: every consumer's next tile slot gets the end code
+      for (int w = 0; w < LT_NC; ++w) {
+        const int n = nt / LT_NC + (w < nt % LT_NC ? 1 : 0);  // tiles warp w received
+        const int j = n * NCH, s = w * K + j % K;
+        if (j >= K) tm_wait(empty0 + 8 * s, ((j / K) - 1) & 1);
+        stage_tile[s] = -1;
+        tm_arrive(full0 + 8 * s);
       }
     }
     return;
   }
   // -------------------------------------------------------------- consumers
-  float* qf = (float*)(basep + SM::QF_OFF + warp * SM::QF);
-  const uint32_t qf_s = smem_u32(qf);
   // per-warp rings: every ring has one consumer that waits for every one of its stages
   // in order, so a parity wait is never more than one phase ahead of its barrier
   // (consumers sharing one ring and skipping each other's stages can alias phases)
-  int nt = 0;  // active-tile counter
-  for (int tile = t_begin; tile < t_end; ++tile) {
-    if (!active(tile)) continue;
-    const int mine = (nt % LT_NC) == warp, n = nt / LT_NC;
-    ++nt;
-    if (!mine) continue;
-    const int bg = tile / tpr, t0 = (tile - bg * tpr) * LG_TR;
-    const int b = bg / G, g = bg - b * G;
-    const int S = __ldg(seq_len + b);
+  float* qf = (float*)(basep + SM::QF_OFF + warp * SM::QF);
+  const uint32_t qf_s = smem_u32(qf);
+  for (int n = 0;; ++n) {
+    int tile = 0, bg = 0, t0 = 0, b = 0, g = 0, S = 0;
     float2 acc[ALPHA][LG_RPT / 2];
 #pragma unroll
     for (int j = 0; j < ALPHA; ++j)
 #pragma unroll
       for (int p = 0; p < LG_RPT / 2; ++p) acc[j][p] = make_float2(0.f, 0.f);
+    bool done = false;
     for (int c = 0; c < NCH; ++c) {
       const int j = n * NCH + c;
-      const int s = warp * SM::K + j % SM::K;
-      tm_wait(full0 + 8 * s, (j / SM::K) & 1);
-      const uint32_t kc = base + s * LT_STAGE;
-      if (c == 0) {  // raw [ALPHA][D] bf16 -> fp32 [D][ALPHA]
+      const int s = warp * K + j % K;
+      tm_wait(full0 + 8 * s, (j / K) & 1);
+      if (c == 0) {
+        tile = stage_tile[s];
+        if (tile < 0) {
+          done = true;
+          break;
+        }
+        bg = tile / tpr;
+        t0 = (tile - bg * tpr) * LG_TR;
+        b = bg / G;
+        g = bg - b * G;
+        S = __ldg(seq_len + b);
+        // raw [ALPHA][D] bf16 -> fp32 [D][ALPHA]
         const uint16_t* qr = (const uint16_t*)(basep + SM::QSLOT_OFF + s * SM::QRAW);
         for (int e = lane; e < ALPHA * D; e += 32) {
-          const int j = e / D, d = e - j * D;
-          qf[d * ALPHA + j] = __uint_as_float((uint32_t)qr[e] << 16);
+          const int jj = e / D, d = e - jj * D;
+          qf[d * ALPHA + jj] = __uint_as_float((uint32_t)qr[e] << 16);
         }
         __syncwarp();
       }
-      lt_stage_math<D, ALPHA>(acc, kc, qf_s, qf, c, lane);
+      lt_stage_math<D, ALPHA>(acc, base + s * LT_STAGE, qf_s, qf, c, lane);
       __syncwarp();
       if (lane == 0) tm_arrive(empty0 + 8 * s);  // stage consumed
     }
+    if (done) break;
     // O1 final multiply by scale, store, O2 tile max -> tile_max
     float tm = 0.0f;
 #pragma unroll

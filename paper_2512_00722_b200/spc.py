@@ -346,7 +346,9 @@ class KvDesc:
             B, G, rows, D = k_layers[0].shape
         for t in list(k_layers) + list(v_layers):
             assert t.dtype == torch.bfloat16 and t.is_contiguous() and t.is_cuda
-            assert t.numel() >= B * G * rows * D
+            # 4-D caches hold every declared row; flat views (aliased layers at row offsets,
+            # bench config C) need only hold the rows the selections address
+            assert t.dim() == 1 or t.numel() >= B * G * rows * D
         self.L, self.B, self.G, self.rows, self.D = L, B, G, rows, D
         self._keep = (list(k_layers), list(v_layers))
         nbytes = int(lib().spc_kv_desc_bytes(L))
