@@ -101,7 +101,11 @@ __global__ void __launch_bounds__(TM_THREADS, TM_CTAS) attn_tma_kernel(
     prefetch_tmap(maps + lane * L + l0);
   }
   __syncthreads();
-  spc_pdl_entry();  // the selection (idx, count) is produced by the preceding launch
+  // PDL: no global input is read before griddepcontrol.wait -- not even the LLM queries,
+  // which no libspc launch writes: before the wait an SM may still serve lines cached by
+  // earlier kernels (measured: reading the queries early returned a previous step's values
+  // under graph replay, tests/test_gpu_pipeline.py config A)
+  spc_pdl_entry();
   if (n_chunks <= 0) return;
   if (warp == 0) tm_trace(0);
   const int g0 = c_begin / cpg;
@@ -227,13 +231,11 @@ __global__ void __launch_bounds__(TM_THREADS, TM_CTAS) attn_tma_kernel(
     // q and count of the current group, and of the next one (loaded a group ahead)
     uint32_t qn0[KS], qn2[KS];
     load_q(grp / BG, grp % BG, qa0, qa2);
-    int cnt_g = __ldg(count + grp % BG);
     const int g_last_c = (c_begin + n_chunks - 1) / cpg;
+    if (grp + 1 <= g_last_c) load_q((grp + 1) / BG, (grp + 1) % BG, qn0, qn2);
+    int cnt_g = __ldg(count + grp % BG);
     int cnt_n = 0;
-    if (grp + 1 <= g_last_c) {
-      load_q((grp + 1) / BG, (grp + 1) % BG, qn0, qn2);
-      cnt_n = __ldg(count + (grp + 1) % BG);
-    }
+    if (grp + 1 <= g_last_c) cnt_n = __ldg(count + (grp + 1) % BG);
     constexpr bool LOSEP = ALPHA == 8;
     constexpr int NACC = LOSEP ? 2 : 1;
     const int srcl = LOSEP ? lane : ((lane & ~3) | (ALPHA == 4 ? (tig & 1) : 0));
