@@ -388,6 +388,54 @@ int spc_rethead_qk(const int32_t* token, const void* emb, int V, int H, const vo
                    void* kr, int32_t* seq_len_out, void* x_out, spc_stream_t stream);
 
 /* ------------------------------------------------------------------------
+ * spc_llm_* — the LLM decoder layer's elementwise operations around the sparse
+ * attention (the per-layer dense compute that the KV prefetch
+ * overlaps, Fig. 3 / P:199, "concurrent execution of computation and KV cache
+ * prefetching").  A Llama-style layer (DeepSeek-R1-Distill-Llama-8B shape, random
+ * weights, reading R28): x = RMSNorm(h); [q k v] = W_qkv x; RoPE(q, k); append k, v;
+ * a = SparseAttn(q, selected K/V) (spc_sparse_decode_attn_kv); h += W_o a;
+ * x = RMSNorm(h); h += W_down(silu(W_g x) * W_u x).  The projections are plain cuBLAS
+ * GEMMs issued by the caller; these calls are the rest.  bf16 storage (raw uint16
+ * bits), fp32 arithmetic, all on `stream`, asynchronous, PDL-chained.
+ * Errors: SPC_E_NULL (required pointer NULL), SPC_E_SHAPE (sizes <= 0, Hq % G, odd D),
+ * SPC_E_UNSUPPORTED (add_rmsnorm: H % 4 or H > 16384; rope_append: D > 128),
+ * SPC_E_RANGE (add_rmsnorm: h, delta, w, xn not 16-byte aligned; rope_append: slot_tok
+ * not 16-byte aligned), SPC_E_CUDA.  Data-dependent violations (token or position out of
+ * range) give zeros / no write; SPC_DEBUG builds flag them (spc_check_device_errors).
+ *
+ * spc_llm_embed:       h [B][H] f32 out = emb[token[b]] ([V][H] bf16; token DEVICE).
+ * spc_llm_add_rmsnorm: h [B][H] f32 in/out (the residual stream); if delta [B][H] bf16
+ *   is not NULL, h += delta first.  xn [B][H] bf16 out = bf16(w * bf16(h * r)),
+ *   r = 1/sqrt(mean_i h_i^2 + eps) (the HF Llama form: normalise, round, scale, round).
+ * spc_llm_rope_append: qkv [B][(Hq + 2G) D] bf16 (W_qkv rows: q heads, k heads, v heads);
+ *   p = seq_len[b] - 1 (the new token's position, DEVICE; 0 <= p < rows).
+ *   q_out [B][Hq][D] bf16 = RoPE(q); k_cache / v_cache [B][G][rows][D] bf16 (device or
+ *   mapped host): row p = RoPE(k) / v.  RoPE on pairs (i, i + D/2) with angle
+ *   fl32(p * inv_freq[i]) (inv_freq [D/2] f32): (u, v) -> (u cos - v sin, v cos + u sin).
+ *   slot_tok [B][G][k] int32 or NULL (SLOTS mode: the slot map after
+ *   spc_elastic_diff): when slot s of (b, g) holds token p, row s of the budget
+ *   buffers k_buf / v_buf [B][G][k][D] receives the same key / value.
+ * spc_llm_swiglu:      gu [B][2F] bf16 (gate then up) -> y [B][F] bf16 =
+ *   bf16(silu(gate) * up), silu(g) = g / (1 + e^-g).
+ * spc_llm_f32_to_bf16: y[i] = bf16_rn(x[i]), n elements.
+ * spc_llm_argmax:      token_out[b] = argmax_v logits[b][v] ([B][V] bf16; lowest index
+ *   among equal maxima; NaN ignored; 0 if all NaN), then seq_len[b] += 1 when seq_len is
+ *   not NULL: the next step's token and position, without a host round trip.
+ * ---------------------------------------------------------------------- */
+int spc_llm_embed(const int32_t* token, const void* emb, int V, int H, int B, float* h,
+                  spc_stream_t stream);
+int spc_llm_add_rmsnorm(float* h, const void* delta, const void* w, int B, int H, float eps,
+                        void* xn, spc_stream_t stream);
+int spc_llm_rope_append(const void* qkv, const float* inv_freq, const int32_t* seq_len, int B,
+                        int Hq, int G, int D, int rows, void* q_out, void* k_cache, void* v_cache,
+                        const int32_t* slot_tok, int k, void* k_buf, void* v_buf,
+                        spc_stream_t stream);
+int spc_llm_swiglu(const void* gu, int B, int F, void* y, spc_stream_t stream);
+int spc_llm_f32_to_bf16(const float* x, long long n, void* y, spc_stream_t stream);
+int spc_llm_argmax(const void* logits, int B, int V, int32_t* token_out, int32_t* seq_len,
+                   spc_stream_t stream);
+
+/* ------------------------------------------------------------------------
  * Adaptive memory management — HOST functions (no GPU work).
  * Paper §6: Eq. 6-8, Algorithm 1 (thresholds at compile time) and
  * Algorithm 2 (progressive per-layer offload during decode).  Readings R25-R27.

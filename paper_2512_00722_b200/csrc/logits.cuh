@@ -287,6 +287,9 @@ __global__ void __launch_bounds__(256) lg_finalize_kernel(const float* __restric
 #ifndef SPC_LT_NC
 #define SPC_LT_NC 4
 #endif
+#ifndef SPC_LT_BATCH
+#define SPC_LT_BATCH 2  // tiles per claim of the LOGITS producer
+#endif
 constexpr int LT_NC = SPC_LT_NC;     // consumer warps
 constexpr int LT_STAGE = LG_TR * 128;  // 128 rows x 128 bytes
 template <int D, int ALPHA>
@@ -390,7 +393,7 @@ __global__ void __launch_bounds__(32 * (LT_NC + 1), 1) logits_tma_kernel(
     // (its latency hides behind the current batch); the counter balances the SMs, whose
     // streaming rates differ (config E: 443 tiles per SM)
     if (lane == 0) {
-      constexpr int LT_BATCH = 2;
+      constexpr int LT_BATCH = SPC_LT_BATCH;
       int nt = 0;  // tiles handed to consumers
       int batch = (int)blockIdx.x;
       int next = (int)gridDim.x + (int)atomicAdd(ctr, 1u);

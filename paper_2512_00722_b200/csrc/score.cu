@@ -188,7 +188,7 @@ int launch_logits(const uint16_t* kr, const uint16_t* q, const int32_t* seq_len,
     SPC_TRY(smem_attr((const void*)logits_tma_kernel<D, ALPHA>, LtSmem<D, ALPHA>::BYTES));
     CUtensorMap map;
     SPC_TRY(make_tmap_tile_bf16(&map, kr, (uint64_t)B * G * Smax, D, LG_TR));
-    const int ncta = max(1, min(num_sms(), (ntiles + 1) / 2));
+    const int ncta = max(1, min(num_sms(), (ntiles + SPC_LT_BATCH - 1) / SPC_LT_BATCH));
     SPC_TRY(launched(launch_k(logits_tma_kernel<D, ALPHA>, dim3(ncta), dim3(32 * (LT_NC + 1)),
                               LtSmem<D, ALPHA>::BYTES, st, map, q, seq_len, G, Smax, scale, tpr,
                               ntiles, logits, tile_max, ctr)));

@@ -172,10 +172,14 @@ class DecodeStep:
         self.graphs = {}
 
     # ------------------------------------------------------------------ eager
-    def enqueue(self, parity: int, stream=None, q_ret=None, q_llm=None):
+    def enqueue(self, parity: int, stream=None, q_ret=None, q_llm=None, attend: bool = True,
+                q_score=None):
         """Enqueue one step writing the selection into idx[parity] (prev = idx[1-parity]).
         q_ret / q_llm: read the step's queries in place from these tensors instead of the
-        step's own input buffers."""
+        step's own input buffers.  attend=False stops after the selection and the diff (the
+        LLM decoder, llm.py, gathers and attends layer by layer between its dense layers).
+        q_score: score this query instead of q_ret (the front-end still writes q_ret and
+        appends its key; llm.py's trace-query benchmark mode)."""
         cur, prev = parity, 1 - parity
         q_ret = self.q_rets[parity] if q_ret is None else q_ret
         q_llm = self.q_llms[parity] if q_llm is None else q_llm
@@ -187,6 +191,8 @@ class DecodeStep:
             spc.rethead_qk(self.tokens[parity], f["emb"], f["norm_w"], f["eps"], f["w_qk"], f["inv"],
                            f["mscale"], None, self.Hq, self.G, q_ret, self.kr,
                            seq_len_out=self.seq_len, stream=stream)
+        if q_score is not None:
+            q_ret = q_score
         if self.one_launch:
             spc.score_select(q_ret, self.kr, self.seq_len, self.scale, self.k, self.head_max,
                              self.head_sumfix, self.gs, self.idx[cur], self.cnt[cur], self.idx[prev],
@@ -211,6 +217,8 @@ class DecodeStep:
             spc.elastic_diff(self.idx[prev], self.cnt[prev], self.idx[cur], self.cnt[cur],
                              self.load_tok, self.n_load, slot_tok=self.slot_tok,
                              load_slot=self.load_slot, stream=stream)
+        if not attend:
+            return
         if self.mode == "slots":
             main = torch.cuda.current_stream(self.dev) if stream is None else stream
             groups = self.layer_groups

@@ -33,7 +33,8 @@ EXPORTS = [
     "spc_mla_sparse_attn", "spc_decode_step_workspace", "spc_decode_step",
     "spc_kv_desc_bytes", "spc_kv_desc_init", "spc_sparse_decode_attn_kv",
     "spc_score_select_supported", "spc_score_select_workspace", "spc_score_select",
-    "spc_debug_build", "spc_check_device_errors",
+    "spc_debug_build", "spc_check_device_errors", "spc_llm_embed", "spc_llm_add_rmsnorm",
+    "spc_llm_rope_append", "spc_llm_swiglu", "spc_llm_f32_to_bf16", "spc_llm_argmax",
 ]
 
 
@@ -127,6 +128,12 @@ def load_library(path: str = LIB_PATH):
                                             i32, i32, f32, P, P, P, sz, P]
     L.spc_select.argtypes = [P, P, P, i32, i32, i32, i32, i32, i32, P, P, P, P, P, P, P, P, P, P,
                              P]
+    L.spc_llm_embed.argtypes = [P, P, i32, i32, i32, P, P]
+    L.spc_llm_add_rmsnorm.argtypes = [P, P, P, i32, i32, f32, P, P]
+    L.spc_llm_rope_append.argtypes = [P, P, P, i32, i32, i32, i32, i32, P, P, P, P, i32, P, P, P]
+    L.spc_llm_swiglu.argtypes = [P, i32, i32, P, P]
+    L.spc_llm_f32_to_bf16.argtypes = [P, ctypes.c_longlong, P, P]
+    L.spc_llm_argmax.argtypes = [P, i32, i32, P, P, P]
     for name in EXPORTS:  # every symbol must resolve (raises AttributeError otherwise)
         getattr(L, name)
     return L
@@ -447,3 +454,49 @@ def plan_step(thresholds, L: int, S: int, l_cpu: int):
     _check(lib().spc_plan_step(th.ctypes.data_as(ctypes.c_void_p), L, int(S), ctypes.byref(lc),
                                lay.ctypes.data_as(ctypes.c_void_p), ctypes.byref(n)), "spc_plan_step")
     return lc.value, lay[:n.value].tolist()
+
+
+# ---------------------------------------------------------------- LLM layer ops (NEXT-4)
+def llm_embed(token, emb, h, stream=None):
+    """spc_llm_embed: h [B][H] f32 = emb[token]."""
+    V, H = emb.shape
+    _check(lib().spc_llm_embed(_p(token), _p(emb), V, H, token.numel(), _p(h), _s(stream)),
+           "spc_llm_embed")
+
+
+def llm_add_rmsnorm(h, delta, w, eps: float, xn, stream=None):
+    """spc_llm_add_rmsnorm: h += delta (if given); xn = RMSNorm(h) * w (bf16)."""
+    B, H = h.shape
+    _check(lib().spc_llm_add_rmsnorm(_p(h), _p(delta), _p(w), B, H, float(eps), _p(xn),
+                                     _s(stream)), "spc_llm_add_rmsnorm")
+
+
+def llm_rope_append(qkv, inv_freq, seq_len, Hq: int, G: int, q_out, k_cache, v_cache,
+                    slot_tok=None, k_buf=None, v_buf=None, stream=None):
+    """spc_llm_rope_append: RoPE on q / k of the fused projection, append k / v at position
+    seq_len - 1 of the layer caches (and into the budget slot holding it, SLOTS mode).
+    k_cache / v_cache: [B][G][rows][D] (device or pinned host tensors)."""
+    B = qkv.shape[0]
+    D = q_out.shape[-1]
+    rows = k_cache.shape[2]
+    kb = 0 if slot_tok is None else slot_tok.shape[-1]
+    _check(lib().spc_llm_rope_append(_p(qkv), _p(inv_freq), _p(seq_len), B, Hq, G, D, rows,
+                                     _p(q_out), _p(k_cache), _p(v_cache), _p(slot_tok), kb,
+                                     _p(k_buf), _p(v_buf), _s(stream)), "spc_llm_rope_append")
+
+
+def llm_swiglu(gu, y, stream=None):
+    B, F2 = gu.shape
+    _check(lib().spc_llm_swiglu(_p(gu), B, F2 // 2, _p(y), _s(stream)), "spc_llm_swiglu")
+
+
+def llm_f32_to_bf16(x, y, stream=None):
+    assert x.numel() == y.numel()
+    _check(lib().spc_llm_f32_to_bf16(_p(x), x.numel(), _p(y), _s(stream)), "spc_llm_f32_to_bf16")
+
+
+def llm_argmax(logits, token_out, seq_len=None, stream=None):
+    """spc_llm_argmax: token_out = argmax(logits) per row (lowest index on ties); seq_len += 1."""
+    B, V = logits.shape
+    _check(lib().spc_llm_argmax(_p(logits), B, V, _p(token_out), _p(seq_len), _s(stream)),
+           "spc_llm_argmax")

@@ -152,3 +152,36 @@ def tokens(steps: int, B: int, V: int, seed: int, device="cpu") -> torch.Tensor:
     """Token ids [steps][B] int32, uniform over the vocabulary."""
     g = _gen(seed * 11 + 4, "cpu")
     return torch.randint(0, V, (steps, B), generator=g, dtype=torch.int32).to(device)
+
+
+# LLM decoder shape for NEXT-4 (DeepSeek-R1-Distill-Llama-8B = Llama-3.1-8B architecture)
+LLAMA8B = dict(L=32, H=4096, Hq=32, G=8, D=128, F=14336, V=128256, rope_base=500000.0, eps=1e-5)
+
+
+def llm_weights(L: int, H: int, Hq: int, G: int, D: int, F: int, V: int, seed: int,
+                device="cpu"):
+    """Random-init weights of a Llama-style decoder (NEXT-4; trained weights are out of scope,
+    DESIGN.md §5), nn.Linear layout [out][in], all bf16: emb [V][H] ~ N(0, 1); per layer
+    ln1 / ln2 [H] ~ 1 + N(0, 0.05^2), w_qkv [(Hq + 2G) D][H], w_o [H][Hq D], w_gu [2F][H]
+    (gate rows then up rows), w_down [H][F], each ~ N(0, 1/in); final norm [H]; lm_head [V][H]
+    ~ N(0, 1/H)."""
+    def lin(o, i, s):
+        return normal_bf16((o, i), s, device).mul_(1.0 / math.sqrt(i))
+
+    def norm(s):
+        return (1.0 + 0.05 * normal_bf16((H,), s, device, torch.float32)).to(torch.bfloat16)
+
+    base = seed * 13
+    w = dict(emb=normal_bf16((V, H), base + 1, device), ln1=[], ln2=[], w_qkv=[], w_o=[],
+             w_gu=[], w_down=[])
+    for l in range(L):
+        s = base + 100 * (l + 1)
+        w["ln1"].append(norm(s + 1))
+        w["ln2"].append(norm(s + 2))
+        w["w_qkv"].append(lin((Hq + 2 * G) * D, H, s + 3))
+        w["w_o"].append(lin(H, Hq * D, s + 4))
+        w["w_gu"].append(lin(2 * F, H, s + 5))
+        w["w_down"].append(lin(H, F, s + 6))
+    w["norm"] = norm(base + 2)
+    w["lm_head"] = lin(V, H, base + 3)
+    return w
