@@ -392,7 +392,7 @@ int spc_rethead_qk(const int32_t* token, const void* emb, int V, int H, const vo
  * attention (the per-layer dense compute that the KV prefetch
  * overlaps, Fig. 3 / P:199, "concurrent execution of computation and KV cache
  * prefetching").  A Llama-style layer (DeepSeek-R1-Distill-Llama-8B shape, random
- * weights, reading R28): x = RMSNorm(h); [q k v] = W_qkv x; RoPE(q, k); append k, v;
+ * weights, reading R30): x = RMSNorm(h); [q k v] = W_qkv x; RoPE(q, k); append k, v;
  * a = SparseAttn(q, selected K/V) (spc_sparse_decode_attn_kv); h += W_o a;
  * x = RMSNorm(h); h += W_down(silu(W_g x) * W_u x).  The projections are plain cuBLAS
  * GEMMs issued by the caller; these calls are the rest.  bf16 storage (raw uint16

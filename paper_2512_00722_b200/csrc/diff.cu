@@ -181,10 +181,8 @@ __global__ void __launch_bounds__(256) gather_kernel(
     const int32_t* __restrict__ load_slot, const int32_t* __restrict__ n_load,
     void* const* __restrict__ k_buf, void* const* __restrict__ v_buf) {
   spc_pdl_entry();
-  // grid: x = chunks of the budget, y = B*G row, z = layer
-  const int bg = blockIdx.y;
+  // grid: x = chunks of the budget, y strides over the B*G rows, z = layer
   const int l = layer_begin + blockIdx.z;
-  const int n = n_load[bg];
   const int lanes_per_row = row_vecs;  // 16-byte vectors per row (8 or 16)
   const int rows_per_block = blockDim.x / lanes_per_row;
   const int sub = threadIdx.x / lanes_per_row, lane = threadIdx.x % lanes_per_row;
@@ -192,18 +190,21 @@ __global__ void __launch_bounds__(256) gather_kernel(
   const VecT* vs = (const VecT*)v_src[l];
   VecT* kd = (VecT*)k_buf[l];
   VecT* vd = (VecT*)v_buf[l];
-  const size_t src_base = (size_t)bg * Smax * row_vecs, dst_base = (size_t)bg * kbud * row_vecs;
-  for (int i = blockIdx.x * rows_per_block + sub; i < n; i += gridDim.x * rows_per_block) {
-    const int t = load_tok[(size_t)bg * kbud + i];
-    const int s = load_slot[(size_t)bg * kbud + i];
+  for (int bg = blockIdx.y; bg < B * G; bg += gridDim.y) {
+    const int n = n_load[bg];
+    const size_t src_base = (size_t)bg * Smax * row_vecs, dst_base = (size_t)bg * kbud * row_vecs;
+    for (int i = blockIdx.x * rows_per_block + sub; i < n; i += gridDim.x * rows_per_block) {
+      const int t = load_tok[(size_t)bg * kbud + i];
+      const int s = load_slot[(size_t)bg * kbud + i];
 #ifdef SPC_DEBUG  // an index out of range is an error (skipped, not read)
-    SPC_DCHECK(t >= 0 && t < Smax && s >= 0 && s < kbud, SPC_E_RANGE);
-    if (t < 0 || t >= Smax || s < 0 || s >= kbud) continue;
+      SPC_DCHECK(t >= 0 && t < Smax && s >= 0 && s < kbud, SPC_E_RANGE);
+      if (t < 0 || t >= Smax || s < 0 || s >= kbud) continue;
 #endif
-    const VecT a = ks[src_base + (size_t)t * row_vecs + lane];
-    const VecT b = vs[src_base + (size_t)t * row_vecs + lane];
-    kd[dst_base + (size_t)s * row_vecs + lane] = a;
-    vd[dst_base + (size_t)s * row_vecs + lane] = b;
+      const VecT a = ks[src_base + (size_t)t * row_vecs + lane];
+      const VecT b = vs[src_base + (size_t)t * row_vecs + lane];
+      kd[dst_base + (size_t)s * row_vecs + lane] = a;
+      vd[dst_base + (size_t)s * row_vecs + lane] = b;
+    }
   }
 }
 
@@ -283,6 +284,19 @@ extern "C" int spc_elastic_diff(const int32_t* prev_idx, const int32_t* prev_cou
                            load_slot, n_load, evict_tok, n_evict));
 }
 
+// CTAs of one gather launch (env SPC_GATHER_CTAS overrides, tools): the strided gather
+// half the SMs (config D's prefetch groups, measured); the layer-major one 32 CTAs of 256
+// threads -- 256 KB of zero-copy loads in flight already reach the PCIe rate, and llm.py's
+// per-layer prefetch measured 8.69 ms serial / 5.65 ms overlapped at 32 CTAs vs 6.50 at 64
+// and 7.44 at 128 (the gather's CTAs take SMs from the dense layers it overlaps)
+static int gather_cap(int dflt) {
+  static const int cap_env = [] {
+    const char* e = std::getenv("SPC_GATHER_CTAS");
+    return e ? std::atoi(e) : 0;
+  }();
+  return cap_env > 0 ? cap_env : dflt;
+}
+
 extern "C" int spc_gather_kv(int dtype, const void* const* k_src, const void* const* v_src, int L,
                              int B, int G, int D, int Smax, int k, int layer_begin, int layer_end,
                              const int32_t* load_tok, const int32_t* load_slot,
@@ -297,7 +311,14 @@ extern "C" int spc_gather_kv(int dtype, const void* const* k_src, const void* co
   if (!esz) return SPC_E_UNSUPPORTED;
   if ((D * esz) % 16 || D * esz / 16 > 32 || 32 % (D * esz / 16)) return SPC_E_UNSUPPORTED;
   const int row_vecs = D * esz / 16;
-  dim3 grid((k + 63) / 64, B * G, layer_end - layer_begin);
+  // grid capped like the strided gather's (gather_cap): a PCIe-bound copy needs a few hundred
+  // KB in flight, not the whole GPU, and the rest of the SMs stay free for the compute it
+  // overlaps (DecodeStep's prefetch groups, llm.py's per-layer prefetch)
+  const int nl = layer_end - layer_begin;
+  const int cap = std::max(nl, gather_cap(32));
+  const int ny = std::max(1, std::min(B * G, cap / nl));
+  const int nx = std::max(1, std::min((k + 63) / 64, cap / (ny * nl)));
+  dim3 grid((unsigned)nx, (unsigned)ny, nl);
   return launched(launch_k(gather_kernel<uint4>, grid, dim3(256), 0, as_stream(stream), k_src,
                            v_src, B, G, Smax, k, row_vecs, layer_begin, load_tok, load_slot,
                            n_load, k_buf, v_buf));
@@ -322,11 +343,7 @@ extern "C" int spc_gather_kv_strided(int dtype, const void* const* k_src, const 
   // PCIe-bound: a few MB in flight saturate the link, so the grid is capped at half the SMs
   // in total -- the other half stays free for the attention of the previous layer group
   // (the prefetch pipeline of DecodeStep); env SPC_GATHER_CTAS overrides (tools)
-  static const int cap_env = [] {
-    const char* e = std::getenv("SPC_GATHER_CTAS");
-    return e ? std::atoi(e) : 0;
-  }();
-  const int cap = cap_env > 0 ? cap_env : std::max(1, num_sms() / 2);
+  const int cap = gather_cap(std::max(1, num_sms() / 2));
   const int nx = std::max(1, std::min((k + tpb - 1) / tpb, (cap + B * G - 1) / (B * G)));
   dim3 grid((unsigned)nx, B * G);
   return launched(launch_k(gather_strided_kernel, grid, dim3(GT_WARPS * 32), 0,

@@ -10,7 +10,7 @@ main stream computes layers 0..l-1: layer l waits only for its own gather event,
 PCIe transfer hides behind the weights-bound dense layers instead of serialising with them.
 
 Layer l (Llama-3 architecture, the DeepSeek-R1-Distill-Llama-8B shape; random weights,
-reading R28):
+reading R30):
     xn = RMSNorm(h; ln1)                          spc_llm_add_rmsnorm (adds the MLP delta)
     qkv = W_qkv xn                                cuBLAS (plain GEMM)
     q, k, v = RoPE(q), RoPE(k), v; append k, v    spc_llm_rope_append
@@ -33,7 +33,7 @@ from .pipeline import DecodeStep
 class LlmDecoder:
     def __init__(self, w: dict, cfg: dict, ret: dict, kr: torch.Tensor, k_cache, v_cache,
                  seq_len: torch.Tensor, k: int, kv: str = "resident", prefetch: bool = True,
-                 force_last: bool = True, trace_queries=None):
+                 force_last: bool = True, trace_queries=None, pf_priority: int = -1):
         """w: llm weights (synth.llm_weights).  cfg: L, H, Hq, G, D, F, V, rope_base, eps.
         ret: the retrieval head's front-end (emb, norm_w, w_qk, inv_freq [D/2] f32 device,
         mscale, Hq); kr [B][G][Smax][D] its key cache.  k_cache / v_cache: L tensors
@@ -72,7 +72,9 @@ class LlmDecoder:
                                  seq_len, L, Hq, k, mode="slots", kv_rows=k,
                                  k_src_layers=self.k_cache, v_src_layers=self.v_cache,
                                  force_last=force_last)
-            self._pf = torch.cuda.Stream(device=dev)
+            # the prefetch stream at high priority: its gathers' CTAs are scheduled ahead of
+            # the next dense kernel's whenever SMs free up
+            self._pf = torch.cuda.Stream(device=dev, priority=pf_priority)
             self._ev_sel = torch.cuda.Event()
             self._ev = [torch.cuda.Event() for _ in range(L)]
         self.st.set_frontend(ret["emb"], ret["norm_w"], ret["w_qk"], ret["inv_freq"],
