@@ -441,6 +441,10 @@ __global__ void __launch_bounds__(128) tma_merge_kernel(
   const size_t h = ((size_t)lr * B + b) * Hq + g * ALPHA + j;  // partial head index
   const size_t oh = ((size_t)(layer_begin + lr) * B + b) * Hq + g * ALPHA + j;
   const float* ml = part_ml + h * segstride * 2;
+  // lane p holds partial p's (m, l) (chunks of 32 partials); the partial outputs are then
+  // read 8 at a time with the weights broadcast by shuffles, so a group's np partials cost
+  // ~np/8 dependent L2 round trips (a per-partial loop cost ~0.5 us per partial: 16
+  // partials per group when one layer is attended per call, llm.py)
   float M = -INFINITY;
   for (int p = lane; p < np; p += 32) M = fmaxf(M, __ldcg(ml + 2 * p));
   M = warp_max(M);
@@ -448,22 +452,31 @@ __global__ void __launch_bounds__(128) tma_merge_kernel(
 #pragma unroll
   for (int i = 0; i < DPL; ++i) acc[i] = 0.f;
   float den = 0.f;
-  for (int p = 0; p < np; ++p) {
-    const float2 mlp = __ldcg(reinterpret_cast<const float2*>(ml) + p);
-    const float w = mlp.x == -INFINITY ? 0.f : exp2f(mlp.x - M);
-    den += w * mlp.y;
-    const float* po = part_o + (h * segstride + p) * D + lane * DPL;
-    if (DPL == 4) {
-      const float4 v = __ldcg(reinterpret_cast<const float4*>(po));
-      acc[0] += w * v.x;
-      acc[DPL > 1 ? 1 : 0] += w * v.y;
-      acc[DPL > 2 ? 2 : 0] += w * v.z;
-      acc[DPL > 3 ? 3 : 0] += w * v.w;
-    } else {
+  for (int p0 = 0; p0 < np; p0 += 32) {
+    const int n = min(32, np - p0);
+    float w = 0.f;
+    if (lane < n) {
+      const float2 mlp = __ldcg(reinterpret_cast<const float2*>(ml) + p0 + lane);
+      w = mlp.x == -INFINITY ? 0.f : exp2f(mlp.x - M);
+      den += w * mlp.y;
+    }
+    const float* po = part_o + (h * segstride + p0) * D + lane * DPL;
+#pragma unroll 8
+    for (int i = 0; i < n; ++i) {
+      const float wi = __shfl_sync(0xffffffffu, w, i);
+      if (DPL == 4) {
+        const float4 v = __ldcg(reinterpret_cast<const float4*>(po + (size_t)i * D));
+        acc[0] += wi * v.x;
+        acc[DPL > 1 ? 1 : 0] += wi * v.y;
+        acc[DPL > 2 ? 2 : 0] += wi * v.z;
+        acc[DPL > 3 ? 3 : 0] += wi * v.w;
+      } else {
 #pragma unroll
-      for (int i = 0; i < DPL; ++i) acc[i] += w * __ldcg(po + i);
+        for (int d = 0; d < DPL; ++d) acc[d] += wi * __ldcg(po + (size_t)i * D + d);
+      }
     }
   }
+  den = warp_sum(den);
   const float inv = den > 0.f ? 1.f / den : 0.f;
 #pragma unroll
   for (int i = 0; i < DPL; ++i) out[oh * D + lane * DPL + i] = acc[i] * inv;
