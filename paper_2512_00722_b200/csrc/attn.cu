@@ -277,6 +277,27 @@ extern "C" int spc_sparse_decode_attn(int dtype, const void* q, const void* cons
 
 extern "C" size_t spc_kv_desc_bytes(int L) { return L > 0 ? (size_t)2 * L * sizeof(CUtensorMap) : 0; }
 
+namespace spc {
+namespace {
+struct TmPart {
+  int n_groups, kpad, cpc, ncta;
+};
+TmPart tm_partition(int layer_begin, int layer_end, int B, int G, int k) {
+  TmPart p;
+  p.n_groups = (layer_end - layer_begin) * B * G;
+  p.kpad = (k + TM_RPS - 1) / TM_RPS * TM_RPS;
+  const long long v_total = (long long)p.n_groups * p.kpad;
+  const int ncta_target = TM_CTAS * num_sms();
+  long long rpc = (v_total + ncta_target - 1) / ncta_target;
+  rpc = (rpc + TM_RPS - 1) / TM_RPS * TM_RPS;
+  p.ncta = (int)((v_total + rpc - 1) / rpc);
+  p.cpc = (int)(rpc / TM_RPS);
+  return p;
+}
+
+}  // namespace
+}  // namespace spc
+
 extern "C" int spc_kv_desc_init(void* desc, const void* const* k_layers, const void* const* v_layers,
                                 int L, int B, int G, int D, int rows) {
   if (!desc || !k_layers || !v_layers) return SPC_E_NULL;
@@ -327,13 +348,9 @@ extern "C" int spc_sparse_decode_attn_kv(const void* kv_desc, const void* q, int
   if (!(D == 64 || D == 128) || !(alpha == 1 || alpha == 2 || alpha == 4 || alpha == 8))
     return SPC_E_UNSUPPORTED;
   AttnWs w = attn_ws_layout(ws, L, B, Hq, D, k);
-  const int n_groups = (layer_end - layer_begin) * B * G;
-  const int kpad = (k + TM_RPS - 1) / TM_RPS * TM_RPS;
-  const long long v_total = (long long)n_groups * kpad;
-  const int ncta_target = TM_CTAS * num_sms();
-  long long rpc = (v_total + ncta_target - 1) / ncta_target;
-  rpc = (rpc + TM_RPS - 1) / TM_RPS * TM_RPS;
-  const int ncta = (int)((v_total + rpc - 1) / rpc);
+  const TmPart part = tm_partition(layer_begin, layer_end, B, G, k);
+  const int n_groups = part.n_groups, kpad = part.kpad, ncta = part.ncta;
+  const long long rpc = (long long)part.cpc * TM_RPS;
   cudaStream_t st = as_stream(stream);
   const CUtensorMap* maps = (const CUtensorMap*)kv_desc;
 #define ATK(DD, AA)                                                                               \

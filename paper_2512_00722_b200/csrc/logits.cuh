@@ -285,12 +285,19 @@ __global__ void __launch_bounds__(256) lg_finalize_kernel(const float* __restric
 // by 16 KiB TMA boxes in 12.65 us per back-to-back launch vs 12.41 us for an LDG.128 stream
 // -- the consumers no longer spend issue slots on 16-byte copies.
 #ifndef SPC_LT_NC
-#define SPC_LT_NC 4
+#define SPC_LT_NC 8  // consumer warps
+#endif
+#ifndef SPC_LT_CPR
+#define SPC_LT_CPR 2  // consumer warps per ring: they split every stage's 128 rows
 #endif
 #ifndef SPC_LT_BATCH
 #define SPC_LT_BATCH 2  // tiles per claim of the LOGITS producer
 #endif
 constexpr int LT_NC = SPC_LT_NC;     // consumer warps
+constexpr int LT_CPR = SPC_LT_CPR;   // consumers per ring (= tile_max entries per tile)
+constexpr int LT_RINGS = LT_NC / LT_CPR;
+constexpr int LT_RPT = LG_RPT / LT_CPR;  // key rows per lane
+static_assert(LT_NC % LT_CPR == 0 && LT_RPT >= 2 && LT_RPT % 2 == 0, "LOGITS consumer split");
 constexpr int LT_STAGE = LG_TR * 128;  // 128 rows x 128 bytes
 template <int D, int ALPHA>
 struct LtSmem {
@@ -298,38 +305,38 @@ struct LtSmem {
   static constexpr int QRAW = ALPHA * D * 2;
   static constexpr int QF = D * ALPHA * 4;
   static constexpr int NST0 = (232448 - 2048 - LT_NC * QF) / (LT_STAGE + QRAW);
-  static constexpr int K = (NST0 > 12 ? 12 : NST0) / LT_NC;  // stages per consumer ring
-  static constexpr int NST = K * LT_NC;
+  static constexpr int K = (NST0 > 12 ? 12 : NST0) / LT_RINGS;  // stages per ring
+  static constexpr int NST = K * LT_RINGS;
   static_assert(K >= 1, "ring too shallow");
   static constexpr int QSLOT_OFF = NST * LT_STAGE;
   static constexpr int QF_OFF = QSLOT_OFF + NST * QRAW;
   static constexpr int BYTES = 1024 + QF_OFF + LT_NC * QF;
 };
 
-// O1 on one TMA stage (128 rows x 64 d, 128-byte swizzle): lane l accumulates rows
-// l + 32 r (r < LG_RPT) of the tile, alpha sequential fp32 chains per row, d ascending
-// (chunk c covers d = 64 c .. 64 c + 63), FFMA2 on row pairs with the query value as a
-// scalar-broadcast operand.  qf: the warp's fp32 [D][ALPHA] query table.
-template <int D, int ALPHA>
-__device__ __forceinline__ void lt_stage_math(float2 (&acc)[ALPHA][LG_RPT / 2], uint32_t kc,
-                                              uint32_t qf_s, const float* qf, int c, int lane) {
-  const uint32_t swz = (uint32_t)(lane & 7) << 4;
-  const uint32_t kl = kc + (uint32_t)lane * 128u;
+// O1 on RPT rows per lane of one TMA stage (128 rows x 64 d, 128-byte swizzle): lane l
+// accumulates rows row0 + l + 32 r (r < RPT; row0 a multiple of 32), alpha sequential fp32
+// chains per row, d ascending (chunk c covers d = 64 c .. 64 c + 63), FFMA2 on row pairs
+// with the query value as a scalar-broadcast operand.  qf: the warp's fp32 [D][ALPHA] table.
+template <int D, int ALPHA, int RPT>
+__device__ __forceinline__ void lt_rows_math(float2 (&acc)[ALPHA][RPT / 2], uint32_t kc, int row0,
+                                             uint32_t qf_s, const float* qf, int c, int lane) {
+  const uint32_t swz = (uint32_t)(lane & 7) << 4;  // granule g of row r sits at g ^ (r & 7)
+  const uint32_t kl = kc + (uint32_t)(row0 + lane) * 128u;
 #ifdef SPC_LT_NOMATH  // debug builds only: the load pipeline alone
   if (lane < 0)
 #endif
 #pragma unroll 2
     for (int u = 0; u < 8; ++u) {  // 16-byte granule = 8 consecutive d
-      uint4 w[LG_RPT];
+      uint4 w[RPT];
       const uint32_t ka = kl + (((uint32_t)u << 4) ^ swz);
 #pragma unroll
-      for (int r = 0; r < LG_RPT; ++r) w[r] = lds128(ka + r * 32 * 128);
+      for (int r = 0; r < RPT; ++r) w[r] = lds128(ka + r * 32 * 128);
       const uint32_t qd = qf_s + (uint32_t)(c * 64 + u * 8) * ALPHA * 4;
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
-        float2 kk[LG_RPT / 2];
+        float2 kk[RPT / 2];
 #pragma unroll
-        for (int p = 0; p < LG_RPT / 2; ++p) {
+        for (int p = 0; p < RPT / 2; ++p) {
           const uint32_t x0 = (&w[2 * p].x)[e >> 1], x1 = (&w[2 * p + 1].x)[e >> 1];
           kk[p] = (e & 1) ? make_float2(bf16hi(x0), bf16hi(x1)) : make_float2(bf16lo(x0), bf16lo(x1));
         }
@@ -338,7 +345,7 @@ __device__ __forceinline__ void lt_stage_math(float2 (&acc)[ALPHA][LG_RPT / 2], 
           if (ALPHA >= 4) {
             const float4 q4 = lds128f(qd + (uint32_t)(e * ALPHA + j) * 4);
 #pragma unroll
-            for (int p = 0; p < LG_RPT / 2; ++p) {
+            for (int p = 0; p < RPT / 2; ++p) {
               acc[j][p] = ffma2(kk[p], make_float2(q4.x, q4.x), acc[j][p]);
               acc[j + 1][p] = ffma2(kk[p], make_float2(q4.y, q4.y), acc[j + 1][p]);
               acc[j + 2][p] = ffma2(kk[p], make_float2(q4.z, q4.z), acc[j + 2][p]);
@@ -347,18 +354,24 @@ __device__ __forceinline__ void lt_stage_math(float2 (&acc)[ALPHA][LG_RPT / 2], 
           } else if (ALPHA == 2) {
             const float2 q2 = lds64f(qd + (uint32_t)(e * ALPHA) * 4);
 #pragma unroll
-            for (int p = 0; p < LG_RPT / 2; ++p) {
+            for (int p = 0; p < RPT / 2; ++p) {
               acc[0][p] = ffma2(kk[p], make_float2(q2.x, q2.x), acc[0][p]);
               acc[ALPHA - 1][p] = ffma2(kk[p], make_float2(q2.y, q2.y), acc[ALPHA - 1][p]);
             }
           } else {
             const float q1 = qf[c * 64 + u * 8 + e];
 #pragma unroll
-            for (int p = 0; p < LG_RPT / 2; ++p) acc[0][p] = ffma2(kk[p], make_float2(q1, q1), acc[0][p]);
+            for (int p = 0; p < RPT / 2; ++p) acc[0][p] = ffma2(kk[p], make_float2(q1, q1), acc[0][p]);
           }
         }
       }
     }
+}
+// all LG_RPT rows of a lane (score_select.cu's LOGITS phase)
+template <int D, int ALPHA>
+__device__ __forceinline__ void lt_stage_math(float2 (&acc)[ALPHA][LG_RPT / 2], uint32_t kc,
+                                              uint32_t qf_s, const float* qf, int c, int lane) {
+  lt_rows_math<D, ALPHA, LG_RPT>(acc, kc, 0, qf_s, qf, c, lane);
 }
 
 template <int D, int ALPHA>
@@ -368,6 +381,7 @@ __global__ void __launch_bounds__(32 * (LT_NC + 1), 1) logits_tma_kernel(
     float* __restrict__ logits, float* __restrict__ tile_max, unsigned* __restrict__ ctr) {
   using SM = LtSmem<D, ALPHA>;
   constexpr int NCH = SM::NCH, NST = SM::NST, K = SM::K;
+  constexpr int HROWS = LG_TR / LT_CPR;  // rows of a stage per consumer warp
   __shared__ __align__(8) uint64_t full[NST], empty[NST];
   __shared__ int stage_tile[NST];  // tile id of a tile's first stage (-1: end of the work)
   extern __shared__ __align__(16) uint8_t lt_raw[];
@@ -379,7 +393,7 @@ __global__ void __launch_bounds__(32 * (LT_NC + 1), 1) logits_tma_kernel(
   if (tid == 0) {
     for (int s = 0; s < NST; ++s) {
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(full0 + 8 * s));
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(empty0 + 8 * s));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(empty0 + 8 * s), "r"(LT_CPR));
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     prefetch_tmap(&kmap);
@@ -391,10 +405,11 @@ __global__ void __launch_bounds__(32 * (LT_NC + 1), 1) logits_tma_kernel(
     // tiles come in batches of LT_BATCH consecutive tiles: the CTA's first batch is static,
     // the next ones are claimed from one grid-wide counter, each claim issued a batch ahead
     // (its latency hides behind the current batch); the counter balances the SMs, whose
-    // streaming rates differ (config E: 443 tiles per SM)
+    // streaming rates differ (config E: 443 tiles per SM).  Tiles go to the LT_RINGS rings
+    // round robin; the LT_CPR consumers of a ring split each of its stages' rows
     if (lane == 0) {
       constexpr int LT_BATCH = SPC_LT_BATCH;
-      int nt = 0;  // tiles handed to consumers
+      int nt = 0;  // tiles handed to rings
       int batch = (int)blockIdx.x;
       int next = (int)gridDim.x + (int)atomicAdd(ctr, 1u);
       for (;;) {
@@ -405,13 +420,14 @@ __global__ void __launch_bounds__(32 * (LT_NC + 1), 1) logits_tma_kernel(
           if (tt * LG_TR >= __ldg(seq_len + bg / G)) {  // an empty tile (ragged batch)
             const int b = bg / G, g = bg - b * G;
             for (int j = 0; j < ALPHA; ++j)
-              tile_max[((size_t)b * Hq + g * ALPHA + j) * tpr + tt] = -INFINITY;
+              for (int hh = 0; hh < LT_CPR; ++hh)
+                tile_max[(((size_t)b * Hq + g * ALPHA + j) * tpr + tt) * LT_CPR + hh] = -INFINITY;
             continue;
           }
-          const int w = nt % LT_NC, n = nt / LT_NC;  // consumer warp and its tile count
+          const int w = nt % LT_RINGS, n = nt / LT_RINGS;  // ring and its tile count
           ++nt;
           for (int c = 0; c < NCH; ++c) {
-            const int j = n * NCH + c;  // sequence number in warp w's ring
+            const int j = n * NCH + c;  // sequence number in ring w
             const int s = w * K + j % K;
             if (j >= K) tm_wait(empty0 + 8 * s, ((j / K) - 1) & 1);
             const uint32_t fb = full0 + 8 * s;
@@ -435,9 +451,9 @@ __global__ void __launch_bounds__(32 * (LT_NC + 1), 1) logits_tma_kernel(
         batch = next;
         if (batch * LT_BATCH < ntiles) next = (int)gridDim.x + (int)atomicAdd(ctr, 1u);
       }
-      // end of the work: every consumer's next tile slot gets the end code
-      for (int w = 0; w < LT_NC; ++w) {
-        const int n = nt / LT_NC + (w < nt % LT_NC ? 1 : 0);  // tiles warp w received
+      // end of the work: every ring's next tile slot gets the end code
+      for (int w = 0; w < LT_RINGS; ++w) {
+        const int n = nt / LT_RINGS + (w < nt % LT_RINGS ? 1 : 0);  // tiles ring w received
         const int j = n * NCH, s = w * K + j % K;
         if (j >= K) tm_wait(empty0 + 8 * s, ((j / K) - 1) & 1);
         stage_tile[s] = -1;
@@ -447,22 +463,25 @@ __global__ void __launch_bounds__(32 * (LT_NC + 1), 1) logits_tma_kernel(
     return;
   }
   // -------------------------------------------------------------- consumers
-  // per-warp rings: every ring has one consumer that waits for every one of its stages
-  // in order, so a parity wait is never more than one phase ahead of its barrier
-  // (consumers sharing one ring and skipping each other's stages can alias phases)
+  // per-ring consumers: each waits for every stage of its ring in order, so a parity wait is
+  // never more than one phase ahead of its barrier (consumers skipping each other's stages
+  // could alias phases); the LT_CPR consumers of a ring take rows half*HROWS .. +HROWS of
+  // every stage, so two warps per scheduler hide each other's dependency stalls
+  const int ring = warp / LT_CPR, half = warp - ring * LT_CPR;
   float* qf = (float*)(basep + SM::QF_OFF + warp * SM::QF);
   const uint32_t qf_s = smem_u32(qf);
+  int qf_bg = -1;  // group whose query qf holds (consecutive tiles are mostly one group's)
   for (int n = 0;; ++n) {
     int tile = 0, bg = 0, t0 = 0, b = 0, g = 0, S = 0;
-    float2 acc[ALPHA][LG_RPT / 2];
+    float2 acc[ALPHA][LT_RPT / 2];
 #pragma unroll
     for (int j = 0; j < ALPHA; ++j)
 #pragma unroll
-      for (int p = 0; p < LG_RPT / 2; ++p) acc[j][p] = make_float2(0.f, 0.f);
+      for (int p = 0; p < LT_RPT / 2; ++p) acc[j][p] = make_float2(0.f, 0.f);
     bool done = false;
     for (int c = 0; c < NCH; ++c) {
       const int j = n * NCH + c;
-      const int s = warp * K + j % K;
+      const int s = ring * K + j % K;
       tm_wait(full0 + 8 * s, (j / K) & 1);
       if (c == 0) {
         tile = stage_tile[s];
@@ -475,30 +494,34 @@ __global__ void __launch_bounds__(32 * (LT_NC + 1), 1) logits_tma_kernel(
         b = bg / G;
         g = bg - b * G;
         S = __ldg(seq_len + b);
-        // raw [ALPHA][D] bf16 -> fp32 [D][ALPHA]
-        const uint16_t* qr = (const uint16_t*)(basep + SM::QSLOT_OFF + s * SM::QRAW);
-        for (int e = lane; e < ALPHA * D; e += 32) {
-          const int jj = e / D, d = e - jj * D;
-          qf[d * ALPHA + jj] = __uint_as_float((uint32_t)qr[e] << 16);
+        if (bg != qf_bg) {  // raw [ALPHA][D] bf16 -> fp32 [D][ALPHA]
+          qf_bg = bg;
+          const uint16_t* qr = (const uint16_t*)(basep + SM::QSLOT_OFF + s * SM::QRAW);
+#pragma unroll 4
+          for (int e = lane; e < ALPHA * D; e += 32) {
+            const int jj = e / D, d = e - jj * D;
+            qf[d * ALPHA + jj] = __uint_as_float((uint32_t)qr[e] << 16);
+          }
+          __syncwarp();
         }
-        __syncwarp();
       }
-      lt_stage_math<D, ALPHA>(acc, base + s * LT_STAGE, qf_s, qf, c, lane);
+      lt_rows_math<D, ALPHA, LT_RPT>(acc, base + s * LT_STAGE, half * HROWS, qf_s, qf, c, lane);
       __syncwarp();
-      if (lane == 0) tm_arrive(empty0 + 8 * s);  // stage consumed
+      if (lane == 0) tm_arrive(empty0 + 8 * s);  // this warp's share of the stage is consumed
     }
     if (done) break;
-    // O1 final multiply by scale, store, O2 tile max -> tile_max
+    // O1 final multiply by scale, store, O2 maximum of this warp's rows -> tile_max
     float tm = 0.0f;
 #pragma unroll
     for (int j = 0; j < ALPHA; ++j) {
-      float* o = logits + ((size_t)b * Hq + g * ALPHA + j) * Smax + t0;
+      float* o = logits + ((size_t)b * Hq + g * ALPHA + j) * Smax + t0 + half * HROWS;
       float m = -INFINITY;
 #pragma unroll
-      for (int r = 0; r < LG_RPT; ++r) {  // row lane + 32 r = pair r/2, half r%2
+      for (int r = 0; r < LT_RPT; ++r) {  // row lane + 32 r = pair r/2, half r%2
         const int row = lane + 32 * r;
+        const int tok = t0 + half * HROWS + row;
         const float sv = __fmul_rn((r & 1) ? acc[j][r >> 1].y : acc[j][r >> 1].x, scale);
-        if (t0 + row < S && t0 + row < Smax) {
+        if (tok < S && tok < Smax) {
           SPC_DCHECK(sv == sv, SPC_E_RANGE);  // NaN key / query (reading R20)
           o[row] = sv;
           m = fmaxf(m, sv);
@@ -507,6 +530,7 @@ __global__ void __launch_bounds__(32 * (LT_NC + 1), 1) logits_tma_kernel(
       m = warp_max(m);
       if (lane == j) tm = m;
     }
-    if (lane < ALPHA) tile_max[((size_t)b * Hq + g * ALPHA + lane) * tpr + (tile - bg * tpr)] = tm;
+    if (lane < ALPHA)
+      tile_max[(((size_t)b * Hq + g * ALPHA + lane) * tpr + (tile - bg * tpr)) * LT_CPR + half] = tm;
   }
 }

@@ -184,7 +184,9 @@ int launch_logits(const uint16_t* kr, const uint16_t* q, const int32_t* seq_len,
   const int tpr = (Smax + LG_TR - 1) / LG_TR;
   const int ntiles = B * G * tpr;
   const int nh = B * G * ALPHA;
+  int tm_per_head = tpr;  // tile_max entries per head (the TMA kernel: one per consumer split)
   if ((long long)B * G * Smax < (1ll << 31)) {  // TMA-fed kernel (int32 row coordinates)
+    tm_per_head = tpr * LT_CPR;
     SPC_TRY(smem_attr((const void*)logits_tma_kernel<D, ALPHA>, LtSmem<D, ALPHA>::BYTES));
     CUtensorMap map;
     SPC_TRY(make_tmap_tile_bf16(&map, kr, (uint64_t)B * G * Smax, D, LG_TR));
@@ -202,7 +204,7 @@ int launch_logits(const uint16_t* kr, const uint16_t* q, const int32_t* seq_len,
                              tile_max, ctr)));
   }
   return launched(launch_k(lg_finalize_kernel, dim3(nh), dim3(256), 0, st,
-                           (const float*)tile_max, tpr, nh, head_max, ctr));
+                           (const float*)tile_max, tm_per_head, nh, head_max, ctr));
 }
 
 // GROUP with float4 accesses (Smax % 4 == 0): a thread takes 4 consecutive tokens, one
@@ -291,7 +293,7 @@ ScoreWs score_ws_layout(void* ws, int B, int Hq, int Smax) {
   ScoreWs w;
   size_t off = 0;
   w.tile_max = (float*)(p + off);
-  off = align_up(off + sizeof(float) * B * Hq * ((Smax + LG_TR - 1) / LG_TR), 256);
+  off = align_up(off + sizeof(float) * B * Hq * ((Smax + LG_TR - 1) / LG_TR) * LT_CPR, 256);
   w.lg_ctr = (unsigned*)(p + off);
   off = align_up(off + sizeof(unsigned) * 2, 256);
   w.tile_sum = (long long*)(p + off);

@@ -35,6 +35,9 @@ namespace cg = cooperative_groups;
 namespace spc {
 namespace {
 
+#ifndef SPC_SEL_SCL
+#define SPC_SEL_SCL 8
+#endif
 constexpr int ST = 512;         // threads per CTA
 constexpr int SEGCAP = 16896;   // tokens per CTA segment: rows up to 8 * SEGCAP = 135168
 // SCL (template parameter) = CTAs per row = cluster size; 8.  (16-CTA non-portable
@@ -50,8 +53,8 @@ __device__ unsigned long long* g_sel_trace = nullptr;
 __device__ __forceinline__ void sel_mark(int slot) {
 #ifdef SPC_TRACE
   if (g_sel_trace && blockIdx.y < 64 && threadIdx.x == 0 && slot < 16) {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    unsigned long long t;  // SM clock cycles (compare marks of one CTA only)
+    asm volatile("mov.u64 %0, %clock64;" : "=l"(t));
     g_sel_trace[(blockIdx.y * gridDim.x + blockIdx.x) * 16 + slot] = t;
   }
 #else
@@ -59,20 +62,84 @@ __device__ __forceinline__ void sel_mark(int slot) {
 #endif
 }
 
+constexpr int MAXPASS = 8;  // radix passes: pass 0 fixes 12 key bits, each later one 8 more
+constexpr int BAR_NORM = 0, BAR_X = 1, BAR_H = 2;  // mbarriers: NORM, candidates, pass p = BAR_H + p
+
+// ---- DSMEM exchanges without cluster barriers.  A sender writes with remote st.async /
+// red.async whose bytes complete the destination CTA's mbarrier (complete_tx) and arrives
+// once on that mbarrier with the byte count it sends (arrive.expect_tx, relaxed: no fence
+// that would wait for this CTA's outstanding global stores, as barrier.cluster.arrive's
+// release does); the receiver waits for the phase (acquire, cluster scope), i.e. until every
+// sender's bytes have landed.  Every mbarrier is used for one phase per launch (parity 0).
+__device__ __forceinline__ uint32_t dsm_map(uint32_t a, int rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void dsm_st64(uint32_t ra, unsigned long long v, uint32_t rbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(ra),
+               "l"(v), "r"(rbar)
+               : "memory");
+}
+__device__ __forceinline__ void dsm_st32(uint32_t ra, uint32_t v, uint32_t rbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];" ::"r"(ra),
+               "r"(v), "r"(rbar)
+               : "memory");
+}
+__device__ __forceinline__ void dsm_st128(uint32_t ra, uint4 v, uint32_t rbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(
+                   ra),
+               "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w), "r"(rbar)
+               : "memory");
+}
+__device__ __forceinline__ void dsm_red_add(uint32_t ra, uint32_t v, uint32_t rbar) {
+  asm volatile(
+      "red.async.relaxed.cluster.shared::cluster.mbarrier::complete_tx::bytes.add.u32 [%0], %1, [%2];" ::"r"(
+          ra),
+      "r"(v), "r"(rbar)
+      : "memory");
+}
+__device__ __forceinline__ void dsm_expect(uint32_t rbar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.relaxed.cluster.shared::cluster.b64 _, [%0], %1;" ::"r"(rbar),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void dsm_wait(uint32_t bar) {
+  const long long t0 = clock64();
+  for (;;) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.test_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], 0;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(bar)
+        : "memory");
+    if (ok) return;
+    if (clock64() - t0 > 8000000000ll) __trap();  // ~4 s: a lost exchange fails loudly
+  }
+}
+
+
 template <int SCL>
 struct SelSm {
   float seg[SEGCAP];                      // group scores of this CTA's segment
   uint32_t bm_prev[SEGCAP / 32];          // previous selection, segment-relative bitmap
-  unsigned long long cand[SCL][CANDMAX];  // threshold bucket, pushed by every rank
-  uint8_t candp[SCL][CANDMAX];            // ... and whether each was previously selected
+  uint4 cand[SCL][CANDMAX];               // threshold bucket, pushed by every rank: key (lo, hi),
+                                          // origin thread | previously selected << 16, 0
+  unsigned long long flat[CANDMAX];       // the bucket of the whole row, flattened
+  uint32_t flati[CANDMAX];                // ... origin thread | previously selected << 16 | rank << 17
+  uint64_t bar[BAR_H + MAXPASS];          // exchange mbarriers
   unsigned hist[NB];                      // this CTA's histogram of the current pass
-  unsigned red[2][NB];                    // cluster sums (pushed by every rank), ping-pong
+  unsigned rx[2][SCL][NB];                // pass p: every rank's histogram (ping-pong by p & 1)
   long long part[SCL][8];                 // NORM partial sums pushed by every rank
   long long wred[ST / 32][8];             // NORM warp partials
+  long long ntot[8];                      // this CTA's NORM partials
   unsigned long long stats[SCL];          // per rank: above | above&prev | bucket | bucket&prev
   unsigned long long my_stats;
   unsigned long long wsc[ST / 32];        // scan scratch
   unsigned wfind[NB / 32];
+  unsigned short xsel[ST], xnew[ST];      // per thread: its bucket tokens selected (and new)
   int candn[SCL];                         // bucket elements pushed by every rank
   int lpre[3];                            // previous tokens < s0, < s1, < len
   int csel[SCL], cselp[SCL];              // selected bucket elements per rank (& previous)
@@ -81,11 +148,6 @@ struct SelSm {
   unsigned long long T;
   unsigned long long total;
 };
-
-// composite key of token p given its group-score bits
-__device__ __forceinline__ unsigned long long key_of(uint32_t vb, int p, int len, int force) {
-  return composite((force && p == len - 1) ? 0x7F800000u : vb, p);
-}
 
 // Block-wide exclusive scan of one uint64 per thread (ST threads).
 template <int SCL>
@@ -114,28 +176,36 @@ __device__ __forceinline__ unsigned long long scan_u64(SelSm<SCL>& s, unsigned l
   return s.wsc[warp] + incl - v;
 }
 
-// Push the nonzero bins of the local histogram into red[buf] of every CTA.
+// Histogram exchange of pass `pass`: this CTA's whole histogram (1 KiB, zeros included)
+// goes to slot `rank` of rx[pass & 1] in every CTA as 16-byte st.async (64 per destination:
+// DSMEM issue, not bytes, is the limit -- 2048 per-bin remote atomics cost ~1 us), completing
+// the destination's pass mbarrier, whose byte count (SCL KiB) every receiver expects itself.
+// Ping-pong is safe: a rank sends pass p + 2 only after pass p + 1 completed, which needs
+// every rank's pass p + 1 data, sent after that rank's find_bin of pass p.
 template <int SCL>
-__device__ __forceinline__ void push_hist(SelSm<SCL>& s, cg::cluster_group& cl, int buf) {
+__device__ __forceinline__ void exchange_hist(SelSm<SCL>& s, int rank, int pass) {
   const int t = threadIdx.x;
-  if (t < NB) {
-    const unsigned h = s.hist[t];
-    if (h) {
+  const uint32_t bar = smem_u32(&s.bar[BAR_H + pass]);
+  if (t == 0) tm_expect(bar, (uint32_t)(SCL * NB * 4));
+  if (t < NB / 4) {
+    const uint4 v = reinterpret_cast<const uint4*>(s.hist)[t];
+    const uint32_t a = smem_u32(&s.rx[pass & 1][rank][4 * t]);
 #pragma unroll
-      for (int q = 0; q < SCL; ++q) atomicAdd(cl.map_shared_rank(&s.red[buf][t], q), h);
-    }
+    for (int q = 0; q < SCL; ++q) dsm_st128(dsm_map(a, q), v, dsm_map(bar, q));
   }
+  dsm_wait(bar);
 }
 
-// After the cluster barrier: bin of the r-th largest element counted from the top of
-// red[buf] -> s.find = {bin, count above it, count in it}.  Clears red[buf].
+// After exchange_hist: bin of the r-th largest element counted from the top of the pass's
+// cluster histogram -> s.find = {bin, count above it, count in it}.
 template <int SCL>
-__device__ __forceinline__ void find_bin(SelSm<SCL>& s, int buf, int r) {
+__device__ __forceinline__ void find_bin(SelSm<SCL>& s, int pass, int r) {
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   unsigned c = 0, incl = 0;
   if (t < NB) {
-    c = s.red[buf][NB - 1 - t];  // thread t holds bin NB-1-t: ascending t = descending bins
-    s.red[buf][NB - 1 - t] = 0u;
+    const int bin = NB - 1 - t;  // ascending t = descending bins
+#pragma unroll
+    for (int q = 0; q < SCL; ++q) c += s.rx[pass & 1][q][bin];
     incl = c;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -170,8 +240,7 @@ __global__ void __launch_bounds__(ST, 1) select_kernel(
   spc_pdl_entry();
   extern __shared__ __align__(16) uint8_t sel_raw[];
   SelSm<SCL>& s = *reinterpret_cast<SelSm<SCL>*>(sel_raw);
-  cg::cluster_group cl = cg::this_cluster();
-  const int rank = (int)cl.block_rank();
+  const int rank = (int)cg::this_cluster().block_rank();
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int bg = blockIdx.y, b = bg / G, g = bg - b * G;
   const int Hq = G * ALPHA;
@@ -179,16 +248,16 @@ __global__ void __launch_bounds__(ST, 1) select_kernel(
   const int need = min(k, len);
   const int per = ((len + SCL - 1) / SCL + 3) & ~3;
   const int s0 = min(len, rank * per), s1 = min(len, s0 + per);
-  const int nch = (s1 - s0 + 3) >> 2;  // float4 chunks of the segment
+  const int nseg = s1 - s0;
+  const int nch = (nseg + 3) >> 2;  // float4 chunks of the segment
   // this thread's tokens: the contiguous chunks [c0, c1) (ordered output needs only a scan)
   const int cpt = max(1, (nch + ST - 1) / ST);
   const int c0 = min(nch, tid * cpt), c1 = min(nch, c0 + cpt);
   const float* lg = logits + ((size_t)b * Hq + g * ALPHA) * Smax + s0;
   const int np = min(max(prev_count[bg], 0), k);
   const int32_t* pv = prev_idx + (size_t)bg * k;
-  // every CTA of the cluster must have started before any remote shared-memory write (the
-  // NORM partials below): arrive now, wait right before the first push (hidden latency)
-  cl.barrier_arrive();
+  // the newest token counts as +inf when forced (R10): its group-score bits are replaced
+  const int tforce = force ? len - 1 - s0 : -1;  // segment-relative, or out of range
   sel_mark(0);
 
   // ---- prologue: logits of the first NC chunks and the previous selection in flight
@@ -213,41 +282,25 @@ __global__ void __launch_bounds__(ST, 1) select_kernel(
   float m[ALPHA];
 #pragma unroll
   for (int j = 0; j < ALPHA; ++j) m[j] = head_max[(size_t)b * Hq + g * ALPHA + j];
-  const int nw = (s1 - s0 + 31) >> 5;
+  const int nw = (nseg + 31) >> 5;
   for (int i = tid; i < nw; i += ST) s.bm_prev[i] = 0u;
-  if (tid < NB) {
-    s.hist[tid] = 0u;
-    s.red[0][tid] = 0u;
-    s.red[1][tid] = 0u;
-  }
+  if (tid < NB) s.hist[tid] = 0u;
+  s.xsel[tid] = 0;
+  s.xnew[tid] = 0;
   if (tid < 3) s.lpre[tid] = 0;
   if (tid < SCL) s.csel[tid] = s.cselp[tid] = 0;
   if (tid == 0) {
     s.ncand = 0;
     s.my_stats = 0ull;
+    for (int i = 0; i < BAR_H + MAXPASS; ++i)  // histogram passes: one local arrive (expect)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&s.bar[i])),
+                   "r"(i < BAR_H ? SCL : 1));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  {  // bitmap of the previous tokens in this segment; prefix counts of the sorted list
-    int c_s0 = 0, c_s1 = 0, c_len = 0;
-#pragma unroll
-    for (int i = 0; i < PVR; ++i) {
-      const int t = pvr[i];
-      if (t >= 0) {
-        if (t >= s0 && t < s1) atomicOr(&s.bm_prev[(t - s0) >> 5], 1u << ((t - s0) & 31));
-        c_s0 += t < s0;
-        c_s1 += t < s1;
-        c_len += t < len;
-      }
-    }
-    c_s0 = __reduce_add_sync(0xffffffffu, c_s0);
-    c_s1 = __reduce_add_sync(0xffffffffu, c_s1);
-    c_len = __reduce_add_sync(0xffffffffu, c_len);
-    if (lane == 0) {
-      if (c_s0) atomicAdd(&s.lpre[0], c_s0);
-      if (c_s1) atomicAdd(&s.lpre[1], c_s1);
-      if (c_len) atomicAdd(&s.lpre[2], c_len);
-    }
-  }
+  // every CTA of the cluster must be initialised (zeroed sums, mbarriers) before any remote
+  // write into it: arrive now (release), wait right before the first send
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
   sel_mark(10);
 
   // ---- NORM (O3, O4)
@@ -265,7 +318,7 @@ __global__ void __launch_bounds__(ST, 1) select_kernel(
       const float es[4] = {ea.x, ea.y, eb.x, eb.y};
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
-        const float e = (c0 + u < c1 && p0 + c < s1 - s0) ? es[c] : 0.0f;
+        const float e = (c0 + u < c1 && p0 + c < nseg) ? es[c] : 0.0f;
         e0[u][j][c] = e;
         acc[j] += fixpoint40(e);
       }
@@ -290,7 +343,7 @@ __global__ void __launch_bounds__(ST, 1) select_kernel(
         const float es[4] = {ea.x, ea.y, eb.x, eb.y};
 #pragma unroll
         for (int c = 0; c < 4; ++c)
-          if (ch + u < c1 && 4 * (ch + u) + c < s1 - s0) acc[j] += fixpoint40(es[c]);
+          if (ch + u < c1 && 4 * (ch + u) + c < nseg) acc[j] += fixpoint40(es[c]);
       }
   }
   sel_mark(11);
@@ -300,16 +353,46 @@ __global__ void __launch_bounds__(ST, 1) select_kernel(
     if (lane == 0) s.wred[warp][j] = v;
   }
   __syncthreads();
-  cl.barrier_wait();
-  if (tid < ALPHA) {
-    long long t = 0;
+  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+  if (warp == 0) {  // this CTA's partial of head j to every rank q
+    if (lane < ALPHA) {
+      long long t = 0;
 #pragma unroll
-    for (int w = 0; w < ST / 32; ++w) t += s.wred[w][tid];
-#pragma unroll
-    for (int q = 0; q < SCL; ++q) cl.map_shared_rank(&s.part[0][0], q)[rank * 8 + tid] = t;
+      for (int w = 0; w < ST / 32; ++w) t += s.wred[w][lane];
+      s.ntot[lane] = t;
+    }
+    const uint32_t bar = smem_u32(&s.bar[BAR_NORM]);
+    if (lane < SCL) dsm_expect(dsm_map(bar, lane), 8u * ALPHA);
+    __syncwarp();
+    const uint32_t a = smem_u32(&s.part[rank][0]);
+    for (int i = lane; i < ALPHA * SCL; i += 32) {
+      const int j = i % ALPHA, q = i / ALPHA;
+      dsm_st64(dsm_map(a + 8u * j, q), (unsigned long long)s.ntot[j], dsm_map(bar, q));
+    }
   }
   sel_mark(12);
-  cl.sync();
+  {  // meanwhile: bitmap of the previous tokens in this segment; prefix counts of the list
+    int c_s0 = 0, c_s1 = 0, c_len = 0;
+#pragma unroll
+    for (int i = 0; i < PVR; ++i) {
+      const int t = pvr[i];
+      if (t >= 0) {
+        if (t >= s0 && t < s1) atomicOr(&s.bm_prev[(t - s0) >> 5], 1u << ((t - s0) & 31));
+        c_s0 += t < s0;
+        c_s1 += t < s1;
+        c_len += t < len;
+      }
+    }
+    c_s0 = __reduce_add_sync(0xffffffffu, c_s0);
+    c_s1 = __reduce_add_sync(0xffffffffu, c_s1);
+    c_len = __reduce_add_sync(0xffffffffu, c_len);
+    if (lane == 0) {
+      if (c_s0) atomicAdd(&s.lpre[0], c_s0);
+      if (c_s1) atomicAdd(&s.lpre[1], c_s1);
+      if (c_len) atomicAdd(&s.lpre[2], c_len);
+    }
+  }
+  dsm_wait(smem_u32(&s.bar[BAR_NORM]));
   sel_mark(1);
 
   // ---- GROUP (O4..O6) + pass-0 histogram
@@ -328,6 +411,10 @@ __global__ void __launch_bounds__(ST, 1) select_kernel(
   const int base0 = top - (NB - 1);
   float* gso = group_score + (size_t)bg * Smax + s0;
   const bool cut = need < len;
+  auto bin0_of = [&](float v, int p) {  // pass-0 bin of segment token p (force: +inf)
+    const uint32_t vb = p == tforce ? 0x7F800000u : __float_as_uint(v);
+    return min(max((int)(vb >> W0_SHIFT) - base0, 0), NB - 1);
+  };
 #pragma unroll
   for (int u = 0; u < NC; ++u) {
     const int ch = c0 + u;
@@ -340,10 +427,7 @@ __global__ void __launch_bounds__(ST, 1) select_kernel(
         for (int j = 1; j < ALPHA; ++j) v = fmaxf(v, __fmul_rn(e0[u][j][c], r[j]));
         gs[c] = v;
         const int p = 4 * ch + c;
-        if (cut && p < s1 - s0) {
-          const unsigned long long key = key_of(__float_as_uint(v), s0 + p, len, force);
-          atomicAdd(&s.hist[min(max((int)(key >> 52) - base0, 0), NB - 1)], 1u);
-        }
+        if (cut && p < nseg) atomicAdd(&s.hist[bin0_of(v, p)], 1u);
       }
       const float4 o = make_float4(gs[0], gs[1], gs[2], gs[3]);
       reinterpret_cast<float4*>(s.seg)[ch] = o;
@@ -370,7 +454,7 @@ __global__ void __launch_bounds__(ST, 1) select_kernel(
         const float2 eb = spc_exp2_dev(__fsub_rn(x[u][j].z, m[j]), __fsub_rn(x[u][j].w, m[j]));
         const float es[4] = {ea.x, ea.y, eb.x, eb.y};
 #pragma unroll
-        for (int c = 0; c < 4; ++c) e[j][c] = 4 * ch + c < s1 - s0 ? es[c] : 0.0f;
+        for (int c = 0; c < 4; ++c) e[j][c] = 4 * ch + c < nseg ? es[c] : 0.0f;
       }
       float gs[4];
 #pragma unroll
@@ -380,10 +464,7 @@ __global__ void __launch_bounds__(ST, 1) select_kernel(
         for (int j = 1; j < ALPHA; ++j) v = fmaxf(v, __fmul_rn(e[j][c], r[j]));
         gs[c] = v;
         const int p = 4 * ch + c;
-        if (cut && p < s1 - s0) {
-          const unsigned long long key = key_of(__float_as_uint(v), s0 + p, len, force);
-          atomicAdd(&s.hist[min(max((int)(key >> 52) - base0, 0), NB - 1)], 1u);
-        }
+        if (cut && p < nseg) atomicAdd(&s.hist[bin0_of(v, p)], 1u);
       }
       const float4 o = make_float4(gs[0], gs[1], gs[2], gs[3]);
       reinterpret_cast<float4*>(s.seg)[ch] = o;
@@ -398,16 +479,19 @@ __global__ void __launch_bounds__(ST, 1) select_kernel(
   __syncthreads();
   sel_mark(2);
 
-  // ---- top-k (O7): selected = {key >= T}; counts of selected tokens (and of those that
-  // were previously selected) in the ranks before this one (b_) and in the row (a_)
+  // ---- top-k (O7): selected = {key >= T}, key = composite(group-score bits, id).  Per thread:
+  // nsel / nnew = its selected / newly selected tokens, nwas = its previously selected ones
   unsigned long long T = 0ull;
   int b_sel = 0, b_selp = 0, a_sel = 0, a_selp = 0;
+  int nsel = 0, nnew = 0, nwas = 0;
   if (cut) {
-    push_hist(s, cl, 0);
-    cl.sync();
+    sel_mark(13);
+    exchange_hist(s, rank, 0);
+    sel_mark(14);
     find_bin(s, 0, need);
     const int bin0 = s.find[0];
     int rr = need - s.find[1], cm = s.find[2];
+    // the threshold bucket = keys in [klo, khi]; everything above khi is selected
     unsigned long long P = 0ull, xlo = 0ull, xmax = ~0ull;
     int bits = 1;  // key bit 63 (sign of the value) is always 0
     if (bin0 == 0) {
@@ -419,10 +503,12 @@ __global__ void __launch_bounds__(ST, 1) select_kernel(
       bits = W0_BITS;
     }
     sel_mark(3);
-    int buf = 1;
-    while (cm != rr && cm > CANDMAX) {
+    for (int pass = 1; cm != rr && cm > CANDMAX; ++pass) {  // rare: resolve 8 more key bits
       const int db = min(8, 64 - bits), sh = 64 - bits - db;
       const unsigned mask = (1u << db) - 1u;
+      const unsigned long long plo = P > xlo ? P : xlo;
+      const unsigned long long phi_ = P | (bits >= 64 ? 0ull : ~0ull >> bits);
+      const unsigned long long phi = phi_ < xmax ? phi_ : xmax;
       if (tid < NB) s.hist[tid] = 0u;
       __syncthreads();
       for (int ch = c0; ch < c1; ++ch) {
@@ -431,28 +517,28 @@ __global__ void __launch_bounds__(ST, 1) select_kernel(
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
           const int p = 4 * ch + c;
-          if (p < s1 - s0) {
-            const unsigned long long x = key_of(__float_as_uint(vs[c]), s0 + p, len, force);
-            if ((x >> (64 - bits)) == (P >> (64 - bits)) && x >= xlo && x <= xmax)
-              atomicAdd(&s.hist[(unsigned)(x >> sh) & mask], 1u);
+          if (p < nseg) {
+            const uint32_t vb = p == tforce ? 0x7F800000u : __float_as_uint(vs[c]);
+            const unsigned long long x = composite(vb, s0 + p);
+            if (x >= plo && x <= phi) atomicAdd(&s.hist[(unsigned)(x >> sh) & mask], 1u);
           }
         }
       }
       __syncthreads();
-      push_hist(s, cl, buf);
-      cl.sync();
-      find_bin(s, buf, rr);
+      exchange_hist(s, rank, pass);
+      find_bin(s, pass, rr);
       rr -= s.find[1];
       cm = s.find[2];
       P |= (unsigned long long)s.find[0] << sh;
       bits += db;
-      buf ^= 1;
     }
     sel_mark(4);
-    // this CTA's counts of tokens above the bucket / in it (each also & previous); the
-    // bucket itself is pushed to every CTA unless it is selected whole (cm == rr)
+    const unsigned long long phi_ = P | (bits >= 64 ? 0ull : ~0ull >> bits);
+    const unsigned long long klo = P > xlo ? P : xlo, khi = phi_ < xmax ? phi_ : xmax;
+    // classification: tokens above the bucket and in it (each also & previous); the bucket
+    // itself is pushed to every CTA unless it is selected whole (cm == rr)
     const bool xchg = cm != rr;
-    unsigned long long st4 = 0ull;  // above | above&prev << 16 | bucket << 32 | bucket&prev << 48
+    int nab = 0, nabp = 0, ninb = 0, ninbp = 0;
     for (int ch = c0; ch < c1; ++ch) {
       const float4 v = reinterpret_cast<const float4*>(s.seg)[ch];
       const float vs[4] = {v.x, v.y, v.z, v.w};
@@ -460,37 +546,52 @@ __global__ void __launch_bounds__(ST, 1) select_kernel(
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         const int p = 4 * ch + c;
-        if (p < s1 - s0) {
-          const unsigned long long x = key_of(__float_as_uint(vs[c]), s0 + p, len, force);
-          const bool was = (pw >> c) & 1u;
-          const bool peq = (x >> (64 - bits)) == (P >> (64 - bits));
-          const bool above = x > xmax || (x >> (64 - bits)) > (P >> (64 - bits));
-          const bool inb = peq && x >= xlo && x <= xmax;
-          st4 += (unsigned long long)above + ((unsigned long long)(above && was) << 16) +
-                 ((unsigned long long)inb << 32) + ((unsigned long long)(inb && was) << 48);
-          if (inb && xchg) {
-            const int slot = atomicAdd(&s.ncand, 1);
+        if (p < nseg) {
+          const uint32_t vb = p == tforce ? 0x7F800000u : __float_as_uint(vs[c]);
+          const unsigned long long x = composite(vb, s0 + p);
+          const int was = (pw >> c) & 1u;
+          nwas += was;
+          if (x > khi) {
+            ++nab;
+            nabp += was;
+          } else if (x >= klo) {
+            ++ninb;
+            ninbp += was;
+            if (xchg) {  // the bucket element to every rank (12 bytes on its BAR_X)
+              const int slot = atomicAdd(&s.ncand, 1);
+              const uint32_t ci = (uint32_t)tid | ((uint32_t)was << 16);
+              const uint32_t ak = smem_u32(&s.cand[rank][slot]), bx = smem_u32(&s.bar[BAR_X]);
+              const uint4 rec = make_uint4((uint32_t)x, (uint32_t)(x >> 32), ci, 0u);
 #pragma unroll
-            for (int q = 0; q < SCL; ++q) {
-              cl.map_shared_rank(&s.cand[rank][slot], q)[0] = x;
-              cl.map_shared_rank(&s.candp[rank][slot], q)[0] = (uint8_t)was;
+              for (int q = 0; q < SCL; ++q) dsm_st128(dsm_map(ak, q), rec, dsm_map(bx, q));
             }
           }
         }
       }
     }
+    sel_mark(6);
+    {
+      unsigned long long st4 = (unsigned long long)nab + ((unsigned long long)nabp << 16) +
+                               ((unsigned long long)ninb << 32) + ((unsigned long long)ninbp << 48);
 #pragma unroll
-    for (int o = 16; o; o >>= 1) st4 += __shfl_xor_sync(0xffffffffu, st4, o);
-    if (lane == 0 && st4) atomicAdd(&s.my_stats, st4);
-    __syncthreads();
-    if (tid < SCL) {
-      cl.map_shared_rank(&s.stats[rank], tid)[0] = s.my_stats;
-      cl.map_shared_rank(&s.candn[rank], tid)[0] = xchg ? s.ncand : 0;
+      for (int o = 16; o; o >>= 1) st4 += __shfl_xor_sync(0xffffffffu, st4, o);
+      if (lane == 0 && st4) atomicAdd(&s.my_stats, st4);
     }
-    cl.sync();
+    __syncthreads();
+    if (tid < SCL) {  // this CTA's counts and bucket size to rank tid (its bucket sent above)
+      const int nc = xchg ? s.ncand : 0;
+      const uint32_t bx = dsm_map(smem_u32(&s.bar[BAR_X]), tid);
+      dsm_expect(bx, 12u + 16u * (uint32_t)nc);
+      dsm_st64(dsm_map(smem_u32(&s.stats[rank]), tid), s.my_stats, bx);
+      dsm_st32(dsm_map(smem_u32(&s.candn[rank]), tid), (uint32_t)nc, bx);
+    }
+    sel_mark(8);
+    dsm_wait(smem_u32(&s.bar[BAR_X]));
     sel_mark(9);
     if (!xchg) {
-      T = P > xlo ? P : xlo;  // the whole bucket is selected: T = its lower end
+      T = klo;  // the whole bucket is selected: T = its lower end
+      nsel = nab + ninb;
+      nnew = (nab - nabp) + (ninb - ninbp);
 #pragma unroll
       for (int q = 0; q < SCL; ++q) {
         const unsigned long long sq = s.stats[q];
@@ -502,42 +603,49 @@ __global__ void __launch_bounds__(ST, 1) select_kernel(
         b_selp += q < rank ? sp : 0;
       }
     } else {
-      // rank the bucket by counting (4 threads per candidate) after flattening it
+      // flatten the row's bucket, then rank it: warp w takes candidates w, w + 16, ..., its
+      // lanes hold the keys lane + 32 i in registers (one compare each + a warp sum)
       int nall = 0;
 #pragma unroll
       for (int q = 0; q < SCL; ++q) nall += s.candn[q];
-      unsigned long long mine = 0ull;
-      int mine_q = 0, mine_p = 0;
       if (tid < nall) {
         int i = tid, q = 0;
         while (i >= s.candn[q]) i -= s.candn[q++];
-        mine = s.cand[q][i];
-        mine_q = q;
-        mine_p = s.candp[q][i];
+        const uint4 rec = s.cand[q][i];
+        s.flat[tid] = (unsigned long long)rec.x | ((unsigned long long)rec.y << 32);
+        s.flati[tid] = rec.z | ((uint32_t)q << 17);
       }
-      unsigned long long* flat = &s.cand[SCL - 1][0];
-      __syncthreads();  // every region read before the flat copy overwrites the last one
-      if (tid < nall) flat[tid] = mine;
       __syncthreads();
       {
-        const int ci = tid >> 2, part = tid & 3;
-        int larger = 0;
-        if (ci < nall) {
-          const unsigned long long x = flat[ci];
-#pragma unroll 4
-          for (int j = part; j < nall; j += 4) larger += flat[j] > x;
+        unsigned long long kk[CANDMAX / 32];
+#pragma unroll
+        for (int i = 0; i < CANDMAX / 32; ++i)  // keys are > 0 (~id has bit 31 set): 0 pads
+          kk[i] = lane + 32 * i < nall ? s.flat[lane + 32 * i] : 0ull;
+        for (int c = warp; c < nall; c += ST / 32) {
+          const unsigned long long x = s.flat[c];
+          int n = 0;
+#pragma unroll
+          for (int i = 0; i < CANDMAX / 32; ++i) n += kk[i] > x;
+          n = __reduce_add_sync(0xffffffffu, n);
+          if (lane == 0 && n == rr - 1) s.T = x;
         }
-        larger += __shfl_xor_sync(0xffffffffu, larger, 1);
-        larger += __shfl_xor_sync(0xffffffffu, larger, 2);
-        if (ci < nall && part == 0 && larger == rr - 1) s.T = flat[ci];
       }
       __syncthreads();
       T = s.T;
-      if (tid < nall && mine >= T) {
+      if (tid < nall && s.flat[tid] >= T) {
+        const uint32_t info = s.flati[tid];
+        const int was = (int)((info >> 16) & 1u), mine_q = (int)(info >> 17);
         atomicAdd(&s.csel[mine_q], 1);
-        if (mine_p) atomicAdd(&s.cselp[mine_q], 1);
+        if (was) atomicAdd(&s.cselp[mine_q], 1);
+        if (mine_q == rank) {  // credit the owning thread of this CTA
+          const int ot = (int)(info & 0xFFFFu);
+          atomicAdd(reinterpret_cast<unsigned*>(&s.xsel[ot & ~1]), 1u << (16 * (ot & 1)));
+          if (!was) atomicAdd(reinterpret_cast<unsigned*>(&s.xnew[ot & ~1]), 1u << (16 * (ot & 1)));
+        }
       }
       __syncthreads();
+      nsel = nab + s.xsel[tid];
+      nnew = (nab - nabp) + s.xnew[tid];
 #pragma unroll
       for (int q = 0; q < SCL; ++q) {
         const unsigned long long sq = s.stats[q];
@@ -555,6 +663,13 @@ __global__ void __launch_bounds__(ST, 1) select_kernel(
     a_sel = len;
     b_selp = s.lpre[0];
     a_selp = s.lpre[2];
+    for (int ch = c0; ch < c1; ++ch) {
+      const uint32_t pw = s.bm_prev[ch >> 3] >> ((ch & 7) * 4);
+      const int nv = min(4, nseg - 4 * ch);
+      nwas += __popc(pw & ((1u << nv) - 1u));
+      nsel += nv;
+    }
+    nnew = nsel - nwas;
   }
   sel_mark(5);
 
@@ -563,28 +678,17 @@ __global__ void __launch_bounds__(ST, 1) select_kernel(
   const int bs = b_sel, bn = b_sel - b_selp, be = s.lpre[0] - b_selp;
   const int as = a_sel, an = a_sel - a_selp, ae = np - a_selp;
   const int ntail = np - s.lpre[2];
-  unsigned long long cnt = 0ull;  // selected | new << 21 | evicted << 42
-  for (int ch = c0; ch < c1; ++ch) {
-    const float4 v = reinterpret_cast<const float4*>(s.seg)[ch];
-    const float vs[4] = {v.x, v.y, v.z, v.w};
-    const uint32_t pw = s.bm_prev[ch >> 3] >> ((ch & 7) * 4);
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      const int p = 4 * ch + c;
-      if (p < s1 - s0) {
-        const bool sel = key_of(__float_as_uint(vs[c]), s0 + p, len, force) >= T;
-        const bool was = (pw >> c) & 1u;
-        cnt += (unsigned long long)sel + ((unsigned long long)(sel && !was) << 21) +
-               ((unsigned long long)(!sel && was) << 42);
-      }
-    }
-  }
+  const int nev = nwas - (nsel - nnew);  // previously selected, not selected now
+  const unsigned long long cnt = (unsigned long long)nsel + ((unsigned long long)nnew << 21) +
+                                 ((unsigned long long)nev << 42);
   const unsigned long long pos = scan_u64(s, cnt);
+  sel_mark(15);
   int32_t* oi = out_idx + (size_t)bg * k;
   int32_t* lt = load_tok + (size_t)bg * k;
   int32_t* et = evict_tok ? evict_tok + (size_t)bg * k : nullptr;
   int ps = bs + (int)(pos & 0x1FFFFF), pn = bn + (int)((pos >> 21) & 0x1FFFFF),
       pe = be + (int)(pos >> 42);
+  const uint32_t Thi = (uint32_t)(T >> 32), Tlo = (uint32_t)T;
   for (int ch = c0; ch < c1; ++ch) {
     const float4 v = reinterpret_cast<const float4*>(s.seg)[ch];
     const float vs[4] = {v.x, v.y, v.z, v.w};
@@ -592,9 +696,11 @@ __global__ void __launch_bounds__(ST, 1) select_kernel(
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
       const int p = 4 * ch + c;
-      if (p < s1 - s0) {
+      if (p < nseg) {
         const int t = s0 + p;
-        const bool sel = key_of(__float_as_uint(vs[c]), t, len, force) >= T;
+        const uint32_t vb = p == tforce ? 0x7F800000u : __float_as_uint(vs[c]);
+        // key >= T on (value bits, ~id) without forming the 64-bit key
+        const bool sel = !cut || vb > Thi || (vb == Thi && ~(uint32_t)t >= Tlo);
         const bool was = (pw >> c) & 1u;
         if (sel) oi[ps++] = t;
         if (sel && !was) lt[pn++] = t;
@@ -617,7 +723,6 @@ __global__ void __launch_bounds__(ST, 1) select_kernel(
   }
   sel_mark(7);
 }
-
 }  // namespace
 }  // namespace spc
 
@@ -665,7 +770,7 @@ extern "C" int spc_select(const float* logits, const float* head_max, const int3
   cudaStream_t st = as_stream(stream);
 #define SEL(AA)                                                                                 \
   if (alpha == AA)                                                                              \
-    return launch_select<AA, 8>(logits, head_max, seq_len, B, G, Smax, k, force_last,           \
+    return launch_select<AA, SPC_SEL_SCL>(logits, head_max, seq_len, B, G, Smax, k, force_last,           \
                                 head_sumfix, group_score, out_idx, out_count, prev_idx,          \
                                 prev_count, load_tok, n_load, evict_tok, n_evict, st);
   SEL(1) SEL(2) SEL(4) SEL(8)

@@ -309,20 +309,27 @@ class DecodeStep:
         torch.cuda.current_stream().wait_stream(s)
         self.use_set(keep)
 
-    def capture_sequence(self, items):
-        """One CUDA graph per step of a fixed input sequence: items[i] = (input set, q_ret,
-        q_llm); step i runs with parity i % 2 (call reset_state() before replaying from step
-        0).  The kernels read each step's queries in place: no staging copies."""
+    def capture_sequence(self, items, bounds=None):
+        """CUDA graphs of a fixed input sequence: items[i] = (input set, q_ret, q_llm); step i
+        runs with parity i % 2 (call reset_state() before replaying from step 0).  The kernels
+        read each step's queries in place: no staging copies.  bounds: [(a, b), ...] index
+        ranges, each captured as ONE graph of the consecutive steps a .. b-1 (a decode loop
+        with no host work between steps: the steps' kernels then chain without a graph launch
+        boundary); default one graph per step."""
+        if bounds is None:
+            bounds = [(i, i + 1) for i in range(len(items))]
         graphs = []
         keep = self.cur_set
         s = torch.cuda.Stream(device=self.dev)
         s.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(s):
-            for i, (si, qr, ql) in enumerate(items):
-                self.use_set(si)
+            for a, b in bounds:
                 g = torch.cuda.CUDAGraph()
                 with torch.cuda.graph(g, stream=s):
-                    self.enqueue(i % 2, q_ret=qr, q_llm=ql)
+                    for i in range(a, b):
+                        si, qr, ql = items[i]
+                        self.use_set(si)
+                        self.enqueue(i % 2, q_ret=qr, q_llm=ql)
                 graphs.append(g)
         torch.cuda.current_stream().wait_stream(s)
         self.use_set(keep)

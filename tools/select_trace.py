@@ -30,29 +30,23 @@ cnt = [z(B, G, dt=i32) for _ in range(2)]
 lt, nl = z(B, G, k, dt=i32), z(B, G, dt=i32)
 tr = torch.zeros(64 * 16 * 16, dtype=torch.int64, device=dev)
 GX = int(os.environ.get("SCL", "16" if B * G <= 9 else "8"))  # CTAs per row used by the lib
-names = ["start", "norm", "group", "pass0", "passes", "T", "counts", "end", "x_comp", "x_sync",
-         "bitmap", "exp", "push"]
+names = ["start", "norm", "group", "pass0", "passes", "T", "cls_loop", "end", "cls_presync",
+         "x_sync", "bitmap", "exp", "push", "h0_push", "h0_sync", "scan"]
 for step in range(4):
     spc.score(qs[step], kr, seq, G, 0.088, lg, hm, F, gs, ws, phases=spc.SCORE_LOGITS)
     torch.cuda.synchronize()
     tr.zero_()
     lib.spc_debug_set_select_trace(ctypes.c_void_p(tr.data_ptr()) if step == 3 else None)
-    e = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
-    e[0].record()
     spc.select(lg, hm, seq, G, k, F, gs, idx[step % 2], cnt[step % 2], idx[1 - step % 2],
                cnt[1 - step % 2], lt, nl, force_last=True)
-    e[1].record()
     torch.cuda.synchronize()
-    print(f"step {step}: {e[0].elapsed_time(e[1]) * 1e3:.1f} us")
+GX = 8
 t = tr[:64 * GX * 16].view(64, GX, 16).cpu().numpy().astype("float64")
-rows = int((t[:, 0, 0] > 0).sum())
-t0 = t[:rows, :, 0].min()
-print("rank " + " ".join(f"{n:>8s}" for n in names))
-for r in range(GX):
-    print(f"{r:4d} " + " ".join(f"{(t[0, r, i] - t0) / 1e3:8.2f}" if t[0, r, i] > 0 else "       -"
-                                for i in range(len(names))))
-print("row  start_min start_max  end_max   (us from the first CTA start)")
-for row in range(rows):
-    st = t[row, :, 0]
-    en = t[row, :, 7]
-    print(f"{row:3d} {(st.min() - t0) / 1e3:9.2f} {(st.max() - t0) / 1e3:9.2f} {(en.max() - t0) / 1e3:9.2f}")
+order = [0, 10, 11, 12, 1, 2, 13, 14, 3, 4, 6, 8, 9, 5, 15, 7]
+print("clock64 marks, us from each CTA's own start (1.965 GHz); row 0 and row 1")
+print("rank " + " ".join(f"{names[i]:>8s}" for i in order))
+for row in range(2):
+    for r in range(GX):
+        st = t[row, r, 0]
+        print(f"{row}.{r:2d} " + " ".join(f"{(t[row, r, i] - st) / 1965.0:8.2f}" if t[row, r, i] > 0 else "       -"
+                                       for i in order))
