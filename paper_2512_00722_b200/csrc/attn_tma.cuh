@@ -421,10 +421,11 @@ __global__ void __launch_bounds__(TM_THREADS, TM_CTAS) attn_tma_kernel(
 
 // LSE merge (O12) of the per-CTA partials of every group, launched right behind
 // attn_tma_kernel (PDL: its CTAs wait at griddepcontrol.wait while the attention drains,
-// so the merge costs two dependent L2 round trips instead of a ticketed tail in the
-// attention kernel -- measured: the in-kernel tickets + merges added ~10 us of tail).
-// One warp per (group, head): lane p < np reads partial p's (m, l); every lane owns D/32
-// output dims.  The partials of group gq are segments (gq*cpg)/cpc .. (gq*cpg+cpg-1)/cpc.
+// so the merge costs one L2 round trip per 8 partials instead of a ticketed tail in the
+// attention kernel -- measured: in-kernel tickets + merges, inline or after each CTA's loop,
+// made the attention 3-10 us slower).  One warp per (group, head): every lane reads the
+// (m, l) of up to 8 partials and its D/32 dims of each, all loads before any use.  The
+// partials of group gq are segments (gq*cpg)/cpc .. (gq*cpg+cpg-1)/cpc.
 template <int D, int ALPHA>
 __global__ void __launch_bounds__(128) tma_merge_kernel(
     const float* __restrict__ part_o, const float* __restrict__ part_ml, int cpg, int cpc,
@@ -432,6 +433,7 @@ __global__ void __launch_bounds__(128) tma_merge_kernel(
     float* __restrict__ lse) {
   spc_pdl_entry();
   constexpr int DPL = D / 32;  // dims per lane
+  constexpr int PU = 8;        // partials per round: all loads of a round issued before any use
   const int wg = blockIdx.x * 4 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (wg >= n_groups * ALPHA) return;
   const int gq = wg / ALPHA, j = wg - gq * ALPHA;
@@ -441,42 +443,52 @@ __global__ void __launch_bounds__(128) tma_merge_kernel(
   const size_t h = ((size_t)lr * B + b) * Hq + g * ALPHA + j;  // partial head index
   const size_t oh = ((size_t)(layer_begin + lr) * B + b) * Hq + g * ALPHA + j;
   const float* ml = part_ml + h * segstride * 2;
-  // lane p holds partial p's (m, l) (chunks of 32 partials); the partial outputs are then
-  // read 8 at a time with the weights broadcast by shuffles, so a group's np partials cost
-  // ~np/8 dependent L2 round trips (a per-partial loop cost ~0.5 us per partial: 16
-  // partials per group when one layer is attended per call, llm.py)
-  float M = -INFINITY;
-  for (int p = lane; p < np; p += 32) M = fmaxf(M, __ldcg(ml + 2 * p));
-  M = warp_max(M);
+  const float* po = part_o + h * segstride * D + lane * DPL;
+  // one L2 round trip per PU partials: every lane loads the (m, l) of all of them (broadcast
+  // loads) and its own DPL dims of each, then merges (M = running maximum, rescaled sums)
+  float M = -INFINITY, den = 0.f;
   float acc[DPL];
 #pragma unroll
   for (int i = 0; i < DPL; ++i) acc[i] = 0.f;
-  float den = 0.f;
-  for (int p0 = 0; p0 < np; p0 += 32) {
-    const int n = min(32, np - p0);
-    float w = 0.f;
-    if (lane < n) {
-      const float2 mlp = __ldcg(reinterpret_cast<const float2*>(ml) + p0 + lane);
-      w = mlp.x == -INFINITY ? 0.f : exp2f(mlp.x - M);
-      den += w * mlp.y;
-    }
-    const float* po = part_o + (h * segstride + p0) * D + lane * DPL;
-#pragma unroll 8
-    for (int i = 0; i < n; ++i) {
-      const float wi = __shfl_sync(0xffffffffu, w, i);
-      if (DPL == 4) {
-        const float4 v = __ldcg(reinterpret_cast<const float4*>(po + (size_t)i * D));
-        acc[0] += wi * v.x;
-        acc[DPL > 1 ? 1 : 0] += wi * v.y;
-        acc[DPL > 2 ? 2 : 0] += wi * v.z;
-        acc[DPL > 3 ? 3 : 0] += wi * v.w;
-      } else {
+  for (int p0 = 0; p0 < np; p0 += PU) {
+    float2 m_l[PU];
+    float v[PU][DPL];
 #pragma unroll
-        for (int d = 0; d < DPL; ++d) acc[d] += wi * __ldcg(po + (size_t)i * D + d);
+    for (int u = 0; u < PU; ++u) {
+      const int p = p0 + u;
+      m_l[u] = p < np ? __ldcg(reinterpret_cast<const float2*>(ml) + p) : make_float2(-INFINITY, 0.f);
+#pragma unroll
+      for (int i = 0; i < DPL; i += (DPL % 4 == 0 ? 4 : 1)) {
+        if (DPL % 4 == 0) {
+          const float4 x = p < np ? __ldcg(reinterpret_cast<const float4*>(po + (size_t)p * D + i))
+                                  : make_float4(0.f, 0.f, 0.f, 0.f);
+          v[u][i] = x.x;
+          v[u][(i + 1) % DPL] = x.y;
+          v[u][(i + 2) % DPL] = x.z;
+          v[u][(i + 3) % DPL] = x.w;
+        } else {
+          v[u][i] = p < np ? __ldcg(po + (size_t)p * D + i) : 0.f;
+        }
       }
     }
+    float Mn = M;
+#pragma unroll
+    for (int u = 0; u < PU; ++u) Mn = fmaxf(Mn, m_l[u].x);
+    if (Mn != -INFINITY) {
+      const float c = M == -INFINITY ? 0.f : exp2f(M - Mn);
+      den *= c;
+#pragma unroll
+      for (int i = 0; i < DPL; ++i) acc[i] *= c;
+#pragma unroll
+      for (int u = 0; u < PU; ++u) {
+        const float w = m_l[u].x == -INFINITY ? 0.f : exp2f(m_l[u].x - Mn);
+        den += w * m_l[u].y;
+#pragma unroll
+        for (int i = 0; i < DPL; ++i) acc[i] += w * v[u][i];
+      }
+      M = Mn;
+    }
   }
-  den = warp_sum(den);
   const float inv = den > 0.f ? 1.f / den : 0.f;
 #pragma unroll
   for (int i = 0; i < DPL; ++i) out[oh * D + lane * DPL + i] = acc[i] * inv;

@@ -35,6 +35,11 @@ namespace cg = cooperative_groups;
 namespace spc {
 namespace {
 
+#ifdef SPC_SEL_NREG  // register cap (experiment: room for attention CTAs beside a select CTA)
+#define SPC_SEL_BOUNDS __maxnreg__(SPC_SEL_NREG)
+#else
+#define SPC_SEL_BOUNDS __launch_bounds__(ST, 1)
+#endif
 #ifndef SPC_SEL_SCL
 #define SPC_SEL_SCL 8
 #endif
@@ -64,62 +69,6 @@ __device__ __forceinline__ void sel_mark(int slot) {
 
 constexpr int MAXPASS = 8;  // radix passes: pass 0 fixes 12 key bits, each later one 8 more
 constexpr int BAR_NORM = 0, BAR_X = 1, BAR_H = 2;  // mbarriers: NORM, candidates, pass p = BAR_H + p
-
-// ---- DSMEM exchanges without cluster barriers.  A sender writes with remote st.async /
-// red.async whose bytes complete the destination CTA's mbarrier (complete_tx) and arrives
-// once on that mbarrier with the byte count it sends (arrive.expect_tx, relaxed: no fence
-// that would wait for this CTA's outstanding global stores, as barrier.cluster.arrive's
-// release does); the receiver waits for the phase (acquire, cluster scope), i.e. until every
-// sender's bytes have landed.  Every mbarrier is used for one phase per launch (parity 0).
-__device__ __forceinline__ uint32_t dsm_map(uint32_t a, int rank) {
-  uint32_t r;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
-  return r;
-}
-__device__ __forceinline__ void dsm_st64(uint32_t ra, unsigned long long v, uint32_t rbar) {
-  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(ra),
-               "l"(v), "r"(rbar)
-               : "memory");
-}
-__device__ __forceinline__ void dsm_st32(uint32_t ra, uint32_t v, uint32_t rbar) {
-  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];" ::"r"(ra),
-               "r"(v), "r"(rbar)
-               : "memory");
-}
-__device__ __forceinline__ void dsm_st128(uint32_t ra, uint4 v, uint32_t rbar) {
-  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(
-                   ra),
-               "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w), "r"(rbar)
-               : "memory");
-}
-__device__ __forceinline__ void dsm_red_add(uint32_t ra, uint32_t v, uint32_t rbar) {
-  asm volatile(
-      "red.async.relaxed.cluster.shared::cluster.mbarrier::complete_tx::bytes.add.u32 [%0], %1, [%2];" ::"r"(
-          ra),
-      "r"(v), "r"(rbar)
-      : "memory");
-}
-__device__ __forceinline__ void dsm_expect(uint32_t rbar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.relaxed.cluster.shared::cluster.b64 _, [%0], %1;" ::"r"(rbar),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void dsm_wait(uint32_t bar) {
-  const long long t0 = clock64();
-  for (;;) {
-    uint32_t ok;
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "mbarrier.test_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], 0;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(ok)
-        : "r"(bar)
-        : "memory");
-    if (ok) return;
-    if (clock64() - t0 > 8000000000ll) __trap();  // ~4 s: a lost exchange fails loudly
-  }
-}
-
 
 template <int SCL>
 struct SelSm {
@@ -229,7 +178,7 @@ __device__ __forceinline__ void find_bin(SelSm<SCL>& s, int pass, int r) {
 }
 
 template <int ALPHA, int NC, int SCL>
-__global__ void __launch_bounds__(ST, 1) select_kernel(
+__global__ void SPC_SEL_BOUNDS select_kernel(
     const float* __restrict__ logits, const float* __restrict__ head_max,
     const int32_t* __restrict__ seq_len, int G, int Smax, int k, int force,
     int64_t* __restrict__ head_sumfix, float* __restrict__ group_score,

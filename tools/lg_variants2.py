@@ -11,6 +11,7 @@ VARIANTS = {
     "b1": ["SPC_LT_BATCH=1"],
     "b4": ["SPC_LT_BATCH=4"],
     "scl16": ["SPC_SEL_SCL=16"],
+    "nreg80": ["SPC_SEL_NREG=80"],
 }
 for name in (sys.argv[1:] or VARIANTS):
     out = os.path.join(os.path.dirname(os.path.abspath(__file__)), f"libspc_{name}.so")

@@ -10,6 +10,10 @@ import torch  # noqa: E402
 from paper_2512_00722_b200 import spc, synth  # noqa: E402
 from paper_2512_00722_b200.pipeline import DecodeStep  # noqa: E402
 
+for a in sys.argv[1:]:
+    if a.startswith("--lib="):
+        spc._lib = spc.load_library(a[6:])
+
 c = synth.CONFIGS["B"]
 B, G, Hq, D, S, L, k = c["B"], c["G"], c["Hq"], c["D"], c["S"], c["L"], c["k"]
 dev = torch.device("cuda")
