@@ -51,11 +51,23 @@ struct TmSmem {
 
 __device__ __forceinline__ void tm_gather4(uint32_t dst, const CUtensorMap* map, uint32_t bar, int col,
                                            int r0, int r1, int r2, int r3) {
+#ifndef SPC_TM_EVICT_NORMAL
+  // the KV rows are read once per step: evict them first, so the step's small hot data (its
+  // kernels' code, logits, selections) is not pushed out of L2 by the 256 MiB stream
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%3, %4, %5, %6, %7}], [%2], %8;" ::"r"(dst),
+      "l"(map), "r"(bar), "r"(col), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "l"(pol)
+      : "memory");
+#else
   asm volatile(
       "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
       " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(dst),
       "l"(map), "r"(bar), "r"(col), "r"(r0), "r"(r1), "r"(r2), "r"(r3)
       : "memory");
+#endif
 }
 // Debug trace (-DSPC_TRACE builds, spc_debug_set_trace): per CTA c < 2048,
 // g_trace[4096 + 4c + i] = %globaltimer at (0) entry after the PDL wait, (1) the consumer's
@@ -182,6 +194,17 @@ __global__ void __launch_bounds__(TM_THREADS, TM_CTAS) attn_tma_kernel(
           else tm_arrive(fb);  // nothing valid in this stage: complete the phase without bytes
         }
         __syncwarp();
+#ifdef SPC_TM_WIDE
+        {  // every lane issues ONE gather4: lane = (kv, half, row quad)
+          const int rq = lane % TM_NREQ, hk = lane / TM_NREQ;  // hk = kv * NH + h
+          const int4 rr = make_int4(__shfl_sync(0xffffffffu, r.x, rq), __shfl_sync(0xffffffffu, r.y, rq),
+                                    __shfl_sync(0xffffffffu, r.z, rq), __shfl_sync(0xffffffffu, r.w, rq));
+          if (any && hk < 2 * NH) {
+            const uint32_t st = ring + (uint32_t)s * SM::STAGE + (uint32_t)rq * 512u + hk * SM::HALF;
+            tm_gather4(st, hk < NH ? km : vm, fb, 64 * (hk % NH), rr.x, rr.y, rr.z, rr.w);
+          }
+        }
+#else
         if (any && lane < TM_NREQ) {
           const uint32_t st = ring + (uint32_t)s * SM::STAGE + (uint32_t)lane * 512u;
 #pragma unroll
@@ -190,6 +213,7 @@ __global__ void __launch_bounds__(TM_THREADS, TM_CTAS) attn_tma_kernel(
             tm_gather4(st + (NH + h) * SM::HALF, vm, fb, 64 * h, r.x, r.y, r.z, r.w);
           }
         }
+#endif
         if (++rc == cpg) {
           rc = 0;
           ++grp;

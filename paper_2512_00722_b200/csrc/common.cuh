@@ -336,7 +336,7 @@ __device__ __forceinline__ void dsm_wait(uint32_t bar) {
     uint32_t ok;
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
-        "mbarrier.test_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], 0;\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], 0;\n\t"
         "selp.u32 %0, 1, 0, p;\n\t}"
         : "=r"(ok)
         : "r"(bar)
@@ -344,6 +344,13 @@ __device__ __forceinline__ void dsm_wait(uint32_t bar) {
     if (ok) return;
     if (clock64() - t0 > 8000000000ll) __trap();  // ~4 s: a lost exchange fails loudly
   }
+}
+// The whole CTA waits for an exchange: ONE thread acquires the phase (cluster scope), the
+// CTA barrier then orders everyone else after it (16 warps spinning on cluster-scope
+// acquires slowed every exchange's exit).
+__device__ __forceinline__ void dsm_wait_cta(uint32_t bar) {
+  if (threadIdx.x == 0) dsm_wait(bar);
+  __syncthreads();
 }
 
 

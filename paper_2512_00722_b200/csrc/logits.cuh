@@ -399,19 +399,38 @@ __global__ void __launch_bounds__(32 * (LT_NC + 1), 1) logits_tma_kernel(
     prefetch_tmap(&kmap);
   }
   __syncthreads();
+  // before the PDL wait (the previous launch may still be running): pull this CTA's first,
+  // static tiles into L2.  Only an L2 hint -- the keys are read by the TMA loads after the
+  // wait, and L2 is coherent with any kernel that writes them (the front-end's newest key) --
+  // so the HBM stream starts while the previous kernel drains (its last CTAs, its merge)
+  if (warp == LT_NC && lane < LT_RINGS) {
+    const int t_lo = ((int)blockIdx.x * LT_RINGS + lane) * SPC_LT_BATCH;
+    for (int tile = t_lo; tile < min(t_lo + SPC_LT_BATCH, ntiles); ++tile) {
+      const int bg = tile / tpr, tt = tile - bg * tpr;
+#pragma unroll
+      for (int c = 0; c < LtSmem<D, ALPHA>::NCH; ++c)
+        asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global [%0, {%1, %2}];" ::"l"(&kmap), "r"(64 * c),
+                     "r"(bg * Smax + tt * LG_TR)
+                     : "memory");
+    }
+  }
   spc_pdl_entry();
   if (warp == LT_NC) {
-    // ------------------------------------------------------------ producer (lane 0)
-    // tiles come in batches of LT_BATCH consecutive tiles: the CTA's first batch is static,
-    // the next ones are claimed from one grid-wide counter, each claim issued a batch ahead
-    // (its latency hides behind the current batch); the counter balances the SMs, whose
-    // streaming rates differ (config E: 443 tiles per SM).  Tiles go to the LT_RINGS rings
-    // round robin; the LT_CPR consumers of a ring split each of its stages' rows
-    if (lane == 0) {
+    // ------------------------------------------------------------ producers (lanes)
+    // lane w < LT_RINGS feeds ring w on its own (divergent lanes progress independently), so
+    // a ring whose consumers lag never blocks the issue for the other rings.  Tiles come in
+    // batches of LT_BATCH consecutive tiles: a lane's first batch is static, the next ones
+    // are claimed from one grid-wide counter, each claim issued a batch ahead (its latency
+    // hides behind the current batch); the counter balances the SMs, whose streaming rates
+    // differ (config E: 443 tiles per SM).  The LT_CPR consumers of a ring split each of its
+    // stages' rows.
+    if (lane < LT_RINGS) {
       constexpr int LT_BATCH = SPC_LT_BATCH;
-      int nt = 0;  // tiles handed to rings
-      int batch = (int)blockIdx.x;
-      int next = (int)gridDim.x + (int)atomicAdd(ctr, 1u);
+      const int w = lane;
+      const int nstatic = (int)gridDim.x * LT_RINGS;
+      int n = 0;  // tiles handed to ring w
+      int batch = (int)blockIdx.x * LT_RINGS + w;
+      int next = nstatic + (int)atomicAdd(ctr, 1u);
       for (;;) {
         const int t_lo = batch * LT_BATCH;
         if (t_lo >= ntiles) break;
@@ -424,8 +443,6 @@ __global__ void __launch_bounds__(32 * (LT_NC + 1), 1) logits_tma_kernel(
                 tile_max[(((size_t)b * Hq + g * ALPHA + j) * tpr + tt) * LT_CPR + hh] = -INFINITY;
             continue;
           }
-          const int w = nt % LT_RINGS, n = nt / LT_RINGS;  // ring and its tile count
-          ++nt;
           for (int c = 0; c < NCH; ++c) {
             const int j = n * NCH + c;  // sequence number in ring w
             const int s = w * K + j % K;
@@ -433,11 +450,21 @@ __global__ void __launch_bounds__(32 * (LT_NC + 1), 1) logits_tma_kernel(
             const uint32_t fb = full0 + 8 * s;
             if (c == 0) stage_tile[s] = tile;  // published by the arrive below (release)
             tm_expect(fb, LT_STAGE + (c == 0 ? SM::QRAW : 0));
+#ifndef SPC_TM_EVICT_NORMAL  // the keys are streamed once per step: evict them first
+            uint64_t pol;
+            asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+            asm volatile(
+                "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+                " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(base + s * LT_STAGE),
+                "l"(&kmap), "r"(64 * c), "r"(bg * Smax + tt * LG_TR), "r"(fb), "l"(pol)
+                : "memory");
+#else
             asm volatile(
                 "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
                 " [%0], [%1, {%2, %3}], [%4];" ::"r"(base + s * LT_STAGE),
                 "l"(&kmap), "r"(64 * c), "r"(bg * Smax + tt * LG_TR), "r"(fb)
                 : "memory");
+#endif
             if (c == 0) {
               const int b = bg / G, g = bg - b * G;
               asm volatile(
@@ -447,18 +474,16 @@ __global__ void __launch_bounds__(32 * (LT_NC + 1), 1) logits_tma_kernel(
                   : "memory");
             }
           }
+          ++n;
         }
         batch = next;
-        if (batch * LT_BATCH < ntiles) next = (int)gridDim.x + (int)atomicAdd(ctr, 1u);
+        if (batch * LT_BATCH < ntiles) next = nstatic + (int)atomicAdd(ctr, 1u);
       }
-      // end of the work: every ring's next tile slot gets the end code
-      for (int w = 0; w < LT_RINGS; ++w) {
-        const int n = nt / LT_RINGS + (w < nt % LT_RINGS ? 1 : 0);  // tiles ring w received
-        const int j = n * NCH, s = w * K + j % K;
-        if (j >= K) tm_wait(empty0 + 8 * s, ((j / K) - 1) & 1);
-        stage_tile[s] = -1;
-        tm_arrive(full0 + 8 * s);
-      }
+      // end of the work: the ring's next tile slot gets the end code
+      const int j = n * NCH, s = w * K + j % K;
+      if (j >= K) tm_wait(empty0 + 8 * s, ((j / K) - 1) & 1);
+      stage_tile[s] = -1;
+      tm_arrive(full0 + 8 * s);
     }
     return;
   }
@@ -497,10 +522,30 @@ __global__ void __launch_bounds__(32 * (LT_NC + 1), 1) logits_tma_kernel(
         if (bg != qf_bg) {  // raw [ALPHA][D] bf16 -> fp32 [D][ALPHA]
           qf_bg = bg;
           const uint16_t* qr = (const uint16_t*)(basep + SM::QSLOT_OFF + s * SM::QRAW);
+          if (ALPHA == 4 && D % 128 == 0) {  // lane: 4 consecutive d of every head, 16-byte stores
+#pragma unroll
+            for (int d0 = 4 * lane; d0 < D; d0 += 128) {
+              uint2 h[4];
+#pragma unroll
+              for (int jj = 0; jj < 4; ++jj) h[jj] = *reinterpret_cast<const uint2*>(qr + jj * D + d0);
+#pragma unroll
+              for (int dd = 0; dd < 4; ++dd) {
+                float4 v;
+                const int sh = (dd & 1) ? 0 : 16;
+                const uint32_t m = (dd & 1) ? 0xFFFF0000u : 0xFFFFFFFFu;
+                v.x = __uint_as_float(((dd < 2 ? h[0].x : h[0].y) << sh) & m);
+                v.y = __uint_as_float(((dd < 2 ? h[1].x : h[1].y) << sh) & m);
+                v.z = __uint_as_float(((dd < 2 ? h[2].x : h[2].y) << sh) & m);
+                v.w = __uint_as_float(((dd < 2 ? h[3].x : h[3].y) << sh) & m);
+                reinterpret_cast<float4*>(qf)[d0 + dd] = v;
+              }
+            }
+          } else {
 #pragma unroll 4
-          for (int e = lane; e < ALPHA * D; e += 32) {
-            const int jj = e / D, d = e - jj * D;
-            qf[d * ALPHA + jj] = __uint_as_float((uint32_t)qr[e] << 16);
+            for (int e = lane; e < ALPHA * D; e += 32) {
+              const int jj = e / D, d = e - jj * D;
+              qf[d * ALPHA + jj] = __uint_as_float((uint32_t)qr[e] << 16);
+            }
           }
           __syncwarp();
         }

@@ -142,7 +142,7 @@ __device__ __forceinline__ void exchange_hist(SelSm<SCL>& s, int rank, int pass)
 #pragma unroll
     for (int q = 0; q < SCL; ++q) dsm_st128(dsm_map(a, q), v, dsm_map(bar, q));
   }
-  dsm_wait(bar);
+  dsm_wait_cta(bar);
 }
 
 // After exchange_hist: bin of the r-th largest element counted from the top of the pass's
@@ -341,7 +341,7 @@ __global__ void SPC_SEL_BOUNDS select_kernel(
       if (c_len) atomicAdd(&s.lpre[2], c_len);
     }
   }
-  dsm_wait(smem_u32(&s.bar[BAR_NORM]));
+  dsm_wait_cta(smem_u32(&s.bar[BAR_NORM]));
   sel_mark(1);
 
   // ---- GROUP (O4..O6) + pass-0 histogram
@@ -535,7 +535,7 @@ __global__ void SPC_SEL_BOUNDS select_kernel(
       dsm_st32(dsm_map(smem_u32(&s.candn[rank]), tid), (uint32_t)nc, bx);
     }
     sel_mark(8);
-    dsm_wait(smem_u32(&s.bar[BAR_X]));
+    dsm_wait_cta(smem_u32(&s.bar[BAR_X]));
     sel_mark(9);
     if (!xchg) {
       T = klo;  // the whole bucket is selected: T = its lower end

@@ -12,6 +12,16 @@ VARIANTS = {
     "b4": ["SPC_LT_BATCH=4"],
     "scl16": ["SPC_SEL_SCL=16"],
     "nreg80": ["SPC_SEL_NREG=80"],
+    "tm3x4": ["SPC_TM_CTAS=3", "SPC_TM_NST=4"],
+    "tm2x6": ["SPC_TM_CTAS=2", "SPC_TM_NST=6"],
+    "tm5x2": ["SPC_TM_CTAS=5", "SPC_TM_NST=2"],
+    "tmnomath": ["SPC_TM_NOMATH"],
+    "tm3x4nm": ["SPC_TM_CTAS=3", "SPC_TM_NST=4", "SPC_TM_NOMATH"],
+    "tm6x2": ["SPC_TM_CTAS=6", "SPC_TM_NST=2"],
+    "tmwide": ["SPC_TM_WIDE"],
+    "evf": ["SPC_TM_EVICT_FIRST"],
+    "tmwide3x4": ["SPC_TM_WIDE", "SPC_TM_CTAS=3", "SPC_TM_NST=4"],
+    "tmwide6x2": ["SPC_TM_WIDE", "SPC_TM_CTAS=6", "SPC_TM_NST=2"],
 }
 for name in (sys.argv[1:] or VARIANTS):
     out = os.path.join(os.path.dirname(os.path.abspath(__file__)), f"libspc_{name}.so")
