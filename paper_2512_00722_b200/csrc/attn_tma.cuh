@@ -2,8 +2,9 @@
 // (spc_sparse_decode_attn_kv; included by attn.cu).  O10 per (layer, b, g), split over
 // CTAs, partials merged with the LSE rule O12 (Eq.1 over the P:324 selected rows).
 //
-// Persistent, TM_CTAS CTAs per SM, each CTA = one TMA producer warp + one MMA consumer
-// warp over a TM_NST-deep ring of TM_RPS-row stages (K and V of the same 32 selected rows).
+// Persistent, TM_CTAS CTAs per SM, each CTA = one TMA producer warp + TM_NCONS MMA consumer
+// warps over a TM_NST-deep ring of TM_RPS-row stages (K and V of the same 32 selected rows;
+// 5 CTAs x 2 stages x 2 consumers per SM, consumer c taking the stages j = c mod 2).
 // The selected rows of all groups (layer, b, g) form one virtual row space of
 // n_groups x kpad rows (kpad = k rounded up to whole stages); CTA c owns a contiguous
 // range of stages.
@@ -20,24 +21,37 @@
 // warp per SM is issue-bound at ~2 TB/s.  The consumer's smem reads are conflict-free
 // because the 16-byte granule c of row r sits at c ^ (r & 7) (128-byte swizzle).
 //
-// Consumer (warp 1): the transposed mma.sync products of attn_bf16.cuh on two 16-row
+// Consumers (warps 1, 2): the transposed mma.sync products of attn_bf16.cuh on two 16-row
 // tiles per stage -- S^T = K Q^T (K rows fill M) and O^T += V^T P with P's columns
 // [P_hi | P_lo] of the alpha heads -- one online-softmax update per 32-row stage,
 // release of the stage to the producer (mbarrier arrive), and at each group end one
-// (m, l, o) partial per CTA with plain stores; tma_merge_kernel (next launch, PDL)
-// merges each group's partials (O12).
+// (m, l, o) partial per consumer with plain stores; tma_merge_kernel (next launch, PDL)
+// merges each group's partials (O12).  The KV rows are loaded with an L2 evict_first
+// policy (read once per step: the step's small hot data stays in L2).
 #pragma once
 
 constexpr int TM_RPS = 32;      // rows per stage
 #ifndef SPC_TM_NST
-#define SPC_TM_NST 3
+#define SPC_TM_NST 2
 #endif
 #ifndef SPC_TM_CTAS
-#define SPC_TM_CTAS 4
+#define SPC_TM_CTAS 5
 #endif
 constexpr int TM_NST = SPC_TM_NST;    // ring depth
 constexpr int TM_CTAS = SPC_TM_CTAS;  // CTAs per SM
-constexpr int TM_THREADS = 64;        // warp 0 producer, warp 1 consumer
+#ifndef SPC_TM_NCONS
+#define SPC_TM_NCONS 2
+#endif
+// consumer warps: consumer c takes the stages j = c mod TM_NCONS, with its own (m, l, o) state
+// and partials.  Measured (config B step, tools/step_parts.py): 5 CTAs x 2 stages x 2
+// consumers 77.5 us; 4 x 3 x 1 (round 2's first TMA kernel) 79.5; 4 x 3 x 3 80.5; 3 CTAs
+// per SM 96 (the producers' gather rate per CTA is the limit); NOMATH 4 x 3 x 1 saves 3.6 us:
+// a second consumer overlaps one stage's MMA / softmax latency with the next stage's
+constexpr int TM_NCONS = SPC_TM_NCONS;
+constexpr int TM_THREADS = 32 * (1 + TM_NCONS);  // warp 0 producer, warps 1.. consumers
+// every ring slot must belong to ONE consumer (slot s = j mod TM_NST, consumer j mod
+// TM_NCONS), or a consumer could wait on a slot's parity one phase ahead and alias it
+static_assert(SPC_TM_NST % SPC_TM_NCONS == 0, "ring slots must map to one consumer each");
 constexpr int TM_PF = 4;              // stages of token metadata loaded ahead by the producer
 constexpr int TM_NREQ = TM_RPS / 4;   // producer lanes (4 rows per gather4)
 
@@ -279,10 +293,12 @@ __global__ void __launch_bounds__(TM_THREADS, TM_CTAS) attn_tma_kernel(
       for (int i = 0; i < D / 16; ++i) o[a][i][0] = o[a][i][1] = o[a][i][2] = o[a][i][3] = 0.f;
     int s = 0;
     uint32_t ph = 0;
+    const int cw = warp - 1;  // this consumer's stages: j = cw mod TM_NCONS (its own partials)
     for (int j = 0; j < n_chunks; ++j) {
       const bool grp_end = (j == n_chunks - 1) || (rc == cpg - 1);
-      const int nv = min(cnt_g, kbud) - rc * TM_RPS;  // valid rows of this stage (<= 0 or > 32 too)
-      tm_wait(full0 + 8 * s, ph);
+      const bool mine = TM_NCONS == 1 || j % TM_NCONS == cw;
+      const int nv = mine ? min(cnt_g, kbud) - rc * TM_RPS : 0;  // valid rows (<= 0 or > 32 too)
+      if (mine) tm_wait(full0 + 8 * s, ph);
       if (j == 0) tm_trace(1);
       const uint32_t st = ring + (uint32_t)s * SM::STAGE;
 #ifdef SPC_TM_NOMATH  // debug builds only: the load pipeline alone
@@ -376,7 +392,7 @@ __global__ void __launch_bounds__(TM_THREADS, TM_CTAS) attn_tma_kernel(
         }
       }
       __syncwarp();
-      if (lane == 0) tm_arrive(empty0 + 8 * s);  // the stage's smem is consumed
+      if (mine && lane == 0) tm_arrive(empty0 + 8 * s);  // the stage's smem is consumed
       if (++s == TM_NST) {
         s = 0;
         ph ^= 1u;
@@ -391,7 +407,7 @@ __global__ void __launch_bounds__(TM_THREADS, TM_CTAS) attn_tma_kernel(
         }
         const int lr = grp / BG, bg = grp % BG;
         const int b = bg / G, g = bg - (bg / G) * G;
-        const int part = blockIdx.x - (grp * cpg) / cpc;
+        const int part = (blockIdx.x - (grp * cpg) / cpc) * TM_NCONS + cw;
         const size_t head_base = ((size_t)lr * B + b) * Hq + g * ALPHA;
         constexpr int PX = ALPHA == 4 ? 2 : 1;
 #pragma unroll
@@ -463,7 +479,7 @@ __global__ void __launch_bounds__(128) tma_merge_kernel(
   const int gq = wg / ALPHA, j = wg - gq * ALPHA;
   const int BG = B * G, Hq = G * ALPHA;
   const int lr = gq / BG, bg = gq - lr * BG, b = bg / G, g = bg - b * G;
-  const int np = (gq * cpg + cpg - 1) / cpc - (gq * cpg) / cpc + 1;
+  const int np = ((gq * cpg + cpg - 1) / cpc - (gq * cpg) / cpc + 1) * TM_NCONS;
   const size_t h = ((size_t)lr * B + b) * Hq + g * ALPHA + j;  // partial head index
   const size_t oh = ((size_t)(layer_begin + lr) * B + b) * Hq + g * ALPHA + j;
   const float* ml = part_ml + h * segstride * 2;

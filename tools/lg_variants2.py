@@ -20,6 +20,14 @@ VARIANTS = {
     "tm6x2": ["SPC_TM_CTAS=6", "SPC_TM_NST=2"],
     "tmwide": ["SPC_TM_WIDE"],
     "evf": ["SPC_TM_EVICT_FIRST"],
+    "ltnomath": ["SPC_LT_NOMATH"],
+    "tmc2": ["SPC_TM_NCONS=2"],
+    "tmc3": ["SPC_TM_NCONS=3"],
+    "tmc2x6": ["SPC_TM_NCONS=2", "SPC_TM_CTAS=6", "SPC_TM_NST=2"],
+    "tmc3x5": ["SPC_TM_NCONS=3", "SPC_TM_CTAS=5", "SPC_TM_NST=2"],
+    "tmc2x5": ["SPC_TM_NCONS=2", "SPC_TM_CTAS=5", "SPC_TM_NST=2"],
+    "ltb1": ["SPC_LT_BATCH=1"],
+    "ltnc4": ["SPC_LT_NC=4", "SPC_LT_CPR=1"],
     "tmwide3x4": ["SPC_TM_WIDE", "SPC_TM_CTAS=3", "SPC_TM_NST=4"],
     "tmwide6x2": ["SPC_TM_WIDE", "SPC_TM_CTAS=6", "SPC_TM_NST=2"],
 }
