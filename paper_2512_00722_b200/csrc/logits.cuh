@@ -291,7 +291,7 @@ __global__ void __launch_bounds__(256) lg_finalize_kernel(const float* __restric
 #define SPC_LT_CPR 2  // consumer warps per ring: they split every stage's 128 rows
 #endif
 #ifndef SPC_LT_BATCH
-#define SPC_LT_BATCH 2  // tiles per claim of the LOGITS producer
+#define SPC_LT_BATCH 0  // tiles per claim of a producer lane; 0: by the launch (below)
 #endif
 constexpr int LT_NC = SPC_LT_NC;     // consumer warps
 constexpr int LT_CPR = SPC_LT_CPR;   // consumers per ring (= tile_max entries per tile)
@@ -378,7 +378,8 @@ template <int D, int ALPHA>
 __global__ void __launch_bounds__(32 * (LT_NC + 1), 1) logits_tma_kernel(
     const __grid_constant__ CUtensorMap kmap, const uint16_t* __restrict__ q,
     const int32_t* __restrict__ seq_len, int G, int Smax, float scale, int tpr, int ntiles,
-    float* __restrict__ logits, float* __restrict__ tile_max, unsigned* __restrict__ ctr) {
+    float* __restrict__ logits, float* __restrict__ tile_max, unsigned* __restrict__ ctr,
+    int lt_batch, int evict_first) {
   using SM = LtSmem<D, ALPHA>;
   constexpr int NCH = SM::NCH, NST = SM::NST, K = SM::K;
   constexpr int HROWS = LG_TR / LT_CPR;  // rows of a stage per consumer warp
@@ -404,8 +405,8 @@ __global__ void __launch_bounds__(32 * (LT_NC + 1), 1) logits_tma_kernel(
   // wait, and L2 is coherent with any kernel that writes them (the front-end's newest key) --
   // so the HBM stream starts while the previous kernel drains (its last CTAs, its merge)
   if (warp == LT_NC && lane < LT_RINGS) {
-    const int t_lo = ((int)blockIdx.x * LT_RINGS + lane) * SPC_LT_BATCH;
-    for (int tile = t_lo; tile < min(t_lo + SPC_LT_BATCH, ntiles); ++tile) {
+    const int t_lo = ((int)blockIdx.x * LT_RINGS + lane) * lt_batch;
+    for (int tile = t_lo; tile < min(t_lo + lt_batch, ntiles); ++tile) {
       const int bg = tile / tpr, tt = tile - bg * tpr;
 #pragma unroll
       for (int c = 0; c < LtSmem<D, ALPHA>::NCH; ++c)
@@ -425,7 +426,7 @@ __global__ void __launch_bounds__(32 * (LT_NC + 1), 1) logits_tma_kernel(
     // differ (config E: 443 tiles per SM).  The LT_CPR consumers of a ring split each of its
     // stages' rows.
     if (lane < LT_RINGS) {
-      constexpr int LT_BATCH = SPC_LT_BATCH;
+      const int LT_BATCH = lt_batch;
       const int w = lane;
       const int nstatic = (int)gridDim.x * LT_RINGS;
       int n = 0;  // tiles handed to ring w
@@ -450,21 +451,21 @@ __global__ void __launch_bounds__(32 * (LT_NC + 1), 1) logits_tma_kernel(
             const uint32_t fb = full0 + 8 * s;
             if (c == 0) stage_tile[s] = tile;  // published by the arrive below (release)
             tm_expect(fb, LT_STAGE + (c == 0 ? SM::QRAW : 0));
-#ifndef SPC_TM_EVICT_NORMAL  // the keys are streamed once per step: evict them first
-            uint64_t pol;
-            asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-            asm volatile(
-                "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
-                " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(base + s * LT_STAGE),
-                "l"(&kmap), "r"(64 * c), "r"(bg * Smax + tt * LG_TR), "r"(fb), "l"(pol)
-                : "memory");
-#else
-            asm volatile(
-                "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
-                " [%0], [%1, {%2, %3}], [%4];" ::"r"(base + s * LT_STAGE),
-                "l"(&kmap), "r"(64 * c), "r"(bg * Smax + tt * LG_TR), "r"(fb)
-                : "memory");
-#endif
+            if (evict_first) {  // a short stream inside a step: keep the step's hot set in L2
+              uint64_t pol;
+              asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+              asm volatile(
+                  "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+                  " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(base + s * LT_STAGE),
+                  "l"(&kmap), "r"(64 * c), "r"(bg * Smax + tt * LG_TR), "r"(fb), "l"(pol)
+                  : "memory");
+            } else {
+              asm volatile(
+                  "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+                  " [%0], [%1, {%2, %3}], [%4];" ::"r"(base + s * LT_STAGE),
+                  "l"(&kmap), "r"(64 * c), "r"(bg * Smax + tt * LG_TR), "r"(fb)
+                  : "memory");
+            }
             if (c == 0) {
               const int b = bg / G, g = bg - b * G;
               asm volatile(

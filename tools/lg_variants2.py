@@ -27,6 +27,8 @@ VARIANTS = {
     "tmc3x5": ["SPC_TM_NCONS=3", "SPC_TM_CTAS=5", "SPC_TM_NST=2"],
     "tmc2x5": ["SPC_TM_NCONS=2", "SPC_TM_CTAS=5", "SPC_TM_NST=2"],
     "ltb1": ["SPC_LT_BATCH=1"],
+    "ltb2": ["SPC_LT_BATCH=2"],
+    "evn": ["SPC_TM_EVICT_NORMAL"],
     "ltnc4": ["SPC_LT_NC=4", "SPC_LT_CPR=1"],
     "tmwide3x4": ["SPC_TM_WIDE", "SPC_TM_CTAS=3", "SPC_TM_NST=4"],
     "tmwide6x2": ["SPC_TM_WIDE", "SPC_TM_CTAS=6", "SPC_TM_NST=2"],
