@@ -1,5 +1,6 @@
-"""One eager decode step of config A and of a 2K-context config-B shape through libspc, for
-compute-sanitizer (tools only): python tools/sanitize_step.py [A|B2K|all]."""
+"""Two eager decode steps of config A, of a 2K-context config-B shape (k = S: no cut) and of an
+8K-context one (k = 1024: a cut on every row) through libspc, for compute-sanitizer (tools
+only): python tools/sanitize_step.py [A|B2K|B8K|all]."""
 import os
 import sys
 
@@ -12,7 +13,8 @@ from paper_2512_00722_b200.pipeline import DecodeStep  # noqa: E402
 which = sys.argv[1] if len(sys.argv) > 1 else "all"
 dev = torch.device("cuda")
 cases = {"A": dict(B=1, G=1, Hq=4, D=64, S=4096, L=1, k=256),
-         "B2K": dict(B=1, G=8, Hq=32, D=128, S=2048, L=32, k=2048)}
+         "B2K": dict(B=1, G=8, Hq=32, D=128, S=2048, L=32, k=2048),
+         "B8K": dict(B=1, G=8, Hq=32, D=128, S=8192, L=4, k=1024)}  # a cut on every row
 for name, c in cases.items():
     if which not in ("all", name):
         continue
