@@ -28,6 +28,8 @@ VARIANTS = {
     "tmc2x5": ["SPC_TM_NCONS=2", "SPC_TM_CTAS=5", "SPC_TM_NST=2"],
     "ltb1": ["SPC_LT_BATCH=1"],
     "ltb2": ["SPC_LT_BATCH=2"],
+    "ltnocvt": ["SPC_LT_EXP_NOCVT"],
+    "lt16": ["SPC_LT_NC=16", "SPC_LT_CPR=4"],
     "evn": ["SPC_TM_EVICT_NORMAL"],
     "ltnc4": ["SPC_LT_NC=4", "SPC_LT_CPR=1"],
     "tmwide3x4": ["SPC_TM_WIDE", "SPC_TM_CTAS=3", "SPC_TM_NST=4"],
