@@ -105,7 +105,10 @@ uint64_t spc_launch_count(void);
  * head_max    [B][Hq]        f32       out (LOGITS) / in (NORM, GROUP)
  * head_sumfix [B][Hq]        int64     out (NORM)   / in (GROUP)
  * group_score [B][G][Smax]   f32       out (GROUP); may be NULL otherwise
- * ws          >= spc_score_workspace(B, Hq, Smax) bytes of device scratch
+ * ws          >= spc_score_workspace(B, Hq, Smax) bytes of device scratch, zero-filled
+ *             once before first use (LOGITS' tile-claim counter and NORM's tickets
+ *             start at 0; every launch leaves them 0); not shared by calls executing at
+ *             the same time.  A launch that failed mid-way leaves it undefined: zero it again.
  *   SPC_SCORE_BATCH (with GROUP): batch-level retrieval
  *                     (Fig. 5(a)): one token set per
  *                     request from the sum over ALL query heads of their weights,
@@ -301,7 +304,9 @@ int spc_gather_kv_strided(int dtype, const void* const* k_src, const void* const
  * k_layers/v_layers: DEVICE arrays of L pointers (device or mapped host).
  * q [L][B][Hq][D] (dtype), out [L][B][Hq][D] f32, lse [L][B][Hq] f32 or NULL.
  * A (b,g) with count 0 yields out = 0, lse = -inf.
- * ws >= spc_attn_workspace(L, B, Hq, D, k) bytes.
+ * ws >= spc_attn_workspace(L, B, Hq, D, k) bytes, zero-filled once before first use (the
+ * per-group merge tickets start at 0; every launch leaves them 0); not shared by calls
+ * executing at the same time.  A launch that failed mid-way leaves it undefined.
  * Supported: dtype SPC_BF16 or SPC_F32; D in {64, 128}; alpha in {1,2,4,8}.
  * ---------------------------------------------------------------------- */
 enum { SPC_KV_INDEXED = 0, SPC_KV_SLOTS = 1 };
