@@ -29,7 +29,7 @@ VARIANTS = {
     "ltb1": ["SPC_LT_BATCH=1"],
     "ltb2": ["SPC_LT_BATCH=2"],
     "ltnocvt": ["SPC_LT_EXP_NOCVT"],
-    "lt16": ["SPC_LT_NC=16", "SPC_LT_CPR=4"],
+    "sel1024": ["SPC_SEL_ST=1024"],
     "evn": ["SPC_TM_EVICT_NORMAL"],
     "ltnc4": ["SPC_LT_NC=4", "SPC_LT_CPR=1"],
     "tmwide3x4": ["SPC_TM_WIDE", "SPC_TM_CTAS=3", "SPC_TM_NST=4"],
