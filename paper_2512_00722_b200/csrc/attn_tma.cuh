@@ -52,7 +52,10 @@ constexpr int TM_THREADS = 32 * (1 + TM_NCONS);  // warp 0 producer, warps 1.. c
 // every ring slot must belong to ONE consumer (slot s = j mod TM_NST, consumer j mod
 // TM_NCONS), or a consumer could wait on a slot's parity one phase ahead and alias it
 static_assert(SPC_TM_NST % SPC_TM_NCONS == 0, "ring slots must map to one consumer each");
-constexpr int TM_PF = 4;              // stages of token metadata loaded ahead by the producer
+#ifndef SPC_TM_PF
+#define SPC_TM_PF 4
+#endif
+constexpr int TM_PF = SPC_TM_PF;      // stages of token metadata loaded ahead by the producer
 constexpr int TM_NREQ = TM_RPS / 4;   // producer lanes (4 rows per gather4)
 
 template <int D>

@@ -30,6 +30,9 @@ VARIANTS = {
     "ltb2": ["SPC_LT_BATCH=2"],
     "ltnocvt": ["SPC_LT_EXP_NOCVT"],
     "sel1024": ["SPC_SEL_ST=1024"],
+    "pf2": ["SPC_TM_PF=2"],
+    "pf6": ["SPC_TM_PF=6"],
+    "pf8": ["SPC_TM_PF=8"],
     "evn": ["SPC_TM_EVICT_NORMAL"],
     "ltnc4": ["SPC_LT_NC=4", "SPC_LT_CPR=1"],
     "tmwide3x4": ["SPC_TM_WIDE", "SPC_TM_CTAS=3", "SPC_TM_NST=4"],
