@@ -30,6 +30,7 @@ VARIANTS = {
     "ltb2": ["SPC_LT_BATCH=2"],
     "ltnocvt": ["SPC_LT_EXP_NOCVT"],
     "sel1024": ["SPC_SEL_ST=1024"],
+    "fixint": ["SPC_FIXPOINT_INT"],
     "pf2": ["SPC_TM_PF=2"],
     "pf6": ["SPC_TM_PF=6"],
     "pf8": ["SPC_TM_PF=8"],
