@@ -176,6 +176,18 @@ struct DenseKey {
   __device__ unsigned long long operator()(int p) const {
     return row_key(row, p, len, force, stride, offset);
   }
+  // the raw quad at p (vec rows) and its keys: scans load several quads before using any
+  __device__ __forceinline__ float4 raw(int p) const {
+    return __ldg(reinterpret_cast<const float4*>(row + p));
+  }
+  __device__ __forceinline__ void keys(const float4& v, int p, unsigned long long (&x)[4]) const {
+    const float vs[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const uint32_t vb = (force && p + i == len - 1) ? 0x7F800000u : __float_as_uint(vs[i]);
+      x[i] = composite(vb, (p + i) * stride + offset);
+    }
+  }
   // keys of positions p .. p+3 (p a multiple of 4; positions >= len are never used)
   __device__ __forceinline__ void quad(int p, unsigned long long (&x)[4]) const {
     if (vec) {
@@ -192,6 +204,38 @@ struct DenseKey {
     }
   }
 };
+
+// f(p, x) for the quads p = a, a + st, a + 2 st, ... < b (x = keys of p .. p+3): SCAN_UNR
+// quads' loads are issued before the first is used -- a row pass issued one dependent
+// float4 load per quad and waited on each (config E's 1M-token rows: 32 quads per thread,
+// ncu: 42% of the top-k's stall samples on those loads)
+constexpr int SCAN_UNR = 4;
+template <class KeyFn, class F>
+__device__ __forceinline__ void scan_quads(const KeyFn& key, int a, int b, int st, F&& f) {
+  if (key.vec) {
+    for (int p0 = a; p0 < b; p0 += st * SCAN_UNR) {
+      float4 v[SCAN_UNR];
+#pragma unroll
+      for (int u = 0; u < SCAN_UNR; ++u)
+        if (p0 + u * st < b) v[u] = key.raw(p0 + u * st);
+#pragma unroll
+      for (int u = 0; u < SCAN_UNR; ++u) {
+        const int p = p0 + u * st;
+        if (p < b) {
+          unsigned long long x[4];
+          key.keys(v[u], p, x);
+          f(p, x);
+        }
+      }
+    }
+  } else {
+    for (int p = a; p < b; p += st) {
+      unsigned long long x[4];
+      key.quad(p, x);
+      f(p, x);
+    }
+  }
+}
 
 struct ClSmem {
   SelSmem sel;               // CTA 0: gathered candidates + refinement scratch
@@ -218,13 +262,11 @@ __device__ void cluster_select(ClSmem& s, cg::cluster_group& cl, const KeyFn& ke
     // ---- 1. top-11-bit histogram, reduced over the cluster
     for (int i = tid; i < NBIN0; i += SEL_THREADS) s.hist[i] = 0;
     __syncthreads();
-    for (int p = s0 + 4 * tid; p < s1; p += 4 * SEL_THREADS) {
-      unsigned long long x[4];
-      key.quad(p, x);
+    scan_quads(key, s0 + 4 * tid, s1, 4 * SEL_THREADS, [&](int p, const unsigned long long(&x)[4]) {
 #pragma unroll
       for (int i = 0; i < 4; ++i)
         if (p + i < s1) atomicAdd(&s.hist[x[i] >> 53], 1u);
-    }
+    });
     cl.sync();
     for (int i = tid; i < NBIN0; i += SEL_THREADS) {
       unsigned t = 0;
@@ -245,14 +287,12 @@ __device__ void cluster_select(ClSmem& s, cg::cluster_group& cl, const KeyFn& ke
       const unsigned mask = (1u << db) - 1;
       for (int i = tid; i < 256; i += SEL_THREADS) s.hist[i] = 0;
       __syncthreads();
-      for (int p = s0 + 4 * tid; p < s1; p += 4 * SEL_THREADS) {
-        unsigned long long x[4];
-        key.quad(p, x);
+      scan_quads(key, s0 + 4 * tid, s1, 4 * SEL_THREADS, [&](int p, const unsigned long long(&x)[4]) {
 #pragma unroll
         for (int i = 0; i < 4; ++i)
           if (p + i < s1 && prefix_match(x[i], prefix, bits))
             atomicAdd(&s.hist[(unsigned)(x[i] >> shift) & mask], 1u);
-      }
+      });
       cl.sync();
       for (int i = tid; i < 256; i += SEL_THREADS) {
         unsigned t = 0;
@@ -274,20 +314,32 @@ __device__ void cluster_select(ClSmem& s, cg::cluster_group& cl, const KeyFn& ke
     cl.sync();
     int* n0 = cl.map_shared_rank(&s.sel.n[0], 0);
     unsigned long long* c0 = cl.map_shared_rank(&s.sel.cand[0][0], 0);
-    for (int p0 = s0; p0 < s1; p0 += 4 * SEL_THREADS) {
-      const int p = p0 + 4 * tid;
-      unsigned long long x[4] = {0, 0, 0, 0};
-      if (p < s1) key.quad(p, x);
+    for (int p00 = s0; p00 < s1; p00 += 4 * SEL_THREADS * SCAN_UNR) {  // warp-uniform trips
+      float4 v[SCAN_UNR];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const bool hit = p + i < s1 && prefix_match(x[i], prefix, bits);
-        const unsigned m = __ballot_sync(0xffffffffu, hit);
-        if (!m) continue;
-        const int leader = __ffs(m) - 1;
-        int base = 0;
-        if (lane == leader) base = atomicAdd(n0, __popc(m));
-        base = __shfl_sync(0xffffffffu, base, leader);
-        if (hit) c0[base + __popc(m & ((1u << lane) - 1))] = x[i];
+      for (int u = 0; u < SCAN_UNR; ++u) {  // every quad's load in flight first
+        const int p = p00 + u * 4 * SEL_THREADS + 4 * tid;
+        if (key.vec && p < s1) v[u] = key.raw(p);
+      }
+#pragma unroll
+      for (int u = 0; u < SCAN_UNR; ++u) {
+        const int p = p00 + u * 4 * SEL_THREADS + 4 * tid;
+        unsigned long long x[4] = {0, 0, 0, 0};
+        if (p < s1) {
+          if (key.vec) key.keys(v[u], p, x);
+          else key.quad(p, x);
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const bool hit = p + i < s1 && prefix_match(x[i], prefix, bits);
+          const unsigned m = __ballot_sync(0xffffffffu, hit);
+          if (!m) continue;
+          const int leader = __ffs(m) - 1;
+          int base = 0;
+          if (lane == leader) base = atomicAdd(n0, __popc(m));
+          base = __shfl_sync(0xffffffffu, base, leader);
+          if (hit) c0[base + __popc(m & ((1u << lane) - 1))] = x[i];
+        }
       }
     }
     cl.sync();
@@ -305,12 +357,10 @@ __device__ void cluster_select(ClSmem& s, cg::cluster_group& cl, const KeyFn& ke
   const int pt = ((seg + SEL_THREADS - 1) / SEL_THREADS + 3) & ~3;  // multiple of 4
   const int q0 = min(s1, s0 + tid * pt), q1 = min(s1, q0 + pt);
   int cnt = 0;
-  for (int p = q0; p < q1; p += 4) {
-    unsigned long long x[4];
-    key.quad(p, x);
+  scan_quads(key, q0, q1, 4, [&](int p, const unsigned long long(&x)[4]) {
 #pragma unroll
     for (int i = 0; i < 4; ++i) cnt += (p + i < q1 && x[i] >= T);
-  }
+  });
   int pos = block_excl_scan(cnt, s.sel.wsum, &s.total);
   __syncthreads();
   if (tid < CL) cl.map_shared_rank(s.counts, tid)[rank] = s.total;
@@ -324,9 +374,7 @@ __device__ void cluster_select(ClSmem& s, cg::cluster_group& cl, const KeyFn& ke
   *my_base = base;
   *my_count = s.counts[rank];
   pos += base;
-  for (int p = q0; p < q1; p += 4) {
-    unsigned long long x[4];
-    key.quad(p, x);
+  scan_quads(key, q0, q1, 4, [&](int p, const unsigned long long(&x)[4]) {
 #pragma unroll
     for (int i = 0; i < 4; ++i)
       if (p + i < q1 && x[i] >= T) {
@@ -334,7 +382,7 @@ __device__ void cluster_select(ClSmem& s, cg::cluster_group& cl, const KeyFn& ke
         if (ov) ov[pos] = __uint_as_float((uint32_t)(x[i] >> 32));
         ++pos;
       }
-  }
+  });
   if (rank == CL - 1)
     for (int i = all + tid; i < k; i += SEL_THREADS) {
       oi[i] = -1;
