@@ -117,6 +117,33 @@ def test_step_host_matches_device_steps():
         assert torch.equal(out_h, want[s].cpu()), s
 
 
+@pytest.mark.parametrize("cfg", ["A", "B"])
+def test_chained_step_graphs_equal_single_step_graphs(cfg):
+    """bench.py times the steps as CUDA graphs of consecutive steps (capture_sequence with
+    bounds): the chained graphs give bit for bit the selections, attention outputs and
+    lse of one graph per step, over 6 steps with graph boundaries inside the sequence."""
+    n = 6
+    c, st, kr, kc, vc, qr, ql = build(cfg, synth.BASE_SEED + 21, steps=n)
+    items = [(0, qr[i], ql[i]) for i in range(n)]
+    st.step(qr[0], ql[0])  # eager warm-up (kernel attributes)
+    runs = []
+    for bounds in ([(i, i + 1) for i in range(n)], [(0, 1), (1, 5), (5, 6)]):
+        graphs = st.capture_sequence(items, bounds=bounds)
+        st.reset_state()
+        res = []
+        for gi, (a, b) in enumerate(bounds):
+            graphs[gi].replay()
+            torch.cuda.synchronize()
+            p = (b - 1) % 2  # the parity of the chunk's last step
+            res.append((st.idx[p].clone(), st.cnt[p].clone(), st.outs[p].clone(), st.lses[p].clone()))
+        runs.append(res)
+    # compare after steps 1, 5 and 6 (the ends of the chained chunks)
+    single, chained = runs
+    for si, ci in ((0, 0), (4, 1), (5, 2)):
+        for x, y in zip(single[si], chained[ci]):
+            assert torch.equal(x, y), (cfg, si)
+
+
 def test_step_with_frontend_equals_frontend_then_step():
     """DecodeStep.set_frontend: the step from token ids (spc_rethead_qk writes the query and
     the newest key row, then the usual step) is bit-identical to calling spc_rethead_qk by
