@@ -211,17 +211,6 @@ __global__ void __launch_bounds__(TM_THREADS, TM_CTAS) attn_tma_kernel(
           else tm_arrive(fb);  // nothing valid in this stage: complete the phase without bytes
         }
         __syncwarp();
-#ifdef SPC_TM_WIDE
-        {  // every lane issues ONE gather4: lane = (kv, half, row quad)
-          const int rq = lane % TM_NREQ, hk = lane / TM_NREQ;  // hk = kv * NH + h
-          const int4 rr = make_int4(__shfl_sync(0xffffffffu, r.x, rq), __shfl_sync(0xffffffffu, r.y, rq),
-                                    __shfl_sync(0xffffffffu, r.z, rq), __shfl_sync(0xffffffffu, r.w, rq));
-          if (any && hk < 2 * NH) {
-            const uint32_t st = ring + (uint32_t)s * SM::STAGE + (uint32_t)rq * 512u + hk * SM::HALF;
-            tm_gather4(st, hk < NH ? km : vm, fb, 64 * (hk % NH), rr.x, rr.y, rr.z, rr.w);
-          }
-        }
-#else
         if (any && lane < TM_NREQ) {
           const uint32_t st = ring + (uint32_t)s * SM::STAGE + (uint32_t)lane * 512u;
 #pragma unroll
@@ -230,7 +219,6 @@ __global__ void __launch_bounds__(TM_THREADS, TM_CTAS) attn_tma_kernel(
             tm_gather4(st + (NH + h) * SM::HALF, vm, fb, 64 * h, r.x, r.y, r.z, r.w);
           }
         }
-#endif
         if (++rc == cpg) {
           rc = 0;
           ++grp;

@@ -18,7 +18,6 @@ VARIANTS = {
     "tmnomath": ["SPC_TM_NOMATH"],
     "tm3x4nm": ["SPC_TM_CTAS=3", "SPC_TM_NST=4", "SPC_TM_NOMATH"],
     "tm6x2": ["SPC_TM_CTAS=6", "SPC_TM_NST=2"],
-    "tmwide": ["SPC_TM_WIDE"],
     "evf": ["SPC_TM_EVICT_FIRST"],
     "ltnomath": ["SPC_LT_NOMATH"],
     "tmc2": ["SPC_TM_NCONS=2"],
@@ -37,8 +36,6 @@ VARIANTS = {
     "pf8": ["SPC_TM_PF=8"],
     "evn": ["SPC_TM_EVICT_NORMAL"],
     "ltnc4": ["SPC_LT_NC=4", "SPC_LT_CPR=1"],
-    "tmwide3x4": ["SPC_TM_WIDE", "SPC_TM_CTAS=3", "SPC_TM_NST=4"],
-    "tmwide6x2": ["SPC_TM_WIDE", "SPC_TM_CTAS=6", "SPC_TM_NST=2"],
 }
 for name in (sys.argv[1:] or VARIANTS):
     out = os.path.join(os.path.dirname(os.path.abspath(__file__)), f"libspc_{name}.so")
