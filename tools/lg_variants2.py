@@ -31,6 +31,7 @@ VARIANTS = {
     "sel1024": ["SPC_SEL_ST=1024"],
     "fixint": ["SPC_FIXPOINT_INT"],
     "vlsu": ["SPC_TM_VLSU=1"],
+    "selearly": ["SPC_SEL_EARLY_LOADS"],
     "pf2": ["SPC_TM_PF=2"],
     "pf6": ["SPC_TM_PF=6"],
     "pf8": ["SPC_TM_PF=8"],
