@@ -117,6 +117,45 @@ def dry_run(args):
 GRAPH_STEPS = 16  # decode steps per CUDA graph in the timed loops
 
 
+def kernel_timeline(replay, names):
+    """Per-kernel time inside a replayed multi-step graph, from CUPTI kernel records
+    (torch.profiler; not timed): the kernels of a step run as a chain (each launched early
+    by PDL, starting its work when its predecessor ends), so a kernel's share is its end
+    minus its predecessor's end; averaged over the steady steps.  names: substring -> label
+    in chain order.  Returns {label: us} or None."""
+    import warnings
+
+    import torch
+    try:
+        from torch.profiler import ProfilerActivity, profile
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore")
+            with profile(activities=[ProfilerActivity.CUDA]) as prof:
+                replay()
+                torch.cuda.synchronize()
+        ks = sorted((e.time_range.start, e.time_range.end, e.name) for e in prof.events()
+                    if e.device_type == torch.autograd.DeviceType.CUDA)
+        lab = []
+        for a, b, n in ks:
+            for key, label in names:
+                if key in n:
+                    lab.append((a, b, label))
+                    break
+        per = len(names)
+        steps = len(lab) // per
+        if steps < 4:
+            return None
+        acc = {label: 0.0 for _, label in names}
+        for st in range(1, steps - 1):  # steady steps: a predecessor in the same graph
+            for i in range(per):
+                j = st * per + i
+                acc[lab[j][2]] += (lab[j][1] - lab[j - 1][1]) / (steps - 2)
+        return {k: round(v, 2) for k, v in acc.items()}
+    except Exception as e:  # noqa: BLE001 -- informational only
+        print(f"# kernel timeline unavailable: {type(e).__name__}: {e}", file=sys.stderr)
+        return None
+
+
 def warm_graphs(st, graphs):
     """Replay every captured step graph once, untimed, then reset the rolling selection
     state: a CUDA graph's first launch carries a one-time upload cost that is not part of a
@@ -396,6 +435,12 @@ def bench_ours(args, attach=None):
     clocks = sampler.stop()
     step_ms = [ev[j].elapsed_time(ev[j + 1]) / (bounds[ci][1] - bounds[ci][0])
                for j, ci in enumerate(timed) for _ in range(bounds[ci][1] - bounds[ci][0])]
+    # per-kernel times inside one replayed chunk (after the timed region, untimed)
+    in_graph = None
+    if st.fused and not st.one_launch and st.desc is not None:
+        in_graph = kernel_timeline(lambda: run_chunk(timed[0]), [
+            ("logits_tma", "logits"), ("lg_finalize", "finalize"), ("select_kernel", "select"),
+            ("attn_tma", "attention"), ("tma_merge", "merge")])
     t_ms = ev[0].elapsed_time(ev[-1])
     if pg:
         t = torch.tensor([t_ms], dtype=torch.float64, device=dev)
@@ -583,6 +628,9 @@ def bench_ours(args, attach=None):
                        "algorithmic_bytes_per_step": step_bytes,
                        "step_us_p50": statistics.median(step_ms) * 1e3,
                        "hbm_roofline_frac_step": step_bytes / (ms_per_step * 1e-3) / 1e9 / peak,
+                       "phase_us_in_graph": in_graph,
+                       "phase_us_in_graph_how": ("CUPTI kernel records of one replayed chunk: "
+                                                 "a kernel's end minus its predecessor's end"),
                        "phase_us": {p: round(acc[p] * 1e3, 2) for p in phases},
                        "phase_us_how": "eager, events between the phases (no PDL overlap)",
                        "attn_us_back_to_back": round(attn_b2b_ms * 1e3, 2),
