@@ -73,6 +73,24 @@ __global__ void __launch_bounds__(RH_WARPS * 32, RH_CPS) rethead_kernel(
     const float* __restrict__ inv_freq, float mscale, const int32_t* __restrict__ pos, int B,
     int Hq, int G, int D, int Smax, uint16_t* __restrict__ q_out, uint16_t* __restrict__ kr,
     int32_t* __restrict__ seq_len_out, uint16_t* __restrict__ x_out) {
+  // the weights are static: before the PDL wait and the RMSNorm prologue, every warp asks for
+  // its row pairs in L2 (a hint: the loads below read them through L2), so the 40 MiB stream
+  // runs while the embedding rows are normalised
+  {
+    const int w = (int)threadIdx.x >> 5;
+    const int half_ = D / 2, npairs_ = (Hq + G) * half_;
+    if ((threadIdx.x & 31) == 0)
+      for (int p = blockIdx.x * RH_WARPS + w; p < npairs_; p += gridDim.x * RH_WARPS) {
+        const int hh = p / half_, i = p - hh * half_;
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(w_qk + ((size_t)hh * D + i) * H),
+                     "r"(H * 2)
+                     : "memory");
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(
+                         w_qk + ((size_t)hh * D + i + half_) * H),
+                     "r"(H * 2)
+                     : "memory");
+      }
+  }
   spc_pdl_entry();
   extern __shared__ __align__(16) uint8_t rh_smem[];
   uint16_t* xs = reinterpret_cast<uint16_t*>(rh_smem);  // [B][H] normalised inputs
