@@ -5,7 +5,7 @@
 
 One "step" = spc_score (LOGITS) + spc_select (NORM, GROUP, top-k, diff) +
 spc_sparse_decode_attn over all L layers, on one batch of synthetic input,
-inputs resident in HBM (each step's queries are read in place), CUDA graphs of up to 16
+inputs resident in HBM (each step's queries are read in place), CUDA graphs of up to 32
 consecutive steps (a device decode loop).  No L2 flush: three
 address-distinct copies of the inputs (each > L2) are rotated step by step; the steps are
 timed with CUDA events on the launching stream.
@@ -114,7 +114,7 @@ def dry_run(args):
         pg.destroy_process_group()
 
 
-GRAPH_STEPS = 16  # decode steps per CUDA graph in the timed loops
+GRAPH_STEPS = 32  # decode steps per CUDA graph in the timed loops
 
 
 def kernel_timeline(replay, names):
