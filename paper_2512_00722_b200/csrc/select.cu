@@ -84,6 +84,7 @@ struct SelSm {
   long long part[SCL][8];                 // NORM partial sums pushed by every rank
   long long wred[ST / 32][8];             // NORM warp partials
   long long ntot[8];                      // this CTA's NORM partials
+  float rj[8];                            // 1 / l per head of the group
   unsigned long long stats[SCL];          // per rank: above | above&prev | bucket | bucket&prev
   unsigned long long my_stats;
   unsigned long long wsc[ST / 32];        // scan scratch
@@ -345,15 +346,20 @@ __global__ void SPC_SEL_BOUNDS select_kernel(
   sel_mark(1);
 
   // ---- GROUP (O4..O6) + pass-0 histogram
+  // F and r = 1 / l per head once per CTA (thread j), then broadcast through shared memory
+  if (tid < ALPHA) {
+    long long F = 0;
+#pragma unroll
+    for (int q = 0; q < SCL; ++q) F += s.part[q][tid];
+    if (rank == 0) head_sumfix[(size_t)b * Hq + g * ALPHA + tid] = F;
+    s.rj[tid] = __fdiv_rn(1.0f, __fmul_rn(__ll2float_rn(F), 9.094947017729282379150390625e-13f));
+  }
+  __syncthreads();
   float r[ALPHA];
   float gmax = 0.0f;
 #pragma unroll
   for (int j = 0; j < ALPHA; ++j) {
-    long long F = 0;
-#pragma unroll
-    for (int q = 0; q < SCL; ++q) F += s.part[q][j];
-    if (rank == 0 && tid == 0) head_sumfix[(size_t)b * Hq + g * ALPHA + j] = F;
-    r[j] = __fdiv_rn(1.0f, __fmul_rn(__ll2float_rn(F), 9.094947017729282379150390625e-13f));
+    r[j] = s.rj[j];
     gmax = fmaxf(gmax, r[j]);
   }
   const int top = (int)(__float_as_uint(gmax) >> W0_SHIFT);
