@@ -1,6 +1,6 @@
 # round-2 final GPU pass: tests, smoke, bench lines for every config, ncu launch list + full capture
 set -x
-TAG=${TAG:-r02c}
+TAG=${TAG:-r02d}
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/${TAG}_build.log 2>&1
 timeout 900 python -m pytest tests -q -m gpu > gpurun_out/${TAG}_pytest.log 2>&1; tail -2 gpurun_out/${TAG}_pytest.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${TAG}_smoke.log 2>&1; tail -1 gpurun_out/${TAG}_smoke.log
